@@ -1,0 +1,268 @@
+"""Thin Python API over the C ABI (include/jf.h) — argument marshalling only.
+
+Names follow jf.h: curve_fit (jf_curve_fit), jpass (jf_pass), residual_pass
+(jf_residual_pass), pass_device (jf_pass_device), trust_region_step
+(jf_trust_region_step), Comm (jf_comm_*).  Arrays may be numpy (host
+memory: the library copies them to HBM) or CUDA torch tensors (device
+memory: read in place).  No computation happens here.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib as L
+
+
+class JFError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        self.code = code
+        msg = L.load().jf_strerror(code).decode()
+        super().__init__(f"{where}: {msg} ({code})")
+
+
+def _model_id(model) -> int:
+    if isinstance(model, str):
+        return L.MODEL_IDS[model]
+    return int(model)
+
+
+def nparams(model) -> int:
+    return L.load().jf_model_nparams(_model_id(model))
+
+
+def _dptr(a: np.ndarray | None):
+    if a is None:
+        return None
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _is_cuda(a) -> bool:
+    return hasattr(a, "is_cuda") and bool(a.is_cuda)
+
+
+def _as_host(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+class _Data:
+    """Holds the (y, z, sigma) buffers alive and resolves their pointers."""
+
+    def __init__(self, y, z, sigma):
+        self.on_device = _is_cuda(z)
+        if self.on_device:
+            import torch
+            for t in (y, sigma):
+                if t is not None and not _is_cuda(t):
+                    raise ValueError("z is a CUDA tensor: y and sigma must be CUDA tensors too")
+            self.z = z.contiguous().to(torch.float64)
+            self.y = None if y is None else y.contiguous().to(torch.float64)
+            self.sigma = None if sigma is None else sigma.contiguous().to(torch.float64)
+            self.zp = self.z.data_ptr()
+            self.yp = None if self.y is None else self.y.data_ptr()
+            self.sp = None if self.sigma is None else self.sigma.data_ptr()
+            self.m = int(self.z.numel())
+        else:
+            self.z = _as_host(z)
+            self.y = None if y is None else _as_host(y)
+            self.sigma = None if sigma is None else _as_host(sigma)
+            self.zp = self.z.ctypes.data
+            self.yp = None if self.y is None else self.y.ctypes.data
+            self.sp = None if self.sigma is None else self.sigma.ctypes.data
+            self.m = int(self.z.size)
+
+
+def make_opts(*, grid=None, t0=0.0, dt=1.0, index0=0, sigma_ptr=None, on_device=False, device=0,
+              stream=None, ftol=1e-8, xtol=1e-8, gtol=1e-8, max_nfev=0, x_scale="jac",
+              policy="speculative", use_graph=True, comm=None, m_global=0, solver="gram"):
+    lib = L.load()
+    o = L.jf_opts()
+    lib.jf_opts_default(C.byref(o))
+    o.ftol, o.xtol, o.gtol = ftol, xtol, gtol
+    o.max_nfev = int(max_nfev or 0)
+    keep = []
+    if isinstance(x_scale, str):
+        o.x_scale_mode = {"jac": L.XSCALE_JAC, "ones": L.XSCALE_ONES}[x_scale]
+    else:
+        xs = _as_host(x_scale)
+        keep.append(xs)
+        o.x_scale_mode = L.XSCALE_ARRAY
+        o.x_scale = _dptr(xs)
+    o.policy = {"speculative": L.POLICY_SPECULATIVE, "conservative": L.POLICY_CONSERVATIVE}[policy]
+    o.solver = {"auto": L.SOLVE_AUTO, "gram": L.SOLVE_GRAM, "tsqr": L.SOLVE_TSQR}[solver]
+    if grid is not None:
+        o.grid_w, o.grid_h = int(grid[0]), int(grid[1])
+        o.grid_row0 = int(grid[2]) if len(grid) > 2 else 0
+    o.t0, o.dt, o.index0 = float(t0), float(dt), int(index0)
+    o.sigma = sigma_ptr
+    o.device = int(device)
+    o.inputs_on_device = 1 if on_device else 0
+    if stream is not None:
+        o.stream = stream if isinstance(stream, int) else int(getattr(stream, "cuda_stream", stream))
+    o.use_graph = 1 if use_graph else 0
+    if comm is not None:
+        o.comm = comm.handle
+        o.m_global = int(m_global)
+    return o, keep
+
+
+@dataclass
+class FitResult:
+    x: np.ndarray
+    cost: float
+    optimality: float
+    grad: np.ndarray
+    gram: np.ndarray
+    status: int
+    nfev: int
+    njev: int
+    nit: int
+    active_mask: np.ndarray
+    kernel_launches: int
+    t_upload_s: float
+    t_solve_s: float
+    trace: np.ndarray = field(default_factory=lambda: np.zeros((0, L.JF_TRACE_FIELDS)))
+
+
+def curve_fit(model, z, y=None, *, grid=None, p0=None, lb=None, ub=None, sigma=None, trace_cap=0,
+              **kw) -> FitResult:
+    """jf_curve_fit: minimise 1/2 sum (h(y_i; x) - z_i)^2 by TRF."""
+    lib = L.load()
+    mid = _model_id(model)
+    n = lib.jf_model_nparams(mid)
+    data = _Data(y, z, sigma)
+    opts, keep = make_opts(grid=grid, sigma_ptr=data.sp, on_device=data.on_device, **kw)
+    tr = None
+    if trace_cap > 0:
+        tr = np.zeros((trace_cap, L.JF_TRACE_FIELDS))
+        opts.trace_cap = trace_cap
+        opts.trace = _dptr(tr)
+    p0a = None if p0 is None else _as_host(p0)
+    lba = None if lb is None else _as_host(lb)
+    uba = None if ub is None else _as_host(ub)
+    res = L.jf_result()
+    rc = lib.jf_curve_fit(mid, data.yp, data.zp, data.m, _dptr(p0a), n, _dptr(lba), _dptr(uba),
+                          C.byref(opts), C.byref(res))
+    if rc < 0:
+        raise JFError(rc, "jf_curve_fit")
+    out = FitResult(
+        x=np.array(res.x[:n]), cost=res.cost, optimality=res.optimality, grad=np.array(res.grad[:n]),
+        gram=np.array(res.gram[: n * n]).reshape(n, n), status=res.status, nfev=res.nfev, njev=res.njev,
+        nit=res.nit, active_mask=np.array(res.active_mask[:n], dtype=np.int64),
+        kernel_launches=res.kernel_launches, t_upload_s=res.t_upload_s, t_solve_s=res.t_solve_s)
+    if tr is not None:
+        out.trace = tr[: res.trace_len].copy()
+    return out
+
+
+def jpass(model, z, x, y=None, *, grid=None, sigma=None, **kw):
+    """jf_pass: (cost, g, G, nonfinite) at x (Eq. 2, 4, 5)."""
+    lib = L.load()
+    mid = _model_id(model)
+    n = lib.jf_model_nparams(mid)
+    data = _Data(y, z, sigma)
+    opts, keep = make_opts(grid=grid, sigma_ptr=data.sp, on_device=data.on_device, **kw)
+    xa = _as_host(x)
+    cost = C.c_double()
+    g = np.zeros(n)
+    G = np.zeros(n * n)
+    bad = C.c_int32()
+    rc = lib.jf_pass(mid, data.yp, data.zp, data.m, _dptr(xa), n, C.byref(opts), C.byref(cost), _dptr(g),
+                     _dptr(G), C.byref(bad))
+    if rc < 0:
+        raise JFError(rc, "jf_pass")
+    return cost.value, g, G.reshape(n, n), bad.value
+
+
+def residual_pass(model, z, x, y=None, *, grid=None, sigma=None, **kw):
+    """jf_residual_pass: (cost, nonfinite) at x."""
+    lib = L.load()
+    mid = _model_id(model)
+    n = lib.jf_model_nparams(mid)
+    data = _Data(y, z, sigma)
+    opts, keep = make_opts(grid=grid, sigma_ptr=data.sp, on_device=data.on_device, **kw)
+    xa = _as_host(x)
+    cost = C.c_double()
+    bad = C.c_int32()
+    rc = lib.jf_residual_pass(mid, data.yp, data.zp, data.m, _dptr(xa), n, C.byref(opts), C.byref(cost),
+                              C.byref(bad))
+    if rc < 0:
+        raise JFError(rc, "jf_residual_pass")
+    return cost.value, bad.value
+
+
+def pass_device(model, z, x_dev, kvec_dev, y=None, *, grid=None, sigma=None, residual_only=False, **kw):
+    """jf_pass_device: enqueue one pass on opts.stream (all CUDA tensors)."""
+    lib = L.load()
+    mid = _model_id(model)
+    n = lib.jf_model_nparams(mid)
+    data = _Data(y, z, sigma)
+    if not data.on_device:
+        raise ValueError("pass_device needs CUDA tensors")
+    opts, keep = make_opts(grid=grid, sigma_ptr=data.sp, on_device=True, **kw)
+    rc = lib.jf_pass_device(mid, data.yp, data.zp, data.m, x_dev.data_ptr(), n, C.byref(opts),
+                            1 if residual_only else 0, kvec_dev.data_ptr())
+    if rc < 0:
+        raise JFError(rc, "jf_pass_device")
+
+
+def trust_region_step(hatG, hatg, m, Delta, alpha=0.0, device=0):
+    """jf_trust_region_step: the single-warp subproblem (Alg. 2 + App. B)."""
+    lib = L.load()
+    G = _as_host(hatG)
+    g = _as_host(hatg)
+    n = g.size
+    p = np.zeros(n)
+    a = C.c_double()
+    it = C.c_int32()
+    opts, _ = make_opts(device=device)
+    rc = lib.jf_trust_region_step(_dptr(G), _dptr(g), n, int(m), float(Delta), float(alpha), C.byref(opts),
+                                  _dptr(p), C.byref(a), C.byref(it))
+    if rc < 0:
+        raise JFError(rc, "jf_trust_region_step")
+    return p, a.value, it.value
+
+
+class Comm:
+    """jf_comm: one rank's mailbox for the in-kernel cross-GPU combine."""
+
+    def __init__(self, handle, lib=None):
+        self.handle = handle
+        self._lib = lib or L.load()
+
+    @classmethod
+    def create(cls, rank: int, nranks: int, device: int) -> "Comm":
+        lib = L.load()
+        h = C.c_void_p()
+        rc = lib.jf_comm_create(rank, nranks, device, C.byref(h))
+        if rc < 0:
+            raise JFError(rc, "jf_comm_create")
+        return cls(h.value, lib)
+
+    @classmethod
+    def create_local(cls, nranks: int, device: int = 0) -> list["Comm"]:
+        lib = L.load()
+        arr = (C.c_void_p * nranks)()
+        rc = lib.jf_comm_create_local(nranks, device, arr)
+        if rc < 0:
+            raise JFError(rc, "jf_comm_create_local")
+        return [cls(arr[i], lib) for i in range(nranks)]
+
+    def export(self) -> bytes:
+        buf = C.create_string_buffer(L.JF_COMM_HANDLE_BYTES)
+        rc = self._lib.jf_comm_export(self.handle, buf)
+        if rc < 0:
+            raise JFError(rc, "jf_comm_export")
+        return buf.raw
+
+    def connect(self, all_handles: bytes):
+        rc = self._lib.jf_comm_connect(self.handle, all_handles)
+        if rc < 0:
+            raise JFError(rc, "jf_comm_connect")
+
+    def destroy(self):
+        if self.handle:
+            self._lib.jf_comm_destroy(self.handle)
+            self.handle = None

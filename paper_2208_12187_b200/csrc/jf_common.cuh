@@ -1,0 +1,64 @@
+// jf_common.cuh — shared device-side definitions of the B200 hot path.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace jf {
+
+constexpr int NMAX = 16;                               // JF_MAX_N
+constexpr int KMAX = (NMAX + 1) * (NMAX + 2) / 2 + 1;  // K-vector length for n = 16
+constexpr int BLOCK = 256;                             // threads per pass block
+constexpr int NWARP = BLOCK / 32;
+constexpr unsigned FULL = 0xffffffffu;
+
+// K-vector slot of W^T W entry (j, k), j <= k <= n, W = [J | r] (jf.h).
+__host__ __device__ constexpr int tri_slot(int n, int j, int k) {
+  return j * (n + 1) - (j * (j - 1)) / 2 + (k - j);
+}
+__host__ __device__ constexpr int tri_count(int n) { return (n + 1) * (n + 2) / 2; }
+
+enum CoordMode : int32_t {
+  COORD_EXPLICIT = 0,  // y arrays: t[m] (d=1) or X[m], Y[m] (d=2)
+  COORD_GRID = 1,      // implicit pixel grid (W, row0): X = i % W, Y = i / W + row0
+  COORD_IMPLICIT_T = 2 // t_i = t0 + (index0 + i) dt
+};
+
+// Epilogue run by the last block of a pass kernel after the deterministic combine.
+enum Epilogue : int32_t { EPI_NONE = 0, EPI_FIT = 1 };
+
+// Multi-GPU mailbox (see jf_comm.cu).  mbox[p] is rank p's mailbox as mapped
+// in this process (mbox[rank] is local).  Layout of one mailbox:
+//   double slot[2][nranks][KMAX]  (parity-double-buffered by epoch)
+//   uint64 flag[nranks]           (epoch written by each sender after its data)
+struct CommDev {
+  int32_t rank, nranks;
+  double* mbox_data[8];
+  unsigned long long* mbox_flag[8];
+  unsigned long long epoch;  // host-side base; the device uses st->comm_epoch
+};
+
+// Kernel inputs that stay fixed during one call (device-resident, so a cached
+// CUDA graph can be replayed for any data).
+struct PassArgs {
+  const double* z;      // observations [m]
+  const double* y0;     // t[m] or X[m] (COORD_EXPLICIT)
+  const double* y1;     // Y[m] (COORD_EXPLICIT, d=2)
+  const double* wsig;   // 1/sigma_i [m] or nullptr (App. C, Eq. C13-C16)
+  int64_t m;            // points in this shard
+  int64_t W;            // grid width (COORD_GRID)
+  int64_t row0;         // first row of this shard (COORD_GRID)
+  int64_t index0;       // first global index (COORD_IMPLICIT_T)
+  double t0, dt;        // COORD_IMPLICIT_T
+  int32_t coord;        // CoordMode
+  int32_t epilogue;     // Epilogue
+  const double* x;      // parameters to evaluate at (device, n doubles) for EPI_NONE
+  double* partials;     // [gridDim.x][KS] per-block partial K-vectors
+  unsigned int* ticket; // last-block ticket (reset by the last block)
+  double* out;          // combined K-vector (EPI_NONE)
+  int32_t use_comm;     // 1: combine across ranks through the mailboxes
+  int32_t pad_;
+  CommDev comm;
+};
+
+}  // namespace jf

@@ -1,0 +1,812 @@
+// jf_host.cu — host driver and C ABI of libjfb200.so (include/jf.h).
+//
+// Responsibilities: validate input (reading R18), stage
+// host data into HBM, pick the kernel instance for (model, coordinate mode),
+// size the grid, and run a fit either as ONE CUDA-graph launch — a WHILE
+// conditional node whose body is the pass kernel(s); the last block of each
+// pass runs the solver step and sets the loop condition on the device — or as
+// a host-driven loop (use_graph = 0).  Graphs are cached per (model, mode,
+// grid, policy) and replayed for any data, so only the first fit pays the
+// instantiation (cf. JAX tracing).
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <vector>
+
+#include "../../include/jf.h"
+#include "jf_kernels.h"
+#include "jf_solver.cuh"
+
+using namespace jf;
+
+namespace {
+
+Kernels get_kernels(int model, int coord) {
+  switch (model) {
+    case JF_LINEAR: return kernels_linear(coord);
+    case JF_EXP_DECAY: return kernels_exp_decay(coord);
+    case JF_GAUSS1D: return kernels_gauss1d(coord);
+    case JF_GAUSS2D_ROT: return kernels_gauss2d(coord);
+    case JF_GAUSS2D_ROT_X2: return kernels_gauss2d_x2(coord);
+    default: return Kernels{};
+  }
+}
+
+int model_n(int model) {
+  switch (model) {
+    case JF_LINEAR: return 2;
+    case JF_EXP_DECAY: return 3;
+    case JF_GAUSS1D: return 4;
+    case JF_GAUSS2D_ROT: return 7;
+    case JF_GAUSS2D_ROT_X2: return 13;
+    default: return -1;
+  }
+}
+int model_d(int model) {
+  switch (model) {
+    case JF_LINEAR:
+    case JF_EXP_DECAY:
+    case JF_GAUSS1D: return 1;
+    case JF_GAUSS2D_ROT:
+    case JF_GAUSS2D_ROT_X2: return 2;
+    default: return -1;
+  }
+}
+
+#define CK(call)                                                                                 \
+  do {                                                                                           \
+    cudaError_t e_ = (call);                                                                     \
+    if (e_ != cudaSuccess) {                                                                     \
+      fprintf(stderr, "jfb200: %s failed: %s (%s:%d)\n", #call, cudaGetErrorString(e_), __FILE__, \
+              __LINE__);                                                                         \
+      return e_ == cudaErrorMemoryAllocation ? JF_ENOMEM : JF_ECUDA;                             \
+    }                                                                                            \
+  } while (0)
+
+struct GraphKey {
+  int model, coord, policy, grid;
+  bool operator<(const GraphKey& o) const {
+    return std::tie(model, coord, policy, grid) < std::tie(o.model, o.coord, o.policy, o.grid);
+  }
+};
+
+struct Ctx {
+  std::mutex mu;
+  bool ready = false;
+  int dev = 0;
+  int nsm = 148;
+  cudaStream_t stream = nullptr;
+  PassArgs* d_args = nullptr;
+  FitState* d_state = nullptr;
+  FitState* h_state = nullptr;  // pinned
+  double* d_partials = nullptr;
+  int partial_blocks = 0;
+  unsigned int* d_ticket = nullptr;
+  double* d_out = nullptr;  // KMAX
+  double* d_x = nullptr;    // NMAX
+  double* d_trace = nullptr;
+  int trace_cap = 0;
+  double* d_in = nullptr;  // staged host inputs
+  size_t in_cap = 0;
+  std::map<int, int> occ;  // model*16+coord -> blocks/SM of the J kernel
+  std::map<GraphKey, cudaGraphExec_t> graphs;
+};
+
+Ctx g_ctx[64];
+
+int ctx_init(Ctx& c, int dev) {
+  if (c.ready) return 0;
+  CK(cudaSetDevice(dev));
+  c.dev = dev;
+  CK(cudaDeviceGetAttribute(&c.nsm, cudaDevAttrMultiProcessorCount, dev));
+  CK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+  CK(cudaMalloc(&c.d_args, sizeof(PassArgs)));
+  CK(cudaMalloc(&c.d_state, sizeof(FitState)));
+  CK(cudaMallocHost(&c.h_state, sizeof(FitState)));
+  c.partial_blocks = c.nsm * 4;
+  CK(cudaMalloc(&c.d_partials, sizeof(double) * (size_t)c.partial_blocks * KMAX));
+  CK(cudaMalloc(&c.d_ticket, sizeof(unsigned int) * 4));
+  CK(cudaMemset(c.d_ticket, 0, sizeof(unsigned int) * 4));
+  CK(cudaMalloc(&c.d_out, sizeof(double) * KMAX));
+  CK(cudaMalloc(&c.d_x, sizeof(double) * NMAX));
+  CK(cudaDeviceSynchronize());
+  c.ready = true;
+  return 0;
+}
+
+int grid_for(Ctx& c, int model, int coord, const Kernels& k, int64_t m) {
+  const int key = model * 16 + coord;
+  auto it = c.occ.find(key);
+  int occ;
+  if (it == c.occ.end()) {
+    occ = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k.jk, BLOCK, 0) != cudaSuccess || occ < 1) occ = 1;
+    if (occ > 4) occ = 4;
+    c.occ[key] = occ;
+  } else {
+    occ = it->second;
+  }
+  const int64_t need = (m + BLOCK - 1) / BLOCK;
+  int64_t g = (int64_t)c.nsm * occ;
+  if (need < g) g = need;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+}  // namespace
+
+struct jf_comm {
+  int rank = 0, nranks = 1, device = 0;
+  unsigned long long epoch = 0;
+  void* mbox = nullptr;           // local mailbox (device)
+  bool owns_mbox = true;
+  bool local = false;             // created by jf_comm_create_local
+  void* peer[8] = {nullptr};      // mapped mailboxes of all ranks
+  bool opened[8] = {false};
+};
+
+namespace {
+
+constexpr size_t MBOX_DATA_BYTES(int R) { return sizeof(double) * 2 * (size_t)R * KMAX; }
+size_t mbox_bytes(int R) { return MBOX_DATA_BYTES(R) + sizeof(unsigned long long) * 8; }
+
+void fill_comm(CommDev& cd, const jf_comm* cm) {
+  memset(&cd, 0, sizeof(cd));
+  cd.rank = cm->rank;
+  cd.nranks = cm->nranks;
+  for (int p = 0; p < cm->nranks; ++p) {
+    char* base = (char*)cm->peer[p];
+    cd.mbox_data[p] = (double*)base;
+    cd.mbox_flag[p] = (unsigned long long*)(base + MBOX_DATA_BYTES(cm->nranks));
+  }
+  cd.epoch = cm->epoch;
+}
+
+struct Staged {
+  const double* z = nullptr;
+  const double* y0 = nullptr;
+  const double* y1 = nullptr;
+  const double* wsig = nullptr;
+  int coord = COORD_EXPLICIT;
+  double upload_s = 0.0;
+};
+
+__global__ void inv_kernel(double* p, int64_t m) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = 1.0 / p[i];
+}
+
+// Validate the data description and make y/z/sigma available in HBM.
+int stage_inputs(Ctx& c, cudaStream_t s, int model, const double* y, const double* z, int64_t m,
+                 const jf_opts& o, Staged& st) {
+  const int d = model_d(model);
+  if (d < 0 || z == nullptr || m < 1) return JF_EINVAL;
+  int coord;
+  if (y != nullptr) {
+    coord = COORD_EXPLICIT;
+  } else if (d == 2) {
+    if (o.grid_w < 1 || o.grid_h < 1 || o.grid_w * o.grid_h != m) return JF_EINVAL;
+    coord = COORD_GRID;
+  } else {
+    if (!(o.dt == o.dt) || !std::isfinite(o.t0) || !std::isfinite(o.dt)) return JF_EINVAL;
+    coord = COORD_IMPLICIT_T;
+  }
+  st.coord = coord;
+  const size_t ny = (coord == COORD_EXPLICIT) ? (size_t)d * m : 0;
+  const size_t nw = o.sigma ? (size_t)m : 0;
+  auto t0 = std::chrono::steady_clock::now();
+  if (o.inputs_on_device) {
+    st.z = z;
+    if (coord == COORD_EXPLICIT) {
+      st.y0 = y;
+      st.y1 = (d == 2) ? y + m : nullptr;
+    }
+    if (o.sigma) {  // 1/sigma needs a scratch copy
+      if (c.in_cap < nw) {
+        if (c.d_in) cudaFree(c.d_in);
+        c.d_in = nullptr;
+        c.in_cap = 0;
+        CK(cudaMalloc(&c.d_in, sizeof(double) * nw));
+        c.in_cap = nw;
+      }
+      CK(cudaMemcpyAsync(c.d_in, o.sigma, sizeof(double) * nw, cudaMemcpyDeviceToDevice, s));
+      inv_kernel<<<c.nsm * 4, 256, 0, s>>>(c.d_in, m);
+      CK(cudaGetLastError());
+      st.wsig = c.d_in;
+    }
+  } else {
+    const size_t need = (size_t)m + ny + nw;
+    if (c.in_cap < need) {
+      if (c.d_in) cudaFree(c.d_in);
+      c.d_in = nullptr;
+      c.in_cap = 0;
+      CK(cudaMalloc(&c.d_in, sizeof(double) * need));
+      c.in_cap = need;
+    }
+    double* p = c.d_in;
+    CK(cudaMemcpyAsync(p, z, sizeof(double) * m, cudaMemcpyHostToDevice, s));
+    st.z = p;
+    p += m;
+    if (ny) {
+      CK(cudaMemcpyAsync(p, y, sizeof(double) * ny, cudaMemcpyHostToDevice, s));
+      st.y0 = p;
+      st.y1 = (d == 2) ? p + m : nullptr;
+      p += ny;
+    }
+    if (nw) {
+      CK(cudaMemcpyAsync(p, o.sigma, sizeof(double) * nw, cudaMemcpyHostToDevice, s));
+      inv_kernel<<<c.nsm * 4, 256, 0, s>>>(p, m);
+      CK(cudaGetLastError());
+      st.wsig = p;
+    }
+    CK(cudaStreamSynchronize(s));
+  }
+  st.upload_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return 0;
+}
+
+void fill_args(PassArgs& a, const Staged& sg, int64_t m, const jf_opts& o) {
+  memset(&a, 0, sizeof(a));
+  a.z = sg.z;
+  a.y0 = sg.y0;
+  a.y1 = sg.y1;
+  a.wsig = sg.wsig;
+  a.m = m;
+  a.W = o.grid_w;
+  a.row0 = o.grid_row0;
+  a.index0 = o.index0;
+  a.t0 = o.t0;
+  a.dt = o.dt;
+  a.coord = sg.coord;
+}
+
+struct Lock {
+  Ctx* c = nullptr;
+  std::unique_lock<std::mutex> lk;
+};
+
+int acquire(const jf_opts& o, Ctx*& c, std::unique_lock<std::mutex>& lk, cudaStream_t& s) {
+  if (o.device < 0 || o.device >= 64) return JF_EINVAL;
+  c = &g_ctx[o.device];
+  lk = std::unique_lock<std::mutex>(c->mu);
+  if (cudaSetDevice(o.device) != cudaSuccess) return JF_ECUDA;
+  int r = ctx_init(*c, o.device);
+  if (r) return r;
+  s = o.stream ? (cudaStream_t)o.stream : c->stream;
+  return 0;
+}
+
+// host-side strict feasibility, rstep = 1e-10 (reading R18/R19: x0 of the bounded path)
+void strictly_feasible_host(double* x, const double* lb, const double* ub, int n, double rstep) {
+  for (int j = 0; j < n; ++j) {
+    const double lo = lb[j], hi = ub[j], v = x[j];
+    double xn = v;
+    if (rstep == 0.0) {
+      if (v <= lo) xn = nextafter(lo, hi);
+      else if (v >= hi) xn = nextafter(hi, lo);
+    } else {
+      const double ld = v - lo, ud = hi - v;
+      const double lt = rstep * fmax(1.0, fabs(lo)), ut = rstep * fmax(1.0, fabs(hi));
+      if (std::isfinite(lo) && ld <= fmin(ud, lt)) xn = lo + lt;
+      else if (std::isfinite(hi) && ud <= fmin(ld, ut)) xn = hi - ut;
+    }
+    if (xn < lo || xn > hi) xn = 0.5 * (lo + hi);
+    x[j] = xn;
+  }
+}
+
+void active_mask_host(const double* x, const double* lb, const double* ub, int n, double rtol, int8_t* act) {
+  for (int j = 0; j < n; ++j) {
+    act[j] = 0;
+    const double ld = x[j] - lb[j], ud = ub[j] - x[j];
+    const double lt = rtol * fmax(1.0, fabs(lb[j])), ut = rtol * fmax(1.0, fabs(ub[j]));
+    if (std::isfinite(lb[j]) && ld <= fmin(ud, lt)) act[j] = -1;
+    if (std::isfinite(ub[j]) && ud <= fmin(ld, ut)) act[j] = 1;
+  }
+}
+
+int launch_pass(const Kernels& k, bool jac, int grid, cudaStream_t s, PassArgs* d_args, FitState* d_state) {
+  KernelFn f = jac ? k.jk : k.rk;
+  f<<<grid, BLOCK, 0, s>>>(d_args, d_state, (cudaGraphConditionalHandle)0, 0);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int build_graph(Ctx& c, const Kernels& k, int grid, int policy, cudaGraphExec_t* out) {
+  cudaGraph_t g;
+  CK(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h;
+  CK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t cn;
+  CK(cudaGraphAddNode(&cn, g, nullptr, 0, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  int use = 1;
+  PassArgs* pa = c.d_args;
+  FitState* st = c.d_state;
+  void* args[4] = {&pa, &st, &h, &use};
+  cudaKernelNodeParams kp;
+  memset(&kp, 0, sizeof(kp));
+  kp.gridDim = dim3(grid);
+  kp.blockDim = dim3(BLOCK);
+  kp.sharedMemBytes = 0;
+  kp.kernelParams = args;
+  cudaGraphNode_t prev = nullptr;
+  if (policy == JF_POLICY_CONSERVATIVE) {
+    kp.func = (void*)k.rk;
+    CK(cudaGraphAddKernelNode(&prev, body, nullptr, 0, &kp));
+  }
+  kp.func = (void*)k.jk;
+  cudaGraphNode_t jn;
+  CK(cudaGraphAddKernelNode(&jn, body, prev ? &prev : nullptr, prev ? 1 : 0, &kp));
+  CK(cudaGraphInstantiate(out, g, 0));
+  cudaGraphDestroy(g);
+  return 0;
+}
+
+}  // namespace
+
+// =============================================================== C ABI
+extern "C" {
+
+void jf_opts_default(jf_opts* o) {
+  if (!o) return;
+  memset(o, 0, sizeof(*o));
+  o->ftol = o->xtol = o->gtol = 1e-8;
+  o->max_nfev = 0;
+  o->x_scale_mode = JF_XSCALE_JAC;
+  o->solver = JF_SOLVE_GRAM;
+  o->policy = JF_POLICY_SPECULATIVE;
+  o->t0 = 0.0;
+  o->dt = 1.0;
+  o->use_graph = 1;
+}
+
+int32_t jf_model_nparams(int32_t model) { return model_n(model); }
+int32_t jf_model_ydim(int32_t model) { return model_d(model); }
+int32_t jf_model_kslots(int32_t model) {
+  const int n = model_n(model);
+  return n < 0 ? -1 : tri_count(n) + 1;
+}
+
+const char* jf_strerror(int32_t code) {
+  switch (code) {
+    case 0: return "max_nfev reached";
+    case 1: return "gtol satisfied";
+    case 2: return "ftol satisfied";
+    case 3: return "xtol satisfied";
+    case 4: return "ftol and xtol satisfied";
+    case JF_EINVAL: return "invalid argument";
+    case JF_EINFEASIBLE: return "initial guess outside the bounds";
+    case JF_ENONFINITE: return "residuals not finite at the initial guess";
+    case JF_ECUDA: return "CUDA error";
+    case JF_ECOMM: return "multi-GPU combine failed";
+    case JF_ENOMEM: return "out of memory";
+    default: return "unknown code";
+  }
+}
+
+const char* jf_version(void) { return "jfb200 0.1 sm_100a"; }
+
+static int pass_common(int32_t model, const double* y, const double* z, int64_t m, const double* x, int x_on_device,
+                       int32_t n, const jf_opts* opts, int residual_only, double* out_dev_or_null,
+                       double* host_out /* KMAX */, bool sync) {
+  jf_opts o;
+  if (opts) o = *opts;
+  else jf_opts_default(&o);
+  if (model_n(model) < 0 || n != model_n(model) || !x || !z || m < 1) return JF_EINVAL;
+  Ctx* c;
+  std::unique_lock<std::mutex> lk;
+  cudaStream_t s;
+  int r = acquire(o, c, lk, s);
+  if (r) return r;
+  Staged sg;
+  r = stage_inputs(*c, s, model, y, z, m, o, sg);
+  if (r) return r;
+  Kernels k = get_kernels(model, sg.coord);
+  if (!k.jk) return JF_EINVAL;
+  const int grid = grid_for(*c, model, sg.coord, k, m);
+  PassArgs a;
+  fill_args(a, sg, m, o);
+  a.epilogue = EPI_NONE;
+  if (x_on_device) {
+    a.x = x;
+  } else {
+    CK(cudaMemcpyAsync(c->d_x, x, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    a.x = c->d_x;
+  }
+  a.partials = c->d_partials;
+  a.ticket = c->d_ticket;
+  a.out = out_dev_or_null ? out_dev_or_null : c->d_out;
+  if (o.comm) {
+    a.use_comm = 1;
+    fill_comm(a.comm, o.comm);
+    o.comm->epoch += 1;
+  }
+  CK(cudaMemcpyAsync(c->d_args, &a, sizeof(a), cudaMemcpyHostToDevice, s));
+  r = launch_pass(k, !residual_only, grid, s, c->d_args, c->d_state);
+  if (r) return r;
+  if (host_out) {
+    const int KS = residual_only ? 2 : tri_count(n) + 1;
+    CK(cudaMemcpyAsync(host_out, a.out, sizeof(double) * KS, cudaMemcpyDeviceToHost, s));
+  }
+  if (sync) CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+int32_t jf_pass(int32_t model, const double* y, const double* z, int64_t m, const double* x, int32_t n,
+                const jf_opts* opts, double* cost, double* grad, double* gram, int32_t* nonfinite) {
+  double kv[KMAX];
+  int r = pass_common(model, y, z, m, x, 0, n, opts, 0, nullptr, kv, true);
+  if (r) return r;
+  if (cost) *cost = 0.5 * kv[tri_slot(n, n, n)];
+  for (int j = 0; j < n; ++j) {
+    if (grad) grad[j] = kv[tri_slot(n, j, n)];
+    for (int k = 0; k < n; ++k)
+      if (gram) gram[j * n + k] = kv[tri_slot(n, j < k ? j : k, j < k ? k : j)];
+  }
+  if (nonfinite) *nonfinite = (int32_t)kv[tri_count(n)];
+  return 0;
+}
+
+int32_t jf_residual_pass(int32_t model, const double* y, const double* z, int64_t m, const double* x, int32_t n,
+                         const jf_opts* opts, double* cost, int32_t* nonfinite) {
+  double kv[KMAX];
+  int r = pass_common(model, y, z, m, x, 0, n, opts, 1, nullptr, kv, true);
+  if (r) return r;
+  if (cost) *cost = 0.5 * kv[0];
+  if (nonfinite) *nonfinite = (int32_t)kv[1];
+  return 0;
+}
+
+int32_t jf_pass_device(int32_t model, const double* y, const double* z, int64_t m, const double* x_dev, int32_t n,
+                       const jf_opts* opts, int32_t residual_only, double* kvec_dev) {
+  jf_opts o;
+  if (opts) o = *opts;
+  else jf_opts_default(&o);
+  if (!o.inputs_on_device || !kvec_dev) return JF_EINVAL;
+  return pass_common(model, y, z, m, x_dev, 1, n, &o, residual_only, kvec_dev, nullptr, false);
+}
+
+static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t m, const double* p0, int32_t n,
+                        const double* lb, const double* ub, const jf_opts* opts, jf_result* out) {
+  auto fail = [&](int code) {
+    out->status = code;
+    return code;
+  };
+  jf_opts o;
+  if (opts) o = *opts;
+  else jf_opts_default(&o);
+  if (model_n(model) < 0 || n != model_n(model) || !z || m < 1) return fail(JF_EINVAL);
+  if (o.comm && o.m_global < m) return fail(JF_EINVAL);
+  out->n = n;
+  // ---- bounds and initial point (R18, R19)
+  double L[NMAX], U[NMAX], X0[NMAX], XS[NMAX];
+  bool bounded = false;
+  for (int j = 0; j < n; ++j) {
+    L[j] = lb ? lb[j] : -INFINITY;
+    U[j] = ub ? ub[j] : INFINITY;
+    if (std::isnan(L[j]) || std::isnan(U[j]) || !(L[j] < U[j])) return fail(JF_EINVAL);
+    if (std::isfinite(L[j]) || std::isfinite(U[j])) bounded = true;
+  }
+  for (int j = 0; j < n; ++j) {
+    if (p0) {
+      X0[j] = p0[j];
+    } else {  // curve_fit's default initial guess
+      const bool lf = std::isfinite(L[j]), uf = std::isfinite(U[j]);
+      X0[j] = (lf && uf) ? 0.5 * (L[j] + U[j]) : (lf ? L[j] + 1.0 : (uf ? U[j] - 1.0 : 1.0));
+    }
+    if (!std::isfinite(X0[j])) return fail(JF_EINVAL);
+    if (X0[j] < L[j] || X0[j] > U[j]) return fail(JF_EINFEASIBLE);
+  }
+  if (o.x_scale_mode == JF_XSCALE_ARRAY) {
+    if (!o.x_scale) return fail(JF_EINVAL);
+    for (int j = 0; j < n; ++j) {
+      if (!std::isfinite(o.x_scale[j]) || !(o.x_scale[j] > 0)) return fail(JF_EINVAL);
+      XS[j] = 1.0 / o.x_scale[j];
+    }
+  } else {
+    for (int j = 0; j < n; ++j) XS[j] = 1.0;
+  }
+  if (o.x_scale_mode < 0 || o.x_scale_mode > 2 || o.policy < 0 || o.policy > 1) return fail(JF_EINVAL);
+  if (bounded) strictly_feasible_host(X0, L, U, n, 1e-10);
+
+  Ctx* c;
+  std::unique_lock<std::mutex> lk;
+  cudaStream_t s;
+  int r = acquire(o, c, lk, s);
+  if (r) return fail(r);
+  Staged sg;
+  r = stage_inputs(*c, s, model, y, z, m, o, sg);
+  if (r) return fail(r);
+  out->t_upload_s = sg.upload_s;
+  Kernels k = get_kernels(model, sg.coord);
+  if (!k.jk) return fail(JF_EINVAL);
+  const int grid = grid_for(*c, model, sg.coord, k, m);
+
+  // trace buffer
+  if (o.trace_cap > 0) {
+    if (!o.trace) return fail(JF_EINVAL);
+    if (c->trace_cap < o.trace_cap) {
+      if (c->d_trace) cudaFree(c->d_trace);
+      c->d_trace = nullptr;
+      c->trace_cap = 0;
+      if (cudaMalloc(&c->d_trace, sizeof(double) * TRACE_FIELDS * (size_t)o.trace_cap) != cudaSuccess)
+        return fail(JF_ENOMEM);
+      c->trace_cap = o.trace_cap;
+    }
+  }
+
+  // ---- device state
+  FitState& h = *c->h_state;
+  memset(&h, 0, sizeof(h));
+  h.n = n;
+  h.bounded = bounded ? 1 : 0;
+  h.jacmode = (o.x_scale_mode == JF_XSCALE_JAC) ? 1 : 0;
+  h.max_nfev = o.max_nfev > 0 ? o.max_nfev : 100 * n;
+  h.policy = o.policy;
+  h.trace_cap = o.trace_cap > 0 ? o.trace_cap : 0;
+  h.trace = c->d_trace;
+  h.m_global = o.comm ? o.m_global : m;
+  h.ftol = o.ftol;
+  h.xtol = o.xtol;
+  h.gtol = o.gtol;
+  for (int j = 0; j < NMAX; ++j) {
+    h.lb[j] = j < n ? L[j] : 0.0;
+    h.ub[j] = j < n ? U[j] : 0.0;
+    h.xs_inv[j] = j < n ? XS[j] : 1.0;
+    h.x[j] = j < n ? X0[j] : 0.0;
+    h.x_eval[j] = h.x[j];
+  }
+  h.phase = PH_INIT_J;
+  h.status = STATUS_NONE;
+  h.cont = 1;
+  h.comm_epoch = o.comm ? o.comm->epoch : 0ull;
+  PassArgs a;
+  fill_args(a, sg, m, o);
+  a.epilogue = EPI_FIT;
+  a.partials = c->d_partials;
+  a.ticket = c->d_ticket;
+  a.out = c->d_out;
+  if (o.comm) {
+    a.use_comm = 1;
+    fill_comm(a.comm, o.comm);
+  }
+  auto t0 = std::chrono::steady_clock::now();
+  CK(cudaMemcpyAsync(c->d_state, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(c->d_args, &a, sizeof(a), cudaMemcpyHostToDevice, s));
+  int launches = 0;
+  if (o.use_graph) {
+    GraphKey key{model, sg.coord, o.policy, grid};
+    auto it = c->graphs.find(key);
+    cudaGraphExec_t ge;
+    if (it == c->graphs.end()) {
+      r = build_graph(*c, k, grid, o.policy, &ge);
+      if (r) return fail(r);
+      c->graphs[key] = ge;
+    } else {
+      ge = it->second;
+    }
+    CK(cudaGraphLaunch(ge, s));
+    CK(cudaMemcpyAsync(&h, c->d_state, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  } else {
+    const int cap = 4 * h.max_nfev + 8;
+    for (int iter = 0; iter < cap; ++iter) {
+      const bool jac = (o.policy == JF_POLICY_CONSERVATIVE) ? (h.phase != PH_TRIAL_R) : true;
+      r = launch_pass(k, jac, grid, s, c->d_args, c->d_state);
+      if (r) return fail(r);
+      CK(cudaMemcpyAsync(&h, c->d_state, sizeof(h), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      if (!h.cont) break;
+    }
+  }
+  out->t_solve_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  launches = h.launches;
+  if (o.comm) o.comm->epoch = h.comm_epoch;
+
+  // ---- result
+  out->kernel_launches = launches;
+  out->nfev = h.nfev;
+  out->njev = h.njev;
+  out->nit = h.nit;
+  out->cost = h.cost;
+  out->optimality = h.gnorm;
+  for (int j = 0; j < n; ++j) {
+    out->x[j] = h.x[j];
+    out->grad[j] = h.g[j];
+    for (int q = 0; q < n; ++q) out->gram[j * n + q] = h.G[j * NMAX + q];
+  }
+  if (bounded) active_mask_host(h.x, L, U, n, o.xtol, out->active_mask);
+  out->trace_len = h.trace_len < o.trace_cap ? h.trace_len : o.trace_cap;
+  if (o.trace_cap > 0 && out->trace_len > 0)
+    CK(cudaMemcpy(o.trace, c->d_trace, sizeof(double) * TRACE_FIELDS * out->trace_len, cudaMemcpyDeviceToHost));
+  if (h.error) return fail(h.error);
+  if (h.cont) return fail(JF_ECUDA);  // loop did not terminate
+  out->status = h.status;
+  return h.status;
+}
+
+int32_t jf_curve_fit(int32_t model, const double* y, const double* z, int64_t m, const double* p0, int32_t n,
+                     const double* lb, const double* ub, const jf_opts* opts, jf_result* out) {
+  if (!out) return JF_EINVAL;
+  memset(out, 0, sizeof(*out));
+  const int32_t r = fit_impl(model, y, z, m, p0, n, lb, ub, opts, out);
+  if (r < 0) out->status = r;
+  return r;
+}
+
+// ----------------------------------------------------- subproblem test hook
+}  // extern "C"
+
+namespace {
+__global__ void tr_step_kernel(const double* hatG, const double* hatg, int n, int64_t m, double Delta,
+                               double alpha_in, double* out) {
+  __shared__ SolverSmem S;
+  const int lane = threadIdx.x;
+  for (int e = lane; e < n * n; e += 32) {
+    const int i = e / n, j = e % n;
+    S.A[i][j] = hatG[e];
+    S.M[i][j] = hatG[e];
+  }
+  __syncwarp();
+  double lam;
+  warp_eig(S, n, lane, lam);
+  const double g = lane < n ? hatg[lane] : 0.0;
+  const double suf = wVtx(S.V, g, n, lane);
+  double alpha = alpha_in, p;
+  const int it = warp_solve_tr(S, n, m, lam, suf, Delta, alpha, p, lane, nullptr);
+  if (lane < n) out[lane] = p;
+  if (lane < n) out[NMAX + lane] = lam;
+  if (lane == 0) {
+    out[2 * NMAX] = alpha;
+    out[2 * NMAX + 1] = it;
+  }
+}
+}  // namespace
+
+extern "C" int32_t jf_trust_region_step(const double* hatG, const double* hatg, int32_t n, int64_t m, double Delta,
+                                        double alpha_in, const jf_opts* opts, double* p, double* alpha_out,
+                                        int32_t* n_iter) {
+  jf_opts o;
+  if (opts) o = *opts;
+  else jf_opts_default(&o);
+  if (!hatG || !hatg || !p || n < 1 || n > NMAX || !(Delta > 0)) return JF_EINVAL;
+  Ctx* c;
+  std::unique_lock<std::mutex> lk;
+  cudaStream_t s;
+  int r = acquire(o, c, lk, s);
+  if (r) return r;
+  double* d;
+  CK(cudaMalloc(&d, sizeof(double) * (n * n + n + 2 * NMAX + 2)));
+  double* dG = d;
+  double* dg = d + n * n;
+  double* dout = dg + n;
+  CK(cudaMemcpyAsync(dG, hatG, sizeof(double) * n * n, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(dg, hatg, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  tr_step_kernel<<<1, 32, 0, s>>>(dG, dg, n, m, Delta, alpha_in, dout);
+  CK(cudaGetLastError());
+  double hout[2 * NMAX + 2];
+  CK(cudaMemcpyAsync(hout, dout, sizeof(hout), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  cudaFree(d);
+  for (int j = 0; j < n; ++j) p[j] = hout[j];
+  if (alpha_out) *alpha_out = hout[2 * NMAX];
+  if (n_iter) *n_iter = (int32_t)hout[2 * NMAX + 1];
+  return 0;
+}
+
+// ============================================================ multi-GPU comm
+// Mailbox-based cross-rank combine (jf.h "Multi-GPU").  Each rank allocates
+// one mailbox in its own HBM; peers map it through CUDA IPC and write into it
+// over NVLink from inside the pass kernel (jf_pass.cuh comm_combine).
+namespace {
+struct HandleBlob {
+  uint32_t magic;
+  int32_t rank, nranks, device;
+  cudaIpcMemHandle_t h;
+};
+constexpr uint32_t kMagic = 0x4a464232u;  // "JFB2"
+}  // namespace
+
+extern "C" {
+
+int32_t jf_comm_create(int32_t rank, int32_t nranks, int32_t device, jf_comm** comm) {
+  if (!comm || nranks < 1 || nranks > 8 || rank < 0 || rank >= nranks) return JF_EINVAL;
+  *comm = nullptr;
+  if (cudaSetDevice(device) != cudaSuccess) return JF_ECUDA;
+  jf_comm* c = new jf_comm();
+  c->rank = rank;
+  c->nranks = nranks;
+  c->device = device;
+  if (cudaMalloc(&c->mbox, mbox_bytes(nranks)) != cudaSuccess) {
+    delete c;
+    return JF_ENOMEM;
+  }
+  if (cudaMemset(c->mbox, 0, mbox_bytes(nranks)) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+    cudaFree(c->mbox);
+    delete c;
+    return JF_ECUDA;
+  }
+  c->peer[rank] = c->mbox;
+  *comm = c;
+  return 0;
+}
+
+int32_t jf_comm_export(const jf_comm* comm, uint8_t handle[JF_COMM_HANDLE_BYTES]) {
+  if (!comm || !handle || comm->local) return JF_EINVAL;
+  HandleBlob b;
+  memset(&b, 0, sizeof(b));
+  b.magic = kMagic;
+  b.rank = comm->rank;
+  b.nranks = comm->nranks;
+  b.device = comm->device;
+  if (cudaSetDevice(comm->device) != cudaSuccess) return JF_ECUDA;
+  if (cudaIpcGetMemHandle(&b.h, comm->mbox) != cudaSuccess) return JF_ECOMM;
+  memset(handle, 0, JF_COMM_HANDLE_BYTES);
+  memcpy(handle, &b, sizeof(b));
+  return 0;
+}
+
+int32_t jf_comm_connect(jf_comm* comm, const uint8_t* all) {
+  if (!comm || !all || comm->local) return JF_EINVAL;
+  if (cudaSetDevice(comm->device) != cudaSuccess) return JF_ECUDA;
+  for (int p = 0; p < comm->nranks; ++p) {
+    HandleBlob b;
+    memcpy(&b, all + (size_t)p * JF_COMM_HANDLE_BYTES, sizeof(b));
+    if (b.magic != kMagic || b.rank != p || b.nranks != comm->nranks) return JF_EINVAL;
+    if (p == comm->rank) continue;
+    int can = 0;
+    if (cudaDeviceCanAccessPeer(&can, comm->device, b.device) == cudaSuccess && can) {
+      cudaError_t e = cudaDeviceEnablePeerAccess(b.device, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return JF_ECOMM;
+      cudaGetLastError();
+    }
+    void* ptr = nullptr;
+    if (cudaIpcOpenMemHandle(&ptr, b.h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return JF_ECOMM;
+    comm->peer[p] = ptr;
+    comm->opened[p] = true;
+  }
+  return 0;
+}
+
+int32_t jf_comm_create_local(int32_t nranks, int32_t device, jf_comm** comms) {
+  if (!comms || nranks < 1 || nranks > 8) return JF_EINVAL;
+  if (cudaSetDevice(device) != cudaSuccess) return JF_ECUDA;
+  std::vector<jf_comm*> cs;
+  for (int r = 0; r < nranks; ++r) {
+    jf_comm* c = nullptr;
+    int e = jf_comm_create(r, nranks, device, &c);
+    if (e) {
+      for (auto* q : cs) jf_comm_destroy(q);
+      return e;
+    }
+    c->local = true;
+    cs.push_back(c);
+  }
+  for (int r = 0; r < nranks; ++r)
+    for (int p = 0; p < nranks; ++p) cs[r]->peer[p] = cs[p]->mbox;
+  for (int r = 0; r < nranks; ++r) comms[r] = cs[r];
+  return 0;
+}
+
+int32_t jf_comm_destroy(jf_comm* comm) {
+  if (!comm) return JF_EINVAL;
+  cudaSetDevice(comm->device);
+  cudaDeviceSynchronize();
+  for (int p = 0; p < comm->nranks; ++p)
+    if (comm->opened[p]) cudaIpcCloseMemHandle(comm->peer[p]);
+  if (comm->mbox) cudaFree(comm->mbox);
+  delete comm;
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,19 @@
+// jf_kernels.h — host-side handles of the pass-kernel instances, one
+// translation unit per model (jf_k_*.cu) so they compile in parallel.
+#pragma once
+
+#include "jf_common.cuh"
+
+namespace jf {
+struct FitState;
+using KernelFn = void (*)(const PassArgs*, FitState*, cudaGraphConditionalHandle, int);
+struct Kernels {
+  KernelFn jk = nullptr;  // J-pass (value + dual Jacobian + fused Gram)
+  KernelFn rk = nullptr;  // residual-only pass
+};
+Kernels kernels_linear(int coord);
+Kernels kernels_exp_decay(int coord);
+Kernels kernels_gauss1d(int coord);
+Kernels kernels_gauss2d(int coord);
+Kernels kernels_gauss2d_x2(int coord);
+}  // namespace jf

@@ -1,0 +1,170 @@
+// jf_models.cuh — the built-in models h(y; x) of the hot path.
+//
+// P:44-48 §II Eq. 1: r_i(x) = h(y_i, x) - z_i.  Each model is written ONCE
+// over a generic scalar: instantiated with JAC = true every parameter is a
+// seeded dual number (jf_dual.cuh) and point() returns h together with the
+// whole Jacobian row dh/dx; with JAC = false the same body is the
+// residual-only evaluation used at trial points (Eq. 15).
+//
+// Each model splits into prologue(x) — parameter-only sub-expressions, once
+// per thread per pass ("hoisted to a per-pass prologue") —
+// and point(pre, y) — the per-data-point work.
+//
+// Parameter orders are jf.h's (reading R21).
+#pragma once
+
+#include "jf_dual.cuh"
+
+namespace jf {
+
+// Parameter j as a dual seed (J-pass) or a plain double (residual pass).
+template <bool JAC, int N, int j>
+__device__ __forceinline__ auto param(double v) {
+  if constexpr (JAC) {
+    return seed<N, j>(v);
+  } else {
+    return v;
+  }
+}
+
+// ---------------------------------------------------------------- LINEAR (n=2)
+struct ModelLinear {
+  static constexpr int N = 2, D = 1;
+  struct Pre {
+    double x0, x1;
+  };
+  template <bool JAC>
+  __device__ __forceinline__ static Pre prologue(const double* x) { return {x[0], x[1]}; }
+  template <bool JAC>
+  __device__ __forceinline__ static auto point(const Pre& p, double t) {
+    return param<JAC, N, 0>(p.x0) * t + param<JAC, N, 1>(p.x1);
+  }
+};
+
+// ------------------------------------------------------------ EXP_DECAY (n=3)
+struct ModelExpDecay {
+  static constexpr int N = 3, D = 1;
+  struct Pre {
+    double a, b, c;
+  };
+  template <bool JAC>
+  __device__ __forceinline__ static Pre prologue(const double* x) { return {x[0], x[1], x[2]}; }
+  template <bool JAC>
+  __device__ __forceinline__ static auto point(const Pre& p, double t) {
+    // a * exp(-b t) + c
+    const auto a = param<JAC, N, 0>(p.a);
+    const auto b = param<JAC, N, 1>(p.b);
+    const auto c = param<JAC, N, 2>(p.c);
+    return a * dexp(-(b * t)) + c;
+  }
+};
+
+// --------------------------------------------------------------- GAUSS1D (n=4)
+template <class TI>
+struct PreGauss1D {
+  double A, mu, c;
+  TI inv2s2;  // 1 / (2 s^2), a dual in s
+};
+struct ModelGauss1D {
+  static constexpr int N = 4, D = 1;
+  template <bool JAC>
+  __device__ __forceinline__ static auto prologue(const double* x) {
+    const auto s = param<JAC, N, 2>(x[2]);
+    auto inv = 0.5 / (s * s);
+    return PreGauss1D<decltype(inv)>{x[0], x[1], x[3], inv};
+  }
+  template <bool JAC, class P>
+  __device__ __forceinline__ static auto point(const P& p, double t) {
+    // A * exp(-(t - mu)^2 / (2 s^2)) + c
+    const auto dt = t - param<JAC, N, 1>(p.mu);
+    const auto E = dexp(-((dt * dt) * p.inv2s2));
+    return param<JAC, N, 0>(p.A) * E + param<JAC, N, 3>(p.c);
+  }
+};
+
+// ------------------------------------------------------- GAUSS2D_ROT (n=7)
+// h = A exp(-(a dx^2 + 2 b dx dy + c2 dy^2)) + off
+//   a  = cos^2/(2 sx^2) + sin^2/(2 sy^2)
+//   b  = sin(2 th) (1/(4 sy^2) - 1/(4 sx^2)) = sin cos (1/(2 sy^2) - 1/(2 sx^2))
+//   c2 = sin^2/(2 sx^2) + cos^2/(2 sy^2)
+template <class TA, class TB, class TC>
+struct PreGauss2D {
+  TA a;
+  TB b2;  // 2 b
+  TC c;
+  double A, x0, y0;
+};
+
+// One rotated Gaussian component whose parameters start at index B of x.
+template <int N, int B>
+struct Gauss2DComponent {
+  template <bool JAC>
+  __device__ __forceinline__ static auto prologue(const double* x) {
+    const auto sx = param<JAC, N, B + 3>(x[B + 3]);
+    const auto sy = param<JAC, N, B + 4>(x[B + 4]);
+    const auto th = param<JAC, N, B + 5>(x[B + 5]);
+    const auto C = dcos(th);
+    const auto S = dsin(th);
+    const auto ix = 0.5 / (sx * sx);  // 1/(2 sx^2)
+    const auto iy = 0.5 / (sy * sy);  // 1/(2 sy^2)
+    const auto CC = C * C;
+    const auto SS = S * S;
+    auto a = CC * ix + SS * iy;
+    auto b2 = 2.0 * ((S * C) * (iy - ix));
+    auto c = SS * ix + CC * iy;
+    return PreGauss2D<decltype(a), decltype(b2), decltype(c)>{a, b2, c, x[B + 0], x[B + 1], x[B + 2]};
+  }
+  // A * exp(-q), q = dx (a dx + 2b dy) + c2 dy^2
+  template <bool JAC, class P>
+  __device__ __forceinline__ static auto point(const P& p, double X, double Y) {
+    const auto dx = X - param<JAC, N, B + 1>(p.x0);
+    const auto dy = Y - param<JAC, N, B + 2>(p.y0);
+    const auto q = dx * (p.a * dx + p.b2 * dy) + p.c * (dy * dy);
+    return param<JAC, N, B + 0>(p.A) * dexp(-q);
+  }
+};
+
+struct ModelGauss2DRot {
+  static constexpr int N = 7, D = 2;
+  using G = Gauss2DComponent<N, 0>;
+  template <class P>
+  struct Pre {
+    P g;
+    double off;
+  };
+  template <bool JAC>
+  __device__ __forceinline__ static auto prologue(const double* x) {
+    auto g = G::template prologue<JAC>(x);
+    return Pre<decltype(g)>{g, x[6]};
+  }
+  template <bool JAC, class P>
+  __device__ __forceinline__ static auto point(const P& p, double X, double Y) {
+    return G::template point<JAC>(p.g, X, Y) + param<JAC, N, 6>(p.off);
+  }
+};
+
+// ---------------------------------------------------- GAUSS2D_ROT_X2 (n=13)
+struct ModelGauss2DRotX2 {
+  static constexpr int N = 13, D = 2;
+  using G1 = Gauss2DComponent<N, 0>;
+  using G2 = Gauss2DComponent<N, 6>;
+  template <class P1, class P2>
+  struct Pre {
+    P1 g1;
+    P2 g2;
+    double off;
+  };
+  template <bool JAC>
+  __device__ __forceinline__ static auto prologue(const double* x) {
+    auto g1 = G1::template prologue<JAC>(x);
+    auto g2 = G2::template prologue<JAC>(x);
+    return Pre<decltype(g1), decltype(g2)>{g1, g2, x[12]};
+  }
+  template <bool JAC, class P>
+  __device__ __forceinline__ static auto point(const P& p, double X, double Y) {
+    return (G1::template point<JAC>(p.g1, X, Y) + G2::template point<JAC>(p.g2, X, Y)) +
+           param<JAC, N, 12>(p.off);
+  }
+};
+
+}  // namespace jf

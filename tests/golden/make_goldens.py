@@ -1,0 +1,43 @@
+"""Write tests/golden/fits_full.json: the ORACLE's fits at BASELINE full sizes.
+
+Calls only oracle/ (and datagen/ for the seeded inputs), never the CUDA path.
+Run on any CPU:  python tests/golden/make_goldens.py   (several minutes)."""
+import json
+import os
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+import datagen as dg  # noqa: E402
+from oracle import trf  # noqa: E402
+
+CASES = {
+    "T_4096_seed6": lambda: dg.make_gauss2d(4096, seed=6),
+    "C3_1024_seed3": lambda: dg.make_gauss2d(1024, seed=3),
+    "C4b_1024_seed4": lambda: dg.make_gauss2d_bounded(1024, "b"),
+    "C4c_1024_seed4": lambda: dg.make_gauss2d_bounded(1024, "c"),
+}
+
+
+def main():
+    out = {}
+    path = os.path.join(HERE, "fits_full.json")
+    if os.path.exists(path):
+        out = json.load(open(path))
+    for key, make in CASES.items():
+        if key in out and "--force" not in sys.argv:
+            continue
+        pr = make()
+        tr = []
+        r = trf.fit(pr.model, pr.coords(), pr.z, pr.p0, pr.lb, pr.ub, trace=tr)
+        out[key] = dict(status=r["status"], nfev=r["nfev"], njev=r["njev"], nit=r["nit"], cost=r["cost"],
+                        x=[float(v) for v in r["x"]], active_mask=[int(v) for v in r["active_mask"]],
+                        trace=[[float(v) for v in row] for row in tr],
+                        source="oracle/trf.py fit on datagen inputs (tests/golden/make_goldens.py)")
+        print(key, r["status"], r["nfev"], r["njev"], r["cost"], flush=True)
+        json.dump(out, open(path, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()

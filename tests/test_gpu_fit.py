@@ -1,0 +1,156 @@
+"""GPU parity of complete fits (device subproblem,
+control and graph driver) against the oracle TRF (oracle/trf.py).
+
+Bar (north star): final parameters within 1e-6 relative, iteration counts
+(nfev, njev, nit) and status identical on these well-conditioned problems;
+per-trial Delta / alpha trace within 1e-9 relative."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import datagen as dg
+from oracle import trf as otrf
+
+jf = pytest.importorskip("paper_2208_12187_b200")
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _kw(pr):
+    if pr.grid is not None:
+        return dict(grid=pr.grid)
+    return dict(y=pr.t)
+
+
+def check_fit(res, ref, trace=None, ref_trace=None):
+    assert (res.status, res.nfev, res.njev, res.nit) == (ref["status"], ref["nfev"], ref["njev"], ref["nit"])
+    x = ref["x"]
+    assert np.all(np.abs(res.x - x) <= 1e-6 * np.maximum(np.abs(x), 1e-3 * np.max(np.abs(x))))
+    assert res.cost == pytest.approx(ref["cost"], rel=1e-9)
+    if ref_trace is not None:
+        tr = np.array(ref_trace)
+        assert trace.shape == tr.shape
+        # Delta (col 5) and alpha (col 6), counters (0-2), branch (11)
+        assert np.array_equal(trace[:, [0, 1, 2, 11]], tr[:, [0, 1, 2, 11]])
+        for col in (5, 6):
+            a, b = trace[:, col], tr[:, col]
+            assert np.all(np.abs(a - b) <= 1e-9 * np.maximum(np.abs(b), 1e-300))
+
+
+FITS = [
+    ("C1", lambda: dg.make_exp_decay()),
+    ("C2 m=1000", lambda: dg.make_gauss1d(1000)),
+    ("C2 m=100000", lambda: dg.make_gauss1d(100_000)),
+    ("linear", lambda: dg.make_linear()),
+    ("C3 W=256", lambda: dg.make_gauss2d(256)),
+    ("C4a W=256", lambda: dg.make_gauss2d_bounded(256, "a")),
+    ("C4b W=256", lambda: dg.make_gauss2d_bounded(256, "b")),
+    ("C4c W=256", lambda: dg.make_gauss2d_bounded(256, "c")),
+    ("C5 W=128", lambda: dg.make_gauss2d_x2(128)),
+]
+
+
+@pytest.mark.parametrize("name,make", FITS, ids=[f[0] for f in FITS])
+@pytest.mark.parametrize("mode", ["graph", "hostloop", "conservative"])
+def test_fit_matches_oracle(name, make, mode):
+    pr = make()
+    tr = []
+    ref = otrf.fit(pr.model, pr.coords(), pr.z, pr.p0, pr.lb, pr.ub, trace=tr)
+    res = jf.curve_fit(pr.model, pr.z, p0=pr.p0, lb=pr.lb, ub=pr.ub, trace_cap=256,
+                       use_graph=(mode != "hostloop"),
+                       policy=("conservative" if mode == "conservative" else "speculative"), **_kw(pr))
+    check_fit(res, ref, res.trace, tr)
+    if pr.lb is not None:
+        assert np.array_equal(res.active_mask, ref["active_mask"])
+
+
+@pytest.mark.parametrize("x_scale", ["ones", "array"])
+def test_fit_x_scale_modes(x_scale):
+    pr = dg.make_gauss2d(200)
+    xs = "ones" if x_scale == "ones" else np.abs(pr.p0) + 1.0
+    ref = otrf.fit(pr.model, pr.coords(), pr.z, pr.p0, x_scale=xs)
+    res = jf.curve_fit(pr.model, pr.z, p0=pr.p0, grid=pr.grid, x_scale=xs)
+    check_fit(res, ref)
+
+
+def test_fit_device_inputs_and_weights():
+    pr = dg.make_gauss1d(20_000)
+    sig = np.random.default_rng(2).uniform(0.5, 2.0, pr.m)
+    ref = otrf.fit(pr.model, pr.t, pr.z, pr.p0, sigma=sig)
+    res = jf.curve_fit(pr.model, torch.as_tensor(pr.z).cuda(), y=torch.as_tensor(pr.t).cuda(), p0=pr.p0,
+                       sigma=torch.as_tensor(sig).cuda())
+    check_fit(res, ref)
+
+
+def test_fit_errors():
+    pr = dg.make_exp_decay()
+    z = pr.z.copy()
+    z[3] = np.inf
+    with pytest.raises(jf.JFError) as e:
+        jf.curve_fit(pr.model, z, y=pr.t, p0=pr.p0)
+    assert e.value.code == -3
+    with pytest.raises(jf.JFError) as e:
+        jf.curve_fit(pr.model, pr.z, y=pr.t, p0=[5.0, 1, 1], lb=[0, 0, 0], ub=[1, 2, 2])
+    assert e.value.code == -2
+
+
+def test_max_nfev_status_zero():
+    pr = dg.make_gauss2d(128)
+    ref = otrf.fit(pr.model, pr.coords(), pr.z, pr.p0, max_nfev=3)
+    res = jf.curve_fit(pr.model, pr.z, p0=pr.p0, grid=pr.grid, max_nfev=3)
+    assert res.status == 0
+    check_fit(res, ref)
+
+
+def test_fit_is_deterministic_and_graph_reusable():
+    pr = dg.make_gauss2d(300)
+    a = jf.curve_fit(pr.model, pr.z, p0=pr.p0, grid=pr.grid)
+    pr2 = dg.make_gauss2d(300, k=1)
+    jf.curve_fit(pr2.model, pr2.z, p0=pr2.p0, grid=pr2.grid)
+    b = jf.curve_fit(pr.model, pr.z, p0=pr.p0, grid=pr.grid)
+    assert np.array_equal(a.x, b.x) and a.cost == b.cost and a.nfev == b.nfev
+
+
+def test_trust_region_step_matches_oracle():
+    """T5: identical (B_hat, g_hat, Delta, alpha) into the warp kernel and the
+    oracle's App. B solve (SVD of J): same n_iter, p and alpha to 1e-9."""
+    rng = np.random.default_rng(5)
+    for k in range(60):
+        m = int(rng.integers(8, 200))
+        n = int(rng.integers(1, 14))
+        J = rng.standard_normal((m, n)) * rng.uniform(0.2, 5, n)
+        r = rng.standard_normal(m)
+        U, s, VT = np.linalg.svd(J, full_matrices=False)
+        Delta = float(np.linalg.norm(np.linalg.lstsq(J, r, rcond=None)[0])) * rng.uniform(0.05, 1.5)
+        a0 = 0.0 if k % 2 else float(rng.uniform(0, 2))
+        p_ref, a_ref, it_ref = otrf.solve_tr(n, m, U.T @ r, s, VT.T, Delta, a0)
+        p, a, it = jf.trust_region_step(J.T @ J, J.T @ r, m, Delta, a0)
+        assert it == it_ref
+        assert np.allclose(p, p_ref, rtol=1e-9, atol=1e-12 * np.linalg.norm(p_ref))
+        assert a == pytest.approx(a_ref, rel=1e-9, abs=1e-300)
+
+
+GOLD = os.path.join(HERE, "golden", "fits_full.json")
+
+
+@pytest.mark.slow
+@pytest.mark.skipif(not os.path.exists(GOLD), reason="golden fits not generated")
+@pytest.mark.parametrize("key", ["T_4096_seed6", "C3_1024_seed3", "C4b_1024_seed4", "C4c_1024_seed4"])
+def test_full_size_fit_matches_oracle_golden(key):
+    """Full BASELINE sizes: the oracle's fit, stored by tests/golden/make_goldens.py
+    (which calls only oracle/), against the device fit with device-resident data."""
+    gold = json.load(open(GOLD))[key]
+    pr = {"T_4096_seed6": lambda: dg.make_gauss2d(4096, seed=6),
+          "C3_1024_seed3": lambda: dg.make_gauss2d(1024, seed=3),
+          "C4b_1024_seed4": lambda: dg.make_gauss2d_bounded(1024, "b"),
+          "C4c_1024_seed4": lambda: dg.make_gauss2d_bounded(1024, "c")}[key]()
+    res = jf.curve_fit(pr.model, torch.as_tensor(pr.z).cuda(), p0=pr.p0, lb=pr.lb, ub=pr.ub, grid=pr.grid,
+                       trace_cap=64)
+    ref = dict(gold)
+    ref["x"] = np.array(gold["x"])
+    check_fit(res, ref, res.trace, gold["trace"])

@@ -1,0 +1,149 @@
+"""GPU parity of the data-parallel passes against the
+oracle (oracle/passes.py), called through the C ABI.
+
+Tolerances (north star: per-pass cost, gradient and Gram to 1e-10 relative,
+fp64), Cauchy-Schwarz-normalised so near-zero entries are well posed
+(SURVEY §8(c) c.3): |dcost| <= 1e-10 cost, |dg_j| <= 1e-10 sqrt(G_jj 2 cost),
+|dG_jk| <= 1e-10 sqrt(G_jj G_kk)."""
+import math
+
+import numpy as np
+import pytest
+
+import datagen as dg
+from oracle import passes as orp
+
+jf = pytest.importorskip("paper_2208_12187_b200")
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+def check_pass(gpu, ref, tol=TOL):
+    c, g, G, bad = gpu
+    cr, gr, Gr, badr = ref
+    assert bad == badr
+    assert abs(c - cr) <= tol * cr
+    d = np.sqrt(np.diag(Gr))
+    assert np.all(np.abs(g - gr) <= tol * d * math.sqrt(2 * cr) + 1e-300)
+    assert np.all(np.abs(G - Gr) <= tol * np.outer(d, d) + 1e-300)
+    assert np.array_equal(G, G.T)
+
+
+def _x_near(pr, k):
+    if k == 0:
+        return pr.p0
+    if k == 1:
+        return pr.truth
+    rng = np.random.default_rng(k)
+    x = pr.truth * (1 + rng.uniform(-0.3, 0.3, pr.n))
+    return x
+
+
+CASES = [
+    ("exp_decay m=1000", lambda: dg.make_exp_decay()),
+    ("exp_decay ragged", lambda: dg.make_exp_decay(m=296 * 256 * 3 + 77)),
+    ("gauss1d m=1000", lambda: dg.make_gauss1d(1000)),
+    ("gauss1d ragged", lambda: dg.make_gauss1d(256 * 1000 + 13)),
+    ("linear", lambda: dg.make_linear(m=5001)),
+    ("gauss2d W=64", lambda: dg.make_gauss2d(64)),
+    ("gauss2d W=1000x777", lambda: dg.make_gauss2d(1000, H=777)),
+    ("gauss2d W=1024", lambda: dg.make_gauss2d(1024)),
+    ("gauss2d_x2 W=96", lambda: dg.make_gauss2d_x2(96)),
+    ("gauss2d_x2 W=700x333", lambda: dg.make_gauss2d_x2(700, H=333)),
+]
+
+
+@pytest.mark.parametrize("name,make", CASES, ids=[c[0] for c in CASES])
+@pytest.mark.parametrize("xk", [0, 1, 2])
+def test_jpass_matches_oracle_implicit_coords(name, make, xk):
+    pr = make()
+    x = _x_near(pr, xk)
+    ref = orp.jpass(pr.model, pr.coords(), pr.z, x)
+    if pr.grid is not None:
+        gpu = jf.jpass(pr.model, pr.z, x, grid=pr.grid)
+    elif "t0" in pr.meta:
+        gpu = jf.jpass(pr.model, pr.z, x, t0=pr.meta["t0"], dt=pr.meta["dt"])
+    else:
+        gpu = jf.jpass(pr.model, pr.z, x, y=pr.t)
+    check_pass(gpu, ref)
+
+
+@pytest.mark.parametrize("name,make", CASES[::2], ids=[c[0] for c in CASES[::2]])
+def test_jpass_matches_oracle_explicit_coords_device_inputs(name, make):
+    pr = make()
+    x = _x_near(pr, 2)
+    y = pr.coords()
+    ref = orp.jpass(pr.model, y, pr.z, x)
+    yd = torch.as_tensor(np.concatenate(y) if isinstance(y, tuple) else y).cuda()
+    gpu = jf.jpass(pr.model, torch.as_tensor(pr.z).cuda(), x, y=yd)
+    check_pass(gpu, ref)
+
+
+@pytest.mark.parametrize("name,make", CASES, ids=[c[0] for c in CASES])
+def test_residual_pass_matches_oracle(name, make):
+    pr = make()
+    x = _x_near(pr, 2)
+    cr, badr = orp.residual_pass(pr.model, pr.coords(), pr.z, x)
+    kw = dict(grid=pr.grid) if pr.grid is not None else dict(y=pr.t)
+    c, bad = jf.residual_pass(pr.model, pr.z, x, **kw)
+    assert bad == badr and abs(c - cr) <= TOL * cr
+
+
+def test_nonfinite_counts_and_weighted_pass():
+    pr = dg.make_gauss1d(50_000)
+    z = pr.z.copy()
+    z[[5, 40_000, 49_999]] = np.nan
+    _, _, _, bad = jf.jpass(pr.model, z, pr.p0, y=pr.t)
+    c, bad2 = jf.residual_pass(pr.model, z, pr.p0, y=pr.t)
+    assert bad == 3 and bad2 == 3 and not np.isfinite(c)
+    sig = np.random.default_rng(1).uniform(0.5, 2.0, pr.m)
+    ref = orp.jpass(pr.model, pr.t, pr.z, pr.p0, sigma=sig)
+    check_pass(jf.jpass(pr.model, pr.z, pr.p0, y=pr.t, sigma=sig), ref)
+
+
+def test_pass_is_bitwise_deterministic():
+    pr = dg.make_gauss2d(512)
+    a = jf.jpass(pr.model, pr.z, pr.p0, grid=pr.grid)
+    b = jf.jpass(pr.model, pr.z, pr.p0, grid=pr.grid)
+    assert a[0] == b[0] and np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
+
+
+def test_pass_device_async_matches_sync():
+    pr = dg.make_gauss2d(300)
+    zd = torch.as_tensor(pr.z).cuda()
+    xd = torch.as_tensor(pr.p0).cuda()
+    kv = torch.zeros(37, dtype=torch.float64, device="cuda")
+    s = torch.cuda.current_stream()
+    jf.pass_device(pr.model, zd, xd, kv, grid=pr.grid, stream=s.cuda_stream)
+    torch.cuda.synchronize()
+    c, g, G, bad = jf.jpass(pr.model, pr.z, pr.p0, grid=pr.grid)
+    k = kv.cpu().numpy()
+    assert k[-2] * 0.5 == c and k[-1] == bad
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("xk", [0, 1])
+def test_full_size_T_pass_matches_oracle(xk):
+    """BASELINE target T (4096^2, seed 6) at the bench's launch configuration."""
+    pr = dg.make_gauss2d(4096, seed=6)
+    x = pr.p0 if xk == 0 else pr.truth
+    ref = orp.jpass(pr.model, pr.coords(), pr.z, x)
+    check_pass(jf.jpass(pr.model, torch.as_tensor(pr.z).cuda(), x, grid=pr.grid), ref)
+    cr, _ = orp.residual_pass(pr.model, pr.coords(), pr.z, x)
+    c, _ = jf.residual_pass(pr.model, pr.z, x, grid=pr.grid)
+    assert abs(c - cr) <= TOL * cr
+
+
+@pytest.mark.slow
+def test_full_size_C5_pass_matches_oracle_on_row_band():
+    """C5 (8192^2, n=13): the pass over a row band, as one rank of 8 sees it."""
+    W = 8192
+    pr = dg.make_gauss2d_x2(W, seed=5)
+    r0, r1 = dg.shard_rows(W, 8, 3)
+    z = pr.z[r0 * W:r1 * W]
+    X, Y = dg.grid_coords(W, r1 - r0, r0)
+    ref = orp.jpass(pr.model, (X, Y), z, pr.p0)
+    check_pass(jf.jpass(pr.model, torch.as_tensor(z).cuda(), pr.p0, grid=(W, r1 - r0, r0)), ref)

@@ -1,0 +1,32 @@
+"""Quick per-pass timing on the GPU (development aid; bench.py is the contract)."""
+import sys, time
+import numpy as np
+import torch
+sys.path.insert(0, ".")
+import datagen as dg
+import paper_2208_12187_b200 as jf
+
+W = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
+pr = dg.make_gauss2d(W, seed=6)
+z = torch.as_tensor(pr.z).cuda()
+x = torch.as_tensor(pr.p0).cuda()
+kv = torch.zeros(64, dtype=torch.float64, device="cuda")
+s = torch.cuda.current_stream()
+for ro in (False, True):
+    for _ in range(3):
+        jf.pass_device(pr.model, z, x, kv, grid=pr.grid, stream=s.cuda_stream, residual_only=ro)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    N = 50
+    e0.record()
+    for _ in range(N):
+        jf.pass_device(pr.model, z, x, kv, grid=pr.grid, stream=s.cuda_stream, residual_only=ro)
+    e1.record(); torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) / N
+    print(f"{'r' if ro else 'J'}-pass W={W}: {t*1e3:.1f} us  {pr.m/t/1e3:.3e} pts/s")
+for mode in ("graph", "hostloop"):
+    for i in range(4):
+        torch.cuda.synchronize(); t0 = time.perf_counter()
+        r = jf.curve_fit(pr.model, z, p0=pr.p0, grid=pr.grid, use_graph=(mode == "graph"))
+        torch.cuda.synchronize(); t1 = time.perf_counter()
+    print(mode, "fit", r.status, r.nfev, r.njev, r.cost, f"{(t1-t0)*1e3:.3f} ms", r.kernel_launches)
