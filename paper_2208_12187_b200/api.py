@@ -123,6 +123,8 @@ class FitResult:
     kernel_launches: int
     t_upload_s: float
     t_solve_s: float
+    t_epilogue_s: float
+    epilogue_cycles: tuple = ()
     trace: np.ndarray = field(default_factory=lambda: np.zeros((0, L.JF_TRACE_FIELDS)))
 
 
@@ -151,7 +153,8 @@ def curve_fit(model, z, y=None, *, grid=None, p0=None, lb=None, ub=None, sigma=N
         x=np.array(res.x[:n]), cost=res.cost, optimality=res.optimality, grad=np.array(res.grad[:n]),
         gram=np.array(res.gram[: n * n]).reshape(n, n), status=res.status, nfev=res.nfev, njev=res.njev,
         nit=res.nit, active_mask=np.array(res.active_mask[:n], dtype=np.int64),
-        kernel_launches=res.kernel_launches, t_upload_s=res.t_upload_s, t_solve_s=res.t_solve_s)
+        kernel_launches=res.kernel_launches, t_upload_s=res.t_upload_s, t_solve_s=res.t_solve_s,
+        t_epilogue_s=res.t_epilogue_s, epilogue_cycles=tuple(res.epilogue_cycles))
     if tr is not None:
         out.trace = tr[: res.trace_len].copy()
     return out
@@ -225,6 +228,21 @@ def trust_region_step(hatG, hatg, m, Delta, alpha=0.0, device=0):
     return p, a.value, it.value
 
 
+def exchange_handles(blob: bytes, dist) -> bytes:
+    """All-gather one fixed-size byte blob per rank (rank order) through a
+    torch.distributed process group; returns the concatenation."""
+    import torch
+    n = len(blob)
+    t = torch.frombuffer(bytearray(blob), dtype=torch.uint8).clone()
+    if dist.get_backend() == "nccl":
+        t = t.cuda()
+    out = [torch.zeros_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, t)
+    res = b"".join(bytes(o.cpu().numpy().tobytes()) for o in out)
+    assert len(res) == n * dist.get_world_size()
+    return res
+
+
 class Comm:
     """jf_comm: one rank's mailbox for the in-kernel cross-GPU combine."""
 
@@ -261,6 +279,16 @@ class Comm:
         rc = self._lib.jf_comm_connect(self.handle, all_handles)
         if rc < 0:
             raise JFError(rc, "jf_comm_connect")
+
+    @classmethod
+    def from_process_group(cls, rank: int, world: int, device: int, dist=None) -> "Comm":
+        """Create this rank's mailbox and connect to every peer, exchanging the
+        IPC handles through torch.distributed (any backend)."""
+        if dist is None:
+            import torch.distributed as dist
+        c = cls.create(rank, world, device)
+        c.connect(exchange_handles(c.export(), dist))
+        return c
 
     def destroy(self):
         if self.handle:

@@ -23,6 +23,17 @@
 
 using namespace jf;
 
+// A rank's view of the multi-GPU mailboxes (jf.h jf_comm_*).
+struct jf_comm {
+  int rank = 0, nranks = 1, device = 0;
+  unsigned long long epoch = 0;
+  void* mbox = nullptr;           // local mailbox (device)
+  bool owns_mbox = true;
+  bool local = false;             // created by jf_comm_create_local
+  void* peer[8] = {nullptr};      // mapped mailboxes of all ranks
+  bool opened[8] = {false};
+};
+
 namespace {
 
 Kernels get_kernels(int model, int coord) {
@@ -68,9 +79,10 @@ int model_d(int model) {
   } while (0)
 
 struct GraphKey {
-  int model, coord, policy, grid;
+  const void* jk;
+  int policy, jgrid, rgrid;
   bool operator<(const GraphKey& o) const {
-    return std::tie(model, coord, policy, grid) < std::tie(o.model, o.coord, o.policy, o.grid);
+    return std::tie(jk, policy, jgrid, rgrid) < std::tie(o.jk, o.policy, o.jgrid, o.rgrid);
   }
 };
 
@@ -92,11 +104,13 @@ struct Ctx {
   int trace_cap = 0;
   double* d_in = nullptr;  // staged host inputs
   size_t in_cap = 0;
-  std::map<int, int> occ;  // model*16+coord -> blocks/SM of the J kernel
+  std::map<const void*, int> occ;  // kernel -> resident blocks/SM
   std::map<GraphKey, cudaGraphExec_t> graphs;
 };
 
-Ctx g_ctx[64];
+// Contexts: [0, 64) one per device; [64, 64 + 64*8) per (device, virtual rank)
+// of a jf_comm_create_local emulation, so emulated ranks run concurrently.
+Ctx g_ctx[64 + 64 * 8];
 
 int ctx_init(Ctx& c, int dev) {
   if (c.ready) return 0;
@@ -118,36 +132,45 @@ int ctx_init(Ctx& c, int dev) {
   return 0;
 }
 
-int grid_for(Ctx& c, int model, int coord, const Kernels& k, int64_t m) {
-  const int key = model * 16 + coord;
-  auto it = c.occ.find(key);
+// The grid of a pass kernel: enough blocks to fill every SM at the kernel's
+// occupancy, fewer for small m.  A pure function of (kernel, m): fixed
+// reduction order, bitwise reproducible passes (H4).
+int grid_for(Ctx& c, KernelFn f, int tpb, int64_t m) {
+  auto it = c.occ.find((const void*)f);
   int occ;
   if (it == c.occ.end()) {
     occ = 1;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k.jk, BLOCK, 0) != cudaSuccess || occ < 1) occ = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, tpb, 0) != cudaSuccess || occ < 1) occ = 1;
     if (occ > 4) occ = 4;
-    c.occ[key] = occ;
+    c.occ[(const void*)f] = occ;
   } else {
     occ = it->second;
   }
-  const int64_t need = (m + BLOCK - 1) / BLOCK;
+  const int64_t need = (m + tpb - 1) / tpb;
   int64_t g = (int64_t)c.nsm * occ;
   if (need < g) g = need;
   if (g < 1) g = 1;
   return (int)g;
 }
 
-}  // namespace
-
-struct jf_comm {
-  int rank = 0, nranks = 1, device = 0;
-  unsigned long long epoch = 0;
-  void* mbox = nullptr;           // local mailbox (device)
-  bool owns_mbox = true;
-  bool local = false;             // created by jf_comm_create_local
-  void* peer[8] = {nullptr};      // mapped mailboxes of all ranks
-  bool opened[8] = {false};
+// The two pass kernels a call uses, with their launch shapes.
+struct PassPair {
+  KernelFn j = nullptr, r = nullptr;
+  int jtpb = 256, rtpb = 256, jgrid = 1, rgrid = 1;
 };
+
+PassPair select_pass(Ctx& c, const Kernels& k, bool weighted, int64_t m) {
+  PassPair p;
+  p.j = weighted ? k.jkw : k.jk;
+  p.r = weighted ? k.rkw : k.rk;
+  p.jtpb = k.jtpb;
+  p.rtpb = k.rtpb;
+  p.jgrid = grid_for(c, p.j, p.jtpb, m);
+  p.rgrid = grid_for(c, p.r, p.rtpb, m);
+  return p;
+}
+
+}  // namespace
 
 namespace {
 
@@ -271,7 +294,8 @@ struct Lock {
 
 int acquire(const jf_opts& o, Ctx*& c, std::unique_lock<std::mutex>& lk, cudaStream_t& s) {
   if (o.device < 0 || o.device >= 64) return JF_EINVAL;
-  c = &g_ctx[o.device];
+  if (o.comm && o.comm->local) c = &g_ctx[64 + o.device * 8 + o.comm->rank];
+  else c = &g_ctx[o.device];
   lk = std::unique_lock<std::mutex>(c->mu);
   if (cudaSetDevice(o.device) != cudaSuccess) return JF_ECUDA;
   int r = ctx_init(*c, o.device);
@@ -309,14 +333,14 @@ void active_mask_host(const double* x, const double* lb, const double* ub, int n
   }
 }
 
-int launch_pass(const Kernels& k, bool jac, int grid, cudaStream_t s, PassArgs* d_args, FitState* d_state) {
-  KernelFn f = jac ? k.jk : k.rk;
-  f<<<grid, BLOCK, 0, s>>>(d_args, d_state, (cudaGraphConditionalHandle)0, 0);
+int launch_pass(const PassPair& k, bool jac, cudaStream_t s, PassArgs* d_args, FitState* d_state) {
+  KernelFn f = jac ? k.j : k.r;
+  f<<<jac ? k.jgrid : k.rgrid, jac ? k.jtpb : k.rtpb, 0, s>>>(d_args, d_state, (cudaGraphConditionalHandle)0, 0);
   CK(cudaGetLastError());
   return 0;
 }
 
-int build_graph(Ctx& c, const Kernels& k, int grid, int policy, cudaGraphExec_t* out) {
+int build_graph(Ctx& c, const PassPair& k, int policy, cudaGraphExec_t* out) {
   cudaGraph_t g;
   CK(cudaGraphCreate(&g, 0));
   cudaGraphConditionalHandle h;
@@ -335,16 +359,18 @@ int build_graph(Ctx& c, const Kernels& k, int grid, int policy, cudaGraphExec_t*
   void* args[4] = {&pa, &st, &h, &use};
   cudaKernelNodeParams kp;
   memset(&kp, 0, sizeof(kp));
-  kp.gridDim = dim3(grid);
-  kp.blockDim = dim3(BLOCK);
   kp.sharedMemBytes = 0;
   kp.kernelParams = args;
   cudaGraphNode_t prev = nullptr;
   if (policy == JF_POLICY_CONSERVATIVE) {
-    kp.func = (void*)k.rk;
+    kp.func = (void*)k.r;
+    kp.gridDim = dim3(k.rgrid);
+    kp.blockDim = dim3(k.rtpb);
     CK(cudaGraphAddKernelNode(&prev, body, nullptr, 0, &kp));
   }
-  kp.func = (void*)k.jk;
+  kp.func = (void*)k.j;
+  kp.gridDim = dim3(k.jgrid);
+  kp.blockDim = dim3(k.jtpb);
   cudaGraphNode_t jn;
   CK(cudaGraphAddKernelNode(&jn, body, prev ? &prev : nullptr, prev ? 1 : 0, &kp));
   CK(cudaGraphInstantiate(out, g, 0));
@@ -411,9 +437,9 @@ static int pass_common(int32_t model, const double* y, const double* z, int64_t 
   Staged sg;
   r = stage_inputs(*c, s, model, y, z, m, o, sg);
   if (r) return r;
-  Kernels k = get_kernels(model, sg.coord);
-  if (!k.jk) return JF_EINVAL;
-  const int grid = grid_for(*c, model, sg.coord, k, m);
+  Kernels kk = get_kernels(model, sg.coord);
+  if (!kk.jk) return JF_EINVAL;
+  const PassPair k = select_pass(*c, kk, sg.wsig != nullptr, m);
   PassArgs a;
   fill_args(a, sg, m, o);
   a.epilogue = EPI_NONE;
@@ -432,7 +458,7 @@ static int pass_common(int32_t model, const double* y, const double* z, int64_t 
     o.comm->epoch += 1;
   }
   CK(cudaMemcpyAsync(c->d_args, &a, sizeof(a), cudaMemcpyHostToDevice, s));
-  r = launch_pass(k, !residual_only, grid, s, c->d_args, c->d_state);
+  r = launch_pass(k, !residual_only, s, c->d_args, c->d_state);
   if (r) return r;
   if (host_out) {
     const int KS = residual_only ? 2 : tri_count(n) + 1;
@@ -528,9 +554,9 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
   r = stage_inputs(*c, s, model, y, z, m, o, sg);
   if (r) return fail(r);
   out->t_upload_s = sg.upload_s;
-  Kernels k = get_kernels(model, sg.coord);
-  if (!k.jk) return fail(JF_EINVAL);
-  const int grid = grid_for(*c, model, sg.coord, k, m);
+  Kernels kk = get_kernels(model, sg.coord);
+  if (!kk.jk) return fail(JF_EINVAL);
+  const PassPair k = select_pass(*c, kk, sg.wsig != nullptr, m);
 
   // trace buffer
   if (o.trace_cap > 0) {
@@ -585,11 +611,11 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
   CK(cudaMemcpyAsync(c->d_args, &a, sizeof(a), cudaMemcpyHostToDevice, s));
   int launches = 0;
   if (o.use_graph) {
-    GraphKey key{model, sg.coord, o.policy, grid};
+    GraphKey key{(const void*)k.j, o.policy, k.jgrid, k.rgrid};
     auto it = c->graphs.find(key);
     cudaGraphExec_t ge;
     if (it == c->graphs.end()) {
-      r = build_graph(*c, k, grid, o.policy, &ge);
+      r = build_graph(*c, k, o.policy, &ge);
       if (r) return fail(r);
       c->graphs[key] = ge;
     } else {
@@ -602,7 +628,7 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
     const int cap = 4 * h.max_nfev + 8;
     for (int iter = 0; iter < cap; ++iter) {
       const bool jac = (o.policy == JF_POLICY_CONSERVATIVE) ? (h.phase != PH_TRIAL_R) : true;
-      r = launch_pass(k, jac, grid, s, c->d_args, c->d_state);
+      r = launch_pass(k, jac, s, c->d_args, c->d_state);
       if (r) return fail(r);
       CK(cudaMemcpyAsync(&h, c->d_state, sizeof(h), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
@@ -615,6 +641,8 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
 
   // ---- result
   out->kernel_launches = launches;
+  out->t_epilogue_s = h.epi_ns * 1e-9;
+  for (int q = 0; q < 4; ++q) out->epilogue_cycles[q] = (double)h.prof[q];
   out->nfev = h.nfev;
   out->njev = h.njev;
   out->nit = h.nit;
@@ -659,7 +687,7 @@ __global__ void tr_step_kernel(const double* hatG, const double* hatg, int n, in
   }
   __syncwarp();
   double lam;
-  warp_eig(S, n, lane, lam);
+  warp_eig(S, n, lane, lam, 0);
   const double g = lane < n ? hatg[lane] : 0.0;
   const double suf = wVtx(S.V, g, n, lane);
   double alpha = alpha_in, p;

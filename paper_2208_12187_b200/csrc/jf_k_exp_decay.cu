@@ -3,8 +3,16 @@
 #include "jf_pass.cuh"
 
 namespace jf {
-Kernels kernels_exp_decay(int coord) {
-  if (coord == COORD_EXPLICIT) return Kernels{pass_kernel<ModelExpDecay, true, COORD_EXPLICIT>, pass_kernel<ModelExpDecay, false, COORD_EXPLICIT>};
-  return Kernels{pass_kernel<ModelExpDecay, true, COORD_IMPLICIT_T>, pass_kernel<ModelExpDecay, false, COORD_IMPLICIT_T>};
+template <int C>
+static Kernels make() {
+  Kernels k;
+  k.jk = pass_kernel<ModelExpDecay, true, C, false>;
+  k.rk = pass_kernel<ModelExpDecay, false, C, false>;
+  k.jkw = pass_kernel<ModelExpDecay, true, C, true>;
+  k.rkw = pass_kernel<ModelExpDecay, false, C, true>;
+  k.jtpb = PassCfg<ModelExpDecay, true>::TPB;
+  k.rtpb = PassCfg<ModelExpDecay, false>::TPB;
+  return k;
 }
+Kernels kernels_exp_decay(int coord) { return coord == COORD_EXPLICIT ? make<COORD_EXPLICIT>() : make<COORD_IMPLICIT_T>(); }
 }  // namespace jf

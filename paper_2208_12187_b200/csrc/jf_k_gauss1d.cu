@@ -3,8 +3,16 @@
 #include "jf_pass.cuh"
 
 namespace jf {
-Kernels kernels_gauss1d(int coord) {
-  if (coord == COORD_EXPLICIT) return Kernels{pass_kernel<ModelGauss1D, true, COORD_EXPLICIT>, pass_kernel<ModelGauss1D, false, COORD_EXPLICIT>};
-  return Kernels{pass_kernel<ModelGauss1D, true, COORD_IMPLICIT_T>, pass_kernel<ModelGauss1D, false, COORD_IMPLICIT_T>};
+template <int C>
+static Kernels make() {
+  Kernels k;
+  k.jk = pass_kernel<ModelGauss1D, true, C, false>;
+  k.rk = pass_kernel<ModelGauss1D, false, C, false>;
+  k.jkw = pass_kernel<ModelGauss1D, true, C, true>;
+  k.rkw = pass_kernel<ModelGauss1D, false, C, true>;
+  k.jtpb = PassCfg<ModelGauss1D, true>::TPB;
+  k.rtpb = PassCfg<ModelGauss1D, false>::TPB;
+  return k;
 }
+Kernels kernels_gauss1d(int coord) { return coord == COORD_EXPLICIT ? make<COORD_EXPLICIT>() : make<COORD_IMPLICIT_T>(); }
 }  // namespace jf

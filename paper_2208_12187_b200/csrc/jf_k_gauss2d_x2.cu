@@ -3,8 +3,16 @@
 #include "jf_pass.cuh"
 
 namespace jf {
-Kernels kernels_gauss2d_x2(int coord) {
-  if (coord == COORD_EXPLICIT) return Kernels{pass_kernel<ModelGauss2DRotX2, true, COORD_EXPLICIT>, pass_kernel<ModelGauss2DRotX2, false, COORD_EXPLICIT>};
-  return Kernels{pass_kernel<ModelGauss2DRotX2, true, COORD_GRID>, pass_kernel<ModelGauss2DRotX2, false, COORD_GRID>};
+template <int C>
+static Kernels make() {
+  Kernels k;
+  k.jk = pass_kernel<ModelGauss2DRotX2, true, C, false>;
+  k.rk = pass_kernel<ModelGauss2DRotX2, false, C, false>;
+  k.jkw = pass_kernel<ModelGauss2DRotX2, true, C, true>;
+  k.rkw = pass_kernel<ModelGauss2DRotX2, false, C, true>;
+  k.jtpb = PassCfg<ModelGauss2DRotX2, true>::TPB;
+  k.rtpb = PassCfg<ModelGauss2DRotX2, false>::TPB;
+  return k;
 }
+Kernels kernels_gauss2d_x2(int coord) { return coord == COORD_EXPLICIT ? make<COORD_EXPLICIT>() : make<COORD_GRID>(); }
 }  // namespace jf

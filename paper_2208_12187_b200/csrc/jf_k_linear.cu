@@ -3,8 +3,16 @@
 #include "jf_pass.cuh"
 
 namespace jf {
-Kernels kernels_linear(int coord) {
-  if (coord == COORD_EXPLICIT) return Kernels{pass_kernel<ModelLinear, true, COORD_EXPLICIT>, pass_kernel<ModelLinear, false, COORD_EXPLICIT>};
-  return Kernels{pass_kernel<ModelLinear, true, COORD_IMPLICIT_T>, pass_kernel<ModelLinear, false, COORD_IMPLICIT_T>};
+template <int C>
+static Kernels make() {
+  Kernels k;
+  k.jk = pass_kernel<ModelLinear, true, C, false>;
+  k.rk = pass_kernel<ModelLinear, false, C, false>;
+  k.jkw = pass_kernel<ModelLinear, true, C, true>;
+  k.rkw = pass_kernel<ModelLinear, false, C, true>;
+  k.jtpb = PassCfg<ModelLinear, true>::TPB;
+  k.rtpb = PassCfg<ModelLinear, false>::TPB;
+  return k;
 }
+Kernels kernels_linear(int coord) { return coord == COORD_EXPLICIT ? make<COORD_EXPLICIT>() : make<COORD_IMPLICIT_T>(); }
 }  // namespace jf

@@ -8,8 +8,11 @@ namespace jf {
 struct FitState;
 using KernelFn = void (*)(const PassArgs*, FitState*, cudaGraphConditionalHandle, int);
 struct Kernels {
-  KernelFn jk = nullptr;  // J-pass (value + dual Jacobian + fused Gram)
-  KernelFn rk = nullptr;  // residual-only pass
+  KernelFn jk = nullptr;   // J-pass (value + dual Jacobian + fused Gram)
+  KernelFn rk = nullptr;   // residual-only pass
+  KernelFn jkw = nullptr;  // weighted variants (App. C)
+  KernelFn rkw = nullptr;
+  int jtpb = 256, rtpb = 256;  // threads per block of the J / r kernels
 };
 Kernels kernels_linear(int coord);
 Kernels kernels_exp_decay(int coord);

@@ -29,7 +29,7 @@ __device__ __forceinline__ auto param(double v) {
 
 // ---------------------------------------------------------------- LINEAR (n=2)
 struct ModelLinear {
-  static constexpr int N = 2, D = 1;
+  static constexpr int N = 2, D = 1, CONST_COL = 1;
   struct Pre {
     double x0, x1;
   };
@@ -43,7 +43,7 @@ struct ModelLinear {
 
 // ------------------------------------------------------------ EXP_DECAY (n=3)
 struct ModelExpDecay {
-  static constexpr int N = 3, D = 1;
+  static constexpr int N = 3, D = 1, CONST_COL = 2;
   struct Pre {
     double a, b, c;
   };
@@ -66,7 +66,7 @@ struct PreGauss1D {
   TI inv2s2;  // 1 / (2 s^2), a dual in s
 };
 struct ModelGauss1D {
-  static constexpr int N = 4, D = 1;
+  static constexpr int N = 4, D = 1, CONST_COL = 3;
   template <bool JAC>
   __device__ __forceinline__ static auto prologue(const double* x) {
     const auto s = param<JAC, N, 2>(x[2]);
@@ -125,7 +125,7 @@ struct Gauss2DComponent {
 };
 
 struct ModelGauss2DRot {
-  static constexpr int N = 7, D = 2;
+  static constexpr int N = 7, D = 2, CONST_COL = 6;
   using G = Gauss2DComponent<N, 0>;
   template <class P>
   struct Pre {
@@ -145,7 +145,7 @@ struct ModelGauss2DRot {
 
 // ---------------------------------------------------- GAUSS2D_ROT_X2 (n=13)
 struct ModelGauss2DRotX2 {
-  static constexpr int N = 13, D = 2;
+  static constexpr int N = 13, D = 2, CONST_COL = 12;
   using G1 = Gauss2DComponent<N, 0>;
   using G2 = Gauss2DComponent<N, 6>;
   template <class P1, class P2>

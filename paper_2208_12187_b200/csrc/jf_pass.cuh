@@ -45,12 +45,15 @@ struct MinBlocks {
   static constexpr int value = Model::N <= 7 ? 2 : 1;
 };
 
-// Accumulate one point's contribution.
+// Accumulate one point's contribution.  CONST_COL: a parameter whose partial
+// is identically 1 (the offset); unweighted, its diagonal slot is the point
+// count, kept as an integer instead of an fp64 add per point.
 template <class Model, bool JAC, class H>
-__device__ __forceinline__ void accumulate(double (&acc)[PassShape<Model, JAC>::KT], int& bad, const H& h, double z,
-                                           double wsig, bool weighted) {
+__device__ __forceinline__ void accumulate(double (&acc)[PassShape<Model, JAC>::KT], int& bad, int& cnt,
+                                           const H& h, double z, double wsig, bool weighted) {
   constexpr int N = Model::N;
   if constexpr (JAC) {
+    constexpr int CC = Model::CONST_COL;
     double w[N + 1];
     static_for<N>([&](auto J) {
       constexpr int j = decltype(J)::value;
@@ -62,12 +65,17 @@ __device__ __forceinline__ void accumulate(double (&acc)[PassShape<Model, JAC>::
       for (int j = 0; j <= N; ++j) w[j] *= wsig;  // App. C Eq. C13-C16
     }
     bad += isfinite(w[N]) ? 0 : 1;
+    ++cnt;
     int s = 0;
 #pragma unroll
     for (int j = 0; j <= N; ++j) {
 #pragma unroll
       for (int k = j; k <= N; ++k) {
-        acc[s] = fma(w[j], w[k], acc[s]);
+        if (j == CC && k == CC) {
+          if (weighted) acc[s] = fma(w[j], w[k], acc[s]);
+        } else {
+          acc[s] = fma(w[j], w[k], acc[s]);
+        }
         ++s;
       }
     }
@@ -80,9 +88,10 @@ __device__ __forceinline__ void accumulate(double (&acc)[PassShape<Model, JAC>::
 }
 
 // Block-level combine of per-thread accumulators into partials[blockIdx.x].
-template <int KT>
+template <int KT, int TPB>
 __device__ __forceinline__ void block_partial(double (&acc)[KT], int bad, double* __restrict__ part,
                                               double (*red)[KT + 1]) {
+  constexpr int NW = TPB / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int k = 0; k < KT; ++k) {
@@ -94,19 +103,19 @@ __device__ __forceinline__ void block_partial(double (&acc)[KT], int bad, double
   const int b = __reduce_add_sync(FULL, bad);
   if (lane == 0) red[warp][KT] = (double)b;
   __syncthreads();
-  for (int k = threadIdx.x; k < KT + 1; k += BLOCK) {
+  for (int k = threadIdx.x; k < KT + 1; k += TPB) {
     double s = 0.0;
 #pragma unroll
-    for (int w = 0; w < NWARP; ++w) s += red[w][k];
+    for (int w = 0; w < NW; ++w) s += red[w][k];
     part[(size_t)blockIdx.x * (KT + 1) + k] = s;
   }
 }
 
 // Last-block deterministic sum over the grid's partials; result in out[0..KS).
-template <int KS>
+template <int KS, int TPB>
 __device__ __forceinline__ void grid_combine(const double* __restrict__ part, int nblk, double* out,
-                                             double* scratch /* BLOCK doubles */) {
-  constexpr int NSEG = (BLOCK / KS) > 0 ? (BLOCK / KS) : 1;
+                                             double* scratch /* TPB doubles */) {
+  constexpr int NSEG = (TPB / KS) > 0 ? (TPB / KS) : 1;
   const int t = threadIdx.x;
   if (t < NSEG * KS) {
     const int k = t % KS, seg = t / KS;
@@ -115,7 +124,7 @@ __device__ __forceinline__ void grid_combine(const double* __restrict__ part, in
     scratch[seg * KS + k] = s;
   }
   __syncthreads();
-  for (int k = t; k < KS; k += BLOCK) {
+  for (int k = t; k < KS; k += TPB) {
     double s = 0.0;
 #pragma unroll
     for (int seg = 0; seg < NSEG; ++seg) s += scratch[seg * KS + k];
@@ -125,14 +134,14 @@ __device__ __forceinline__ void grid_combine(const double* __restrict__ part, in
 }
 
 // Cross-rank combine through the NVLink mailboxes (see jf_comm.cu).
-template <int KS>
+template <int KS, int TPB>
 __device__ __forceinline__ bool comm_combine(const CommDev& cm, unsigned long long epoch, double* vec /* smem */) {
   const int R = cm.nranks, me = cm.rank;
   const int par = (int)(epoch & 1ull);
   // 1. push my vector into slot [par][me] of every mailbox (peer stores over NVLink)
   for (int p = 0; p < R; ++p) {
     double* dst = cm.mbox_data[p] + ((size_t)par * R + me) * KMAX;
-    for (int k = threadIdx.x; k < KS; k += BLOCK) dst[k] = vec[k];
+    for (int k = threadIdx.x; k < KS; k += TPB) dst[k] = vec[k];
   }
   __threadfence_system();
   __syncthreads();
@@ -161,7 +170,7 @@ __device__ __forceinline__ bool comm_combine(const CommDev& cm, unsigned long lo
   if (timed_out) return false;
   // 4. sum in rank order (identical on every rank)
   const double* box = cm.mbox_data[me] + (size_t)par * R * KMAX;
-  for (int k = threadIdx.x; k < KS; k += BLOCK) {
+  for (int k = threadIdx.x; k < KS; k += TPB) {
     double s = 0.0;
     for (int p = 0; p < R; ++p) s += __ldcv(box + (size_t)p * KMAX + k);
     vec[k] = s;
@@ -170,23 +179,21 @@ __device__ __forceinline__ bool comm_combine(const CommDev& cm, unsigned long lo
   return true;
 }
 
-// Per-thread point iterator over the shard: index i and its coordinates.
-template <int D, int COORD>
+// Per-thread point iterator over the shard: index i and, for the implicit
+// pixel grid, (row, col) maintained incrementally (no division per point).
+template <int COORD>
 struct PointIter {
   int64_t i, S;
-  // grid state
-  int64_t row, col, dr, dc, W;
-  double row0d;
+  int32_t row, col, dr, dc, W;
   __device__ __forceinline__ void init(const PassArgs& a, int64_t i0, int64_t stride) {
     i = i0;
     S = stride;
     if constexpr (COORD == COORD_GRID) {
-      W = a.W;
-      row = i0 / W;
-      col = i0 - row * W;
-      dr = stride / W;
-      dc = stride - dr * W;
-      row0d = (double)a.row0;
+      W = (int32_t)a.W;
+      row = (int32_t)(i0 / a.W);
+      col = (int32_t)(i0 - (int64_t)row * a.W);
+      dr = (int32_t)(stride / a.W);
+      dc = (int32_t)(stride - (int64_t)dr * a.W);
     }
   }
   __device__ __forceinline__ void advance() {
@@ -202,13 +209,25 @@ struct PointIter {
   }
 };
 
-// The pass kernel.  st != nullptr and epilogue == EPI_FIT: part of a fit.
-template <class Model, bool JAC, int COORD>
-__global__ void __launch_bounds__(BLOCK, MinBlocks<Model>::value)
+// Launch shape per (model, pass): points per thread per iteration (ILP) and
+// minimum resident blocks per SM (register budget).
+template <class Model, bool JAC>
+struct PassCfg {
+  static constexpr bool BIG = JAC && Model::N >= 7;
+  static constexpr int P = JAC ? (Model::N == 7 ? 2 : 1) : 4;
+  static constexpr int TPB = (JAC && Model::N == 7) ? 384 : 256;
+  static constexpr int MINB = BIG ? 1 : 2;
+};
+
+// The pass kernel.  epilogue == EPI_FIT: one pass of a fit (st is the state).
+template <class Model, bool JAC, int COORD, bool WGT>
+__global__ void __launch_bounds__((PassCfg<Model, JAC>::TPB), (PassCfg<Model, JAC>::MINB))
     pass_kernel(const PassArgs* __restrict__ pa, FitState* __restrict__ st, cudaGraphConditionalHandle cond,
                 int use_cond) {
   using Sh = PassShape<Model, JAC>;
   constexpr int KT = Sh::KT, KS = Sh::KS;
+  constexpr int P = PassCfg<Model, JAC>::P;
+  constexpr int TPB = PassCfg<Model, JAC>::TPB;
   const PassArgs& a = *pa;
 
   // Phase predication inside a fit: run only when this pass type is wanted.
@@ -226,58 +245,93 @@ __global__ void __launch_bounds__(BLOCK, MinBlocks<Model>::value)
   double acc[KT];
 #pragma unroll
   for (int k = 0; k < KT; ++k) acc[k] = 0.0;
-  int bad = 0;
+  int bad = 0, cnt = 0;
 
   const int64_t m = a.m;
-  const int64_t stride = (int64_t)gridDim.x * BLOCK;
-  PointIter<Model::D, COORD> it;
-  it.init(a, (int64_t)blockIdx.x * BLOCK + threadIdx.x, stride);
+  const int64_t S = (int64_t)gridDim.x * TPB;
+  PointIter<COORD> it;
+  it.init(a, (int64_t)blockIdx.x * TPB + threadIdx.x, S);
   const double* __restrict__ z = a.z;
   const double* __restrict__ y0 = a.y0;
   const double* __restrict__ y1 = a.y1;
   const double* __restrict__ ws = a.wsig;
-  const bool weighted = ws != nullptr;
-  for (; it.i < m; it.advance()) {
-    const int64_t i = it.i;
-    const double zi = __ldg(z + i);
-    const double wi = weighted ? __ldg(ws + i) : 1.0;
-    if constexpr (Model::D == 1) {
-      double t;
-      if constexpr (COORD == COORD_IMPLICIT_T) t = fma((double)(a.index0 + i), a.dt, a.t0);
-      else t = __ldg(y0 + i);
-      const auto h = Model::template point<JAC>(pre, t);
-      accumulate<Model, JAC>(acc, bad, h, zi, wi, weighted);
-    } else {
-      double X, Y;
-      if constexpr (COORD == COORD_GRID) {
-        X = (double)it.col;
-        Y = (double)it.row + it.row0d;
-      } else {
-        X = __ldg(y0 + i);
-        Y = __ldg(y1 + i);
+  constexpr bool weighted = WGT;
+  constexpr bool EXPL = (COORD == COORD_EXPLICIT);
+  constexpr bool TWO = (Model::D == 2);
+
+  // Software pipeline: the loads of the next group of P points are issued
+  // before the current group is computed, so HBM latency hides behind the
+  // fp64 work of the current points.
+  double qz[P], qw[P], qa[P], qb[P];
+  auto issue = [&](int64_t base) {
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const int64_t idx = base + p * S;
+      const bool v = idx < m;
+      qz[p] = v ? __ldg(z + idx) : 0.0;
+      qw[p] = (v && weighted) ? __ldg(ws + idx) : 1.0;
+      if constexpr (EXPL) {
+        qa[p] = v ? __ldg(y0 + idx) : 0.0;
+        if constexpr (TWO) qb[p] = v ? __ldg(y1 + idx) : 0.0;
       }
-      const auto h = Model::template point<JAC>(pre, X, Y);
-      accumulate<Model, JAC>(acc, bad, h, zi, wi, weighted);
+    }
+  };
+  issue(it.i);
+  while (it.i < m) {
+    double cz[P], cw[P], cx[P], cy[P];
+    bool cv[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      cv[p] = it.i < m;
+      cz[p] = qz[p];
+      cw[p] = qw[p];
+      if constexpr (EXPL) {
+        cx[p] = qa[p];
+        if constexpr (TWO) cy[p] = qb[p];
+      } else if constexpr (COORD == COORD_GRID) {
+        cx[p] = (double)it.col;
+        cy[p] = (double)(it.row + (int32_t)a.row0);
+      } else {
+        cx[p] = fma((double)(a.index0 + it.i), a.dt, a.t0);
+      }
+      it.advance();
+    }
+    issue(it.i);
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      if (P == 1 || cv[p]) {
+        if constexpr (TWO) {
+          const auto h = Model::template point<JAC>(pre, cx[p], cy[p]);
+          accumulate<Model, JAC>(acc, bad, cnt, h, cz[p], cw[p], weighted);
+        } else {
+          const auto h = Model::template point<JAC>(pre, cx[p]);
+          accumulate<Model, JAC>(acc, bad, cnt, h, cz[p], cw[p], weighted);
+        }
+      }
     }
   }
+  if constexpr (JAC) {
+    constexpr int CC = Model::CONST_COL;
+    if (!weighted) acc[tri_slot(Model::N, CC, CC)] = (double)cnt;
+  }
 
-  __shared__ double red[NWARP][KT + 1];
+  __shared__ double red[TPB / 32][KT + 1];
   __shared__ double vec[KMAX];
-  __shared__ double scratch[BLOCK];
+  __shared__ double scratch[TPB];
   __shared__ unsigned int is_last;
-  block_partial<KT>(acc, bad, a.partials, red);
+  block_partial<KT, TPB>(acc, bad, a.partials, red);
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) is_last = (atomicAdd(a.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
   __syncthreads();
   if (!is_last) return;
   __threadfence();
-  grid_combine<KS>(a.partials, gridDim.x, vec, scratch);
+  grid_combine<KS, TPB>(a.partials, gridDim.x, vec, scratch);
   if (threadIdx.x == 0) *a.ticket = 0u;  // ready for the next launch
 
   if (a.use_comm) {
     const unsigned long long epoch = (a.epilogue == EPI_FIT) ? (st->comm_epoch + 1) : (a.comm.epoch + 1);
-    const bool ok = comm_combine<KS>(a.comm, epoch, vec);
+    const bool ok = comm_combine<KS, TPB>(a.comm, epoch, vec);
     if (threadIdx.x == 0 && a.epilogue == EPI_FIT) st->comm_epoch = epoch;
     if (!ok) {
       if (threadIdx.x == 0 && a.epilogue == EPI_FIT) {
@@ -292,14 +346,31 @@ __global__ void __launch_bounds__(BLOCK, MinBlocks<Model>::value)
   }
 
   if (a.epilogue != EPI_FIT) {
-    for (int k = threadIdx.x; k < KS; k += BLOCK) a.out[k] = vec[k];
+    for (int k = threadIdx.x; k < KS; k += TPB) a.out[k] = vec[k];
     return;
   }
-  // ---- fit epilogue: one warp runs the solver state machine
+  // ---- fit epilogue: one warp runs the solver state machine on a shared-
+  // memory copy of the state (no global-latency chains), then writes it back.
   if (threadIdx.x < 32) {
     __shared__ SolverSmem S;
-    fit_after_pass(st, S, vec, JAC);
-    if (threadIdx.x == 0 && use_cond) cudaGraphSetConditional(cond, st->cont ? 1u : 0u);
+    __shared__ FitState sst;
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    constexpr int NW = sizeof(FitState) / 8;
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(st);
+    unsigned long long* dst = reinterpret_cast<unsigned long long*>(&sst);
+    for (int k = threadIdx.x; k < NW; k += 32) dst[k] = src[k];
+    __syncwarp();
+    fit_after_pass(&sst, S, vec, JAC);
+    __syncwarp();
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    if (threadIdx.x == 0) sst.epi_ns += (t1 - t0);
+    __syncwarp();
+    unsigned long long* back = reinterpret_cast<unsigned long long*>(st);
+    for (int k = threadIdx.x; k < NW; k += 32) back[k] = dst[k];
+    __syncwarp();
+    if (threadIdx.x == 0 && use_cond) cudaGraphSetConditional(cond, sst.cont ? 1u : 0u);
   }
 }
 

@@ -50,8 +50,10 @@ struct FitState {
   double* trace;
   // ---- iteration state
   int32_t phase, status, nfev, njev, nit, cont, error, trace_len;
-  int32_t full_rank, branch, launches, pad3;
+  int32_t full_rank, branch, launches, have_V;
   unsigned long long comm_epoch;
+  unsigned long long epi_ns;  // device time spent in the solver epilogue (globaltimer)
+  long long prof[4];          // SM cycles: eig, solve_tr, select_step, fit_after_pass
   double cost, cost_new, Delta, alpha, gnorm, theta, actual;
   double pred, hn, step_norm, Delta_used, ratio, pad4;
   double x[NMAX], x_eval[NMAX];
@@ -66,34 +68,35 @@ struct SolverSmem {
   double A[NMAX][NMAX + 1];
   double V[NMAX][NMAX + 1];
   double M[NMAX][NMAX + 1];  // scaled Gram (incl. diag_h) for quadratic forms
+  double T[NMAX][NMAX + 1];  // scratch
   double c[NMAX], e[NMAX];
   int partner[NMAX];
 };
 
 // ------------------------------------------------------------ warp helpers
-__device__ __forceinline__ double wsum(double v) {
+static __device__ __forceinline__ double wsum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
   return v;
 }
-__device__ __forceinline__ double wmin(double v) {
+static __device__ __forceinline__ double wmin(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(FULL, v, o));
   return v;
 }
-__device__ __forceinline__ double wmax(double v) {
+static __device__ __forceinline__ double wmax(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, o));
   return v;
 }
-__device__ __forceinline__ bool wall(bool b) { return __all_sync(FULL, b); }
-__device__ __forceinline__ bool wany(bool b) { return __any_sync(FULL, b); }
-__device__ __forceinline__ double lanev(double v, int src) { return __shfl_sync(FULL, v, src); }
-__device__ __forceinline__ double wdot(double a, double b) { return wsum(a * b); }
-__device__ __forceinline__ double wnorm(double a) { return sqrt(wsum(a * a)); }
+static __device__ __forceinline__ bool wall(bool b) { return __all_sync(FULL, b); }
+static __device__ __forceinline__ bool wany(bool b) { return __any_sync(FULL, b); }
+static __device__ __forceinline__ double lanev(double v, int src) { return __shfl_sync(FULL, v, src); }
+static __device__ __forceinline__ double wdot(double a, double b) { return wsum(a * b); }
+static __device__ __forceinline__ double wnorm(double a) { return sqrt(wsum(a * a)); }
 
 // y = M x for an n x n matrix in shared memory (row-major, stride NMAX+1).
-__device__ __forceinline__ double wmatvec(const double (*M)[NMAX + 1], double x, int n, int lane) {
+static __device__ __forceinline__ double wmatvec(const double (*M)[NMAX + 1], double x, int n, int lane) {
   double y = 0.0;
   for (int k = 0; k < n; ++k) {
     const double xk = lanev(x, k);
@@ -102,11 +105,11 @@ __device__ __forceinline__ double wmatvec(const double (*M)[NMAX + 1], double x,
   return lane < n ? y : 0.0;
 }
 // y = V x (V columns are eigenvectors)
-__device__ __forceinline__ double wVx(const double (*V)[NMAX + 1], double x, int n, int lane) {
+static __device__ __forceinline__ double wVx(const double (*V)[NMAX + 1], double x, int n, int lane) {
   return wmatvec(V, x, n, lane);
 }
 // y = V^T x
-__device__ __forceinline__ double wVtx(const double (*V)[NMAX + 1], double x, int n, int lane) {
+static __device__ __forceinline__ double wVtx(const double (*V)[NMAX + 1], double x, int n, int lane) {
   double y = 0.0;
   for (int k = 0; k < n; ++k) {
     const double xk = lanev(x, k);
@@ -115,11 +118,11 @@ __device__ __forceinline__ double wVtx(const double (*V)[NMAX + 1], double x, in
   return lane < n ? y : 0.0;
 }
 // s^T M s
-__device__ __forceinline__ double wquad(const double (*M)[NMAX + 1], double s, int n, int lane) {
+static __device__ __forceinline__ double wquad(const double (*M)[NMAX + 1], double s, int n, int lane) {
   return wdot(s, wmatvec(M, s, n, lane));
 }
 // u^T M v
-__device__ __forceinline__ double wbilin(const double (*M)[NMAX + 1], double u, double v, int n, int lane) {
+static __device__ __forceinline__ double wbilin(const double (*M)[NMAX + 1], double u, double v, int n, int lane) {
   return wdot(u, wmatvec(M, v, n, lane));
 }
 
@@ -128,14 +131,51 @@ __device__ __forceinline__ double wbilin(const double (*M)[NMAX + 1], double u, 
 // on return lam (lane j, j < n) holds the eigenvalues sorted descending and
 // the columns of S.V the matching orthonormal eigenvectors.  This is App. B's
 // SVD of the scaled Jacobian computed through its Gram matrix (c.1b).
-__device__ __noinline__ void warp_eig(SolverSmem& S, int n, int lane, double& lam_out) {
+//
+// warm != 0: S.V holds an orthogonal matrix V0 on entry (the previous
+// iterate's eigenvectors); the sweeps run on V0^T A V0, which is nearly
+// diagonal between consecutive iterations, and accumulate onto V0 — one or
+// two sweeps instead of six.  Rotations are skipped when
+// |a_pq| <= eps sqrt(|a_pp a_qq|) or |a_pq| <= 2^-60 max_i |a_ii|; the
+// sweep loop ends when a sweep applies none.
+static __device__ __noinline__ void warp_eig(SolverSmem& S, int n, int lane, double& lam_out, int warm) {
   const int N2 = (n + 1) & ~1;  // pad to even with a zero row / column
-  for (int e = lane; e < NMAX * NMAX; e += 32) {
-    const int i = e / NMAX, j = e % NMAX;
-    if (i >= n || j >= n) S.A[i][j] = 0.0;
-    S.V[i][j] = (i == j) ? 1.0 : 0.0;
+  if (!warm) {
+    for (int e = lane; e < NMAX * NMAX; e += 32) {
+      const int i = e / NMAX, j = e % NMAX;
+      if (i >= n || j >= n) S.A[i][j] = 0.0;
+      S.V[i][j] = (i == j) ? 1.0 : 0.0;
+    }
+    __syncwarp();
+  } else {
+    // T = A V0, then A = V0^T T (lane-parallel over elements)
+    for (int e = lane; e < n * n; e += 32) {
+      const int i = e / n, j = e % n;
+      double t = 0.0;
+      for (int k = 0; k < n; ++k) t = fma(S.A[i][k], S.V[k][j], t);
+      S.T[i][j] = t;
+    }
+    __syncwarp();
+    for (int e = lane; e < NMAX * NMAX; e += 32) {
+      const int i = e / NMAX, j = e % NMAX;
+      double t = 0.0;
+      if (i < n && j < n) {
+        for (int k = 0; k < n; ++k) t = fma(S.V[k][i], S.T[k][j], t);
+      }
+      S.A[i][j] = t;
+      if (i >= n || j >= n) S.V[i][j] = (i == j) ? 1.0 : 0.0;
+    }
+    __syncwarp();
+    // exact symmetry
+    for (int e = lane; e < n * n; e += 32) {
+      const int i = e / n, j = e % n;
+      if (i < j) S.A[j][i] = S.A[i][j];
+    }
+    __syncwarp();
   }
-  __syncwarp();
+  double amax = (lane < n) ? fabs(S.A[lane][lane]) : 0.0;
+  amax = wmax(amax);
+  const double abs_tol = amax * 8.673617379884035e-19;  // 2^-60
   for (int sweep = 0; sweep < 40; ++sweep) {
     bool rotated = false;
     for (int r = 0; r < N2 - 1; ++r) {
@@ -155,12 +195,14 @@ __device__ __noinline__ void warp_eig(SolverSmem& S, int n, int lane, double& la
           q = t;
         }
         const double apq = S.A[p][q], app = S.A[p][p], aqq = S.A[q][q];
-        double c = 1.0, s = 0.0, t = 0.0;
-        const bool tiny = fabs(apq) <= 1.1102230246251565e-16 * sqrt(fabs(app) * fabs(aqq)) || apq == 0.0;
+        double c = 1.0, s = 0.0;
+        const double aa = fabs(apq);
+        const bool tiny = aa <= abs_tol || aa <= 1.1102230246251565e-16 * sqrt(fabs(app) * fabs(aqq));
         if (!tiny) {
-          const double th = (aqq - app) / (2.0 * apq);
-          t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(fma(th, th, 1.0)));
-          c = 1.0 / sqrt(fma(t, t, 1.0));
+          // t = tan(phi), the smaller root: t = 2 apq sgn(d) / (|d| + sqrt(d^2 + 4 apq^2)), d = aqq - app
+          const double d = aqq - app;
+          const double t = (2.0 * apq) * (d >= 0.0 ? 1.0 : -1.0) / (fabs(d) + sqrt(fma(d, d, 4.0 * apq * apq)));
+          c = rsqrt(fma(t, t, 1.0));
           s = t * c;
           rotated = true;
         }
@@ -174,26 +216,35 @@ __device__ __noinline__ void warp_eig(SolverSmem& S, int n, int lane, double& la
       }
       __syncwarp();
       rotated = wany(rotated);
+      if (!rotated) continue;
       // write phase: A' = P^T A P, V' = V P (each lane owns up to 8 elements)
       double newA[8], newV[8];
       int cnt = 0;
-      for (int e = lane; e < N2 * N2; e += 32, ++cnt) {
-        const int i = e / N2, j = e % N2;
-        const int ib = S.partner[i], jb = S.partner[j];
-        const double ci = S.c[i], ei = S.e[i], cj = S.c[j], ej = S.e[j];
-        newA[cnt] = ci * (cj * S.A[i][j] + ej * S.A[i][jb]) + ei * (cj * S.A[ib][j] + ej * S.A[ib][jb]);
-        newV[cnt] = cj * S.V[i][j] + ej * S.V[i][jb];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int e = lane + 32 * k;
+        if (e < N2 * N2) {
+          const int i = e / N2, j = e % N2;
+          const int ib = S.partner[i], jb = S.partner[j];
+          const double ci = S.c[i], ei = S.e[i], cj = S.c[j], ej = S.e[j];
+          newA[k] = ci * (cj * S.A[i][j] + ej * S.A[i][jb]) + ei * (cj * S.A[ib][j] + ej * S.A[ib][jb]);
+          newV[k] = cj * S.V[i][j] + ej * S.V[i][jb];
+        }
       }
+      (void)cnt;
       __syncwarp();
-      cnt = 0;
-      for (int e = lane; e < N2 * N2; e += 32, ++cnt) {
-        const int i = e / N2, j = e % N2;
-        S.A[i][j] = (S.partner[i] == j && i != j) ? 0.0 : newA[cnt];
-        S.V[i][j] = newV[cnt];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int e = lane + 32 * k;
+        if (e < N2 * N2) {
+          const int i = e / N2, j = e % N2;
+          S.A[i][j] = (S.partner[i] == j && i != j) ? 0.0 : newA[k];
+          S.V[i][j] = newV[k];
+        }
       }
       __syncwarp();
     }
-    if (!rotated) break;
+    if (!__any_sync(FULL, rotated)) break;
   }
   // sort descending (ties by index); permute V columns accordingly
   double lam = (lane < n) ? S.A[lane][lane] : 0.0;
@@ -202,15 +253,14 @@ __device__ __noinline__ void warp_eig(SolverSmem& S, int n, int lane, double& la
     const double lk = lanev(lam, k);
     if (lane < n && (lk > lam || (lk == lam && k < lane))) ++rank;
   }
-  // stash V in A (A is no longer needed) then scatter columns
   for (int e = lane; e < n * n; e += 32) {
     const int i = e / n, j = e % n;
-    S.A[i][j] = S.V[i][j];
+    S.T[i][j] = S.V[i][j];
   }
   __syncwarp();
   for (int j = 0; j < n; ++j) {
     const int rj = __shfl_sync(FULL, rank, j);
-    if (lane < n) S.V[lane][rj] = S.A[lane][j];
+    if (lane < n) S.V[lane][rj] = S.T[lane][j];
   }
   __syncwarp();
   double sorted = 0.0;
@@ -226,7 +276,7 @@ __device__ __noinline__ void warp_eig(SolverSmem& S, int n, int lane, double& la
 // Inputs: lam (descending eigenvalues of B_hat, lane j), V (S.V), suf = V^T g_hat
 // (lane j), radius Delta, warm-start alpha, m (number of residuals, R6).
 // Output: p (lane j), alpha, number of Moré iterations (0 = Gauss-Newton).
-__device__ __noinline__ int warp_solve_tr(const SolverSmem& S, int n, int64_t m, double lam, double suf, double Delta,
+static __device__ __noinline__ int warp_solve_tr(const SolverSmem& S, int n, int64_t m, double lam, double suf, double Delta,
                              double& alpha, double& p_out, int lane, int* full_rank_out) {
   const bool act = lane < n;
   const double s = act ? sqrt(fmax(lam, 0.0)) : 0.0;
@@ -281,7 +331,7 @@ __device__ __noinline__ int warp_solve_tr(const SolverSmem& S, int n, int64_t m,
 
 // --------------------------------------------------- Coleman-Li helpers (R19)
 // Smallest t >= 0 with x + t s on a bound; hit pattern sign(s_j) where attained.
-__device__ __forceinline__ double w_step_to_bound(double x, double s, double lb, double ub, bool act, int& hit) {
+static __device__ __forceinline__ double w_step_to_bound(double x, double s, double lb, double ub, bool act, int& hit) {
   double st = INFINITY;
   if (act && s != 0.0) st = fmax((lb - x) / s, (ub - x) / s);
   const double t = wmin(st);
@@ -290,7 +340,7 @@ __device__ __forceinline__ double w_step_to_bound(double x, double s, double lb,
 }
 
 // 1-D quadratic minimiser on [lo, hi]: candidates lo, hi, vertex (R20)
-__device__ __forceinline__ void min_quad_1d(double a, double b, double lo, double hi, double c, double& t_out,
+static __device__ __forceinline__ void min_quad_1d(double a, double b, double lo, double hi, double c, double& t_out,
                                             double& y_out) {
   double ts[3] = {lo, hi, 0.0};
   int nt = 2;
@@ -314,13 +364,13 @@ __device__ __forceinline__ void min_quad_1d(double a, double b, double lo, doubl
 }
 
 // Q(s) = 1/2 s^T B s + g^T s  (B = B_hat incl. diag_h; R13)
-__device__ __forceinline__ double w_eval_quad(const SolverSmem& S, double gh, double s, int n, int lane) {
+static __device__ __forceinline__ double w_eval_quad(const SolverSmem& S, double gh, double s, int n, int lane) {
   return 0.5 * wquad(S.M, s, n, lane) + wdot(s, gh);
 }
 
 // Coleman-Li step selection (R19, R20).  In: p_h (lane), d, x, lb, ub, g_hat.
 // Out: step (original space), step_h (hat space), predicted reduction, branch.
-__device__ __noinline__ void w_select_step(const SolverSmem& S, int n, int lane, double x, double lb, double ub, double gh,
+static __device__ __noinline__ void w_select_step(const SolverSmem& S, int n, int lane, double x, double lb, double ub, double gh,
                               double d, double p_h, double Delta, double theta, double& step, double& step_h,
                               double& pred, int& branch) {
   const bool act = lane < n;
@@ -415,7 +465,7 @@ __device__ __noinline__ void w_select_step(const SolverSmem& S, int n, int lane,
 
 // rstep = 0 strict feasibility (R19): x <= lb -> nextafter(lb, ub), x >= ub ->
 // nextafter(ub, lb); still outside -> midpoint.
-__device__ __forceinline__ double strict_feasible0(double x, double lb, double ub) {
+static __device__ __forceinline__ double strict_feasible0(double x, double lb, double ub) {
   double xn = x;
   if (x <= lb) xn = nextafter(lb, ub);
   else if (x >= ub) xn = nextafter(ub, lb);
@@ -424,7 +474,7 @@ __device__ __forceinline__ double strict_feasible0(double x, double lb, double u
 }
 
 // ----------------------------------------------------------- control logic
-__device__ __forceinline__ void st_trace(FitState* st, int lane, double cost_new, double ratio) {
+static __device__ __forceinline__ void st_trace(FitState* st, int lane, double cost_new, double ratio) {
   if (st->trace_cap > 0 && st->trace_len < st->trace_cap) {
     if (lane == 0) {
       double* rec = st->trace + (int64_t)st->trace_len * TRACE_FIELDS;
@@ -448,7 +498,7 @@ __device__ __forceinline__ void st_trace(FitState* st, int lane, double cost_new
 }
 
 // Unpack the K-vector into (cost, g, G) at the current iterate.
-__device__ __forceinline__ void st_take_pass(FitState* st, const double* kv, int n, int lane) {
+static __device__ __forceinline__ void st_take_pass(FitState* st, const double* kv, int n, int lane) {
   if (lane < n) {
     st->g[lane] = kv[tri_slot(n, lane, n)];
     for (int k = 0; k < n; ++k) {
@@ -461,7 +511,7 @@ __device__ __forceinline__ void st_take_pass(FitState* st, const double* kv, int
 }
 
 // scale_inv from the Gram diagonal (reading R3: column norms of J = sqrt(G_jj))
-__device__ __forceinline__ void st_update_scale(FitState* st, int n, int lane, bool first) {
+static __device__ __forceinline__ void st_update_scale(FitState* st, int n, int lane, bool first) {
   if (lane < n) {
     double si = sqrt(st->G[lane * NMAX + lane]);
     if (first) {
@@ -475,7 +525,7 @@ __device__ __forceinline__ void st_update_scale(FitState* st, int n, int lane, b
 }
 
 // Coleman-Li vector v, dv (R19)
-__device__ __forceinline__ void cl_vector(double x, double g, double lb, double ub, double& v, double& dv) {
+static __device__ __forceinline__ void cl_vector(double x, double g, double lb, double ub, double& v, double& dv) {
   v = 1.0;
   dv = 0.0;
   if (g < 0.0 && isfinite(ub)) {
@@ -491,7 +541,7 @@ __device__ __forceinline__ void cl_vector(double x, double g, double lb, double 
 // Solve the subproblem for the current hat space and stage the trial point
 // in st->x_eval (Alg. 1 l.141-148 / Alg. 2 / select_step).  Then set the phase
 // of the next pass.
-__device__ void st_make_trial(FitState* st, SolverSmem& S, int n, int lane) {
+static __device__ void st_make_trial(FitState* st, SolverSmem& S, int n, int lane) {
   const bool act = lane < n;
   // restore the hat space (S.V, S.M) from global state
   for (int e = lane; e < n * n; e += 32) {
@@ -505,7 +555,9 @@ __device__ void st_make_trial(FitState* st, SolverSmem& S, int n, int lane) {
   const double Delta = st->Delta;
   double alpha = st->alpha;
   double p_h;
+  const long long c0 = clock64();
   warp_solve_tr(S, n, st->m_global, lam, suf, Delta, alpha, p_h, lane, nullptr);
+  if (lane == 0) st->prof[1] += clock64() - c0;
   const double x = act ? st->x[lane] : 0.0;
   const double d = act ? st->d[lane] : 0.0;
   const double gh = act ? st->gh[lane] : 0.0;
@@ -513,7 +565,9 @@ __device__ void st_make_trial(FitState* st, SolverSmem& S, int n, int lane) {
   int branch = -1;
   if (st->bounded) {
     const double lb = act ? st->lb[lane] : 0.0, ub = act ? st->ub[lane] : 0.0;
+    const long long c1 = clock64();
     w_select_step(S, n, lane, x, lb, ub, gh, d, p_h, Delta, st->theta, step, step_h, pred, branch);
+    if (lane == 0) st->prof[2] += clock64() - c1;
     x_new = act ? strict_feasible0(x + step, lb, ub) : 0.0;
   } else {
     step_h = p_h;
@@ -542,7 +596,7 @@ __device__ void st_make_trial(FitState* st, SolverSmem& S, int n, int lane) {
 
 // Alg. 1 loop top: termination by gtol / max_nfev, then the hat space of the
 // new iterate (Eq. 7-8, App. B) and the first trial.
-__device__ void st_outer_top(FitState* st, SolverSmem& S, int n, int lane) {
+static __device__ void st_outer_top(FitState* st, SolverSmem& S, int n, int lane) {
   const bool act = lane < n;
   const double x = act ? st->x[lane] : 0.0;
   const double g = act ? st->g[lane] : 0.0;
@@ -601,9 +655,18 @@ __device__ void st_outer_top(FitState* st, SolverSmem& S, int n, int lane) {
     S.M[i][j] = b;
     st->Gh[i * NMAX + j] = b;
   }
+  const int warm = st->have_V;
+  if (warm) {
+    for (int e = lane; e < NMAX * NMAX; e += 32) {
+      const int i = e / NMAX, j = e % NMAX;
+      S.V[i][j] = (i < n && j < n) ? st->V[i * NMAX + j] : 0.0;
+    }
+  }
   __syncwarp();
   double lam;
-  warp_eig(S, n, lane, lam);
+  const long long c0 = clock64();
+  warp_eig(S, n, lane, lam, warm);
+  if (lane == 0) st->prof[0] += clock64() - c0;
   const double suf = wVtx(S.V, gh, n, lane);  // S^T U^T r = V^T g_hat (c.1b)
   if (act) {
     st->lam[lane] = lam;
@@ -616,13 +679,14 @@ __device__ void st_outer_top(FitState* st, SolverSmem& S, int n, int lane) {
   if (lane == 0) {
     st->theta = fmax(0.995, 1.0 - gnorm);
     st->actual = -1.0;
+    st->have_V = 1;
   }
   __syncwarp();
   st_make_trial(st, S, n, lane);
 }
 
 // Initialisation after the J-pass at x0 (Alg. 1 l.137-138; R3, R4, R18).
-__device__ void st_init(FitState* st, SolverSmem& S, const double* kv, int n, int lane) {
+static __device__ void st_init(FitState* st, SolverSmem& S, const double* kv, int n, int lane) {
   const bool act = lane < n;
   if (kv[tri_count(n)] != 0.0) {  // R18: residuals at x0 must be finite
     if (lane == 0) {
@@ -667,7 +731,7 @@ __device__ void st_init(FitState* st, SolverSmem& S, const double* kv, int n, in
 
 // End of the inner (retry) loop: accept or keep x, count the iteration.
 // For the conservative policy an accepted step first needs the J-pass at x_new.
-__device__ void st_end_inner(FitState* st, SolverSmem& S, int n, int lane, bool have_jac) {
+static __device__ void st_end_inner(FitState* st, SolverSmem& S, int n, int lane, bool have_jac) {
   const bool act = lane < n;
   if (st->actual > 0.0) {
     if (!have_jac) {  // conservative: J at the new x (counts as njev there)
@@ -695,7 +759,7 @@ __device__ void st_end_inner(FitState* st, SolverSmem& S, int n, int lane, bool 
 }
 
 // After a trial pass at x_eval (speculative J-pass or conservative r-pass).
-__device__ void st_after_trial(FitState* st, SolverSmem& S, const double* kv, int n, int lane, bool jac) {
+static __device__ void st_after_trial(FitState* st, SolverSmem& S, const double* kv, int n, int lane, bool jac) {
   const double rr = jac ? kv[tri_slot(n, n, n)] : kv[0];
   const double bad = jac ? kv[tri_count(n)] : kv[1];
   if (lane == 0) st->nfev = st->nfev + 1;
@@ -756,8 +820,9 @@ __device__ void st_after_trial(FitState* st, SolverSmem& S, const double* kv, in
 
 // Entry point: called by warp 0 of the last block of every pass kernel in a
 // fit, with the combined K-vector of the pass that just finished.
-__device__ __noinline__ void fit_after_pass(FitState* st, SolverSmem& S, const double* kv, bool jac) {
+static __device__ __noinline__ void fit_after_pass(FitState* st, SolverSmem& S, const double* kv, bool jac) {
   const int lane = threadIdx.x & 31;
+  const long long cstart = clock64();
   const int n = st->n;
   const int KS = jac ? tri_count(n) + 1 : 2;
   for (int k = lane; k < KS; k += 32) st->kv[k] = kv[k];
@@ -782,6 +847,8 @@ __device__ __noinline__ void fit_after_pass(FitState* st, SolverSmem& S, const d
     __syncwarp();
     st_outer_top(st, S, n, lane);
   }
+  __syncwarp();
+  if (lane == 0) st->prof[3] += clock64() - cstart;
   __syncwarp();
 }
 

@@ -1,0 +1,90 @@
+"""The multi-GPU path on ONE GPU: R virtual ranks
+(jf_comm_create_local) run concurrently on separate streams; each pass kernel
+pushes its K-vector into every rank's mailbox and sums them in rank order, as
+on R GPUs over NVLink.  The sharded fit must match the single-rank fit of the
+whole image (per-pass 1e-10 normalised; fits: identical counts, x to 1e-6)
+and every rank must return the identical result."""
+import threading
+
+import numpy as np
+import pytest
+
+import datagen as dg
+from oracle import passes as orp
+
+jf = pytest.importorskip("paper_2208_12187_b200")
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+def _run_ranks(R, fn):
+    out = [None] * R
+    err = [None] * R
+
+    def work(r):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                out[r] = fn(r, s)
+        except Exception as e:  # pragma: no cover
+            err[r] = e
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(R)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    for e in err:
+        if e is not None:
+            raise e
+    return out
+
+
+@pytest.mark.parametrize("R", [2, 3, 4])
+def test_sharded_pass_equals_whole_image(R):
+    W, H = 512, 509
+    pr = dg.make_gauss2d(W, H=H, seed=12)
+    comms = jf.Comm.create_local(R, 0)
+    try:
+        def fn(r, s):
+            r0, r1 = dg.shard_rows(H, R, r)
+            z = torch.as_tensor(pr.z[r0 * W:r1 * W]).cuda()
+            return jf.jpass(pr.model, z, pr.p0, grid=(W, r1 - r0, r0), comm=comms[r], m_global=pr.m,
+                            stream=s.cuda_stream)
+        outs = _run_ranks(R, fn)
+    finally:
+        for c in comms:
+            c.destroy()
+    cr, gr, Gr, _ = orp.jpass(pr.model, pr.coords(), pr.z, pr.p0)
+    d = np.sqrt(np.diag(Gr))
+    for c, g, G, bad in outs:
+        assert bad == 0 and abs(c - cr) <= 1e-10 * cr
+        assert np.all(np.abs(g - gr) <= 1e-10 * d * np.sqrt(2 * cr))
+        assert np.all(np.abs(G - Gr) <= 1e-10 * np.outer(d, d))
+    for o in outs[1:]:
+        assert o[0] == outs[0][0] and np.array_equal(o[2], outs[0][2])
+
+
+@pytest.mark.parametrize("R", [2, 4])
+def test_sharded_fit_matches_single_rank(R):
+    W, H = 384, 384
+    pr = dg.make_gauss2d(W, H=H, seed=13)
+    ref = jf.curve_fit(pr.model, pr.z, p0=pr.p0, grid=pr.grid)
+    comms = jf.Comm.create_local(R, 0)
+    try:
+        def fn(r, s):
+            r0, r1 = dg.shard_rows(H, R, r)
+            z = torch.as_tensor(pr.z[r0 * W:r1 * W]).cuda()
+            return jf.curve_fit(pr.model, z, p0=pr.p0, grid=(W, r1 - r0, r0), comm=comms[r], m_global=pr.m,
+                                stream=s.cuda_stream)
+        outs = _run_ranks(R, fn)
+    finally:
+        for c in comms:
+            c.destroy()
+    for o in outs:
+        assert (o.status, o.nfev, o.njev, o.nit) == (ref.status, ref.nfev, ref.njev, ref.nit)
+        assert np.allclose(o.x, ref.x, rtol=1e-6)
+    for o in outs[1:]:
+        assert np.array_equal(o.x, outs[0].x) and o.cost == outs[0].cost

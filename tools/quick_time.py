@@ -11,7 +11,8 @@ pr = dg.make_gauss2d(W, seed=6)
 z = torch.as_tensor(pr.z).cuda()
 x = torch.as_tensor(pr.p0).cuda()
 kv = torch.zeros(64, dtype=torch.float64, device="cuda")
-s = torch.cuda.current_stream()
+s = torch.cuda.Stream()
+torch.cuda.set_stream(s)
 for ro in (False, True):
     for _ in range(3):
         jf.pass_device(pr.model, z, x, kv, grid=pr.grid, stream=s.cuda_stream, residual_only=ro)
@@ -23,10 +24,12 @@ for ro in (False, True):
         jf.pass_device(pr.model, z, x, kv, grid=pr.grid, stream=s.cuda_stream, residual_only=ro)
     e1.record(); torch.cuda.synchronize()
     t = e0.elapsed_time(e1) / N
-    print(f"{'r' if ro else 'J'}-pass W={W}: {t*1e3:.1f} us  {pr.m/t/1e3:.3e} pts/s")
+    print(f"{'r' if ro else 'J'}-pass W={W}: {t*1e3:.1f} us  {pr.m/t*1e3:.3e} pts/s")
+if len(sys.argv) > 2 and sys.argv[2] == "passonly":
+    sys.exit(0)
 for mode in ("graph", "hostloop"):
     for i in range(4):
         torch.cuda.synchronize(); t0 = time.perf_counter()
-        r = jf.curve_fit(pr.model, z, p0=pr.p0, grid=pr.grid, use_graph=(mode == "graph"))
+        r = jf.curve_fit(pr.model, z, p0=pr.p0, grid=pr.grid, use_graph=(mode == "graph"), stream=s.cuda_stream)
         torch.cuda.synchronize(); t1 = time.perf_counter()
-    print(mode, "fit", r.status, r.nfev, r.njev, r.cost, f"{(t1-t0)*1e3:.3f} ms", r.kernel_launches)
+    print(mode, "fit", r.status, r.nfev, r.njev, r.cost, f"{(t1-t0)*1e3:.3f} ms", r.kernel_launches, f"epi {r.t_epilogue_s*1e6:.1f} us", [int(c) for c in r.epilogue_cycles])
