@@ -196,7 +196,10 @@ def main():
     H_total = W_IMG * world
     pr_full = dg.make_gauss2d(W_IMG, seed=SEED, H=H_total) if world > 1 else dg.make_gauss2d(W_IMG, seed=SEED)
     r0, r1 = dg.shard_rows(H_total, world, rank)
-    z_host = np.ascontiguousarray(pr_full.z[r0 * W_IMG: r1 * W_IMG])
+    import torch as _t
+    z_pin = _t.empty(((r1 - r0) * W_IMG,), dtype=_t.float64, pin_memory=True)  # e2e: pinned host input
+    z_pin.numpy()[:] = pr_full.z[r0 * W_IMG: r1 * W_IMG]
+    z_host = z_pin.numpy()
     m_local = z_host.size
     m_total = pr_full.m
     grid = (W_IMG, r1 - r0, r0)

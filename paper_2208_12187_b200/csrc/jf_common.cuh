@@ -56,6 +56,7 @@ struct PassArgs {
   double* partials;     // [gridDim.x][KS] per-block partial K-vectors
   unsigned int* ticket; // last-block ticket (reset by the last block)
   double* out;          // combined K-vector (EPI_NONE)
+  int* err;             // EPI_NONE: set to JF_ECOMM (-5) if the cross-rank combine failed
   int32_t use_comm;     // 1: combine across ranks through the mailboxes
   int32_t pad_;
   CommDev comm;

@@ -104,13 +104,14 @@ struct Ctx {
   int trace_cap = 0;
   double* d_in = nullptr;  // staged host inputs
   size_t in_cap = 0;
-  std::map<const void*, int> occ;  // kernel -> resident blocks/SM
+  double* d_scratch = nullptr;  // small per-call scratch (status word, subproblem I/O)
   std::map<GraphKey, cudaGraphExec_t> graphs;
 };
 
 // Contexts: [0, 64) one per device; [64, 64 + 64*8) per (device, virtual rank)
 // of a jf_comm_create_local emulation, so emulated ranks run concurrently.
 Ctx g_ctx[64 + 64 * 8];
+constexpr int SCRATCH_DOUBLES = 1024;
 
 int ctx_init(Ctx& c, int dev) {
   if (c.ready) return 0;
@@ -124,10 +125,14 @@ int ctx_init(Ctx& c, int dev) {
   c.partial_blocks = c.nsm * 4;
   CK(cudaMalloc(&c.d_partials, sizeof(double) * (size_t)c.partial_blocks * KMAX));
   CK(cudaMalloc(&c.d_ticket, sizeof(unsigned int) * 4));
-  CK(cudaMemset(c.d_ticket, 0, sizeof(unsigned int) * 4));
   CK(cudaMalloc(&c.d_out, sizeof(double) * KMAX));
   CK(cudaMalloc(&c.d_x, sizeof(double) * NMAX));
-  CK(cudaDeviceSynchronize());
+  CK(cudaMalloc(&c.d_scratch, sizeof(double) * SCRATCH_DOUBLES));
+  // no device-wide synchronisation here: emulated ranks (jf_comm_create_local)
+  // may have pass kernels spinning on their mailboxes while a peer initialises
+  CK(cudaMemsetAsync(c.d_ticket, 0, sizeof(unsigned int) * 4, c.stream));
+  CK(cudaMemsetAsync(c.d_scratch, 0, sizeof(double) * SCRATCH_DOUBLES, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
   c.ready = true;
   return 0;
 }
@@ -135,16 +140,23 @@ int ctx_init(Ctx& c, int dev) {
 // The grid of a pass kernel: enough blocks to fill every SM at the kernel's
 // occupancy, fewer for small m.  A pure function of (kernel, m): fixed
 // reduction order, bitwise reproducible passes (H4).
+std::mutex g_occ_mu;
+std::map<std::pair<int, const void*>, int> g_occ;  // (device, kernel) -> resident blocks/SM
+
 int grid_for(Ctx& c, KernelFn f, int tpb, int64_t m) {
-  auto it = c.occ.find((const void*)f);
   int occ;
-  if (it == c.occ.end()) {
-    occ = 1;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, tpb, 0) != cudaSuccess || occ < 1) occ = 1;
-    if (occ > 4) occ = 4;
-    c.occ[(const void*)f] = occ;
-  } else {
-    occ = it->second;
+  {
+    std::lock_guard<std::mutex> g(g_occ_mu);
+    auto key = std::make_pair(c.dev, (const void*)f);
+    auto it = g_occ.find(key);
+    if (it == g_occ.end()) {
+      occ = 1;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, tpb, 0) != cudaSuccess || occ < 1) occ = 1;
+      if (occ > 4) occ = 4;
+      g_occ[key] = occ;
+    } else {
+      occ = it->second;
+    }
   }
   const int64_t need = (m + tpb - 1) / tpb;
   int64_t g = (int64_t)c.nsm * occ;
@@ -198,6 +210,18 @@ struct Staged {
   double upload_s = 0.0;
 };
 
+// Grow a device buffer with the stream-ordered allocator (no device-wide
+// synchronisation, which could stall against emulated ranks' kernels).
+int ensure(double*& p, size_t& cap, size_t need, cudaStream_t s) {
+  if (cap >= need) return 0;
+  if (p) CK(cudaFreeAsync(p, s));
+  p = nullptr;
+  cap = 0;
+  CK(cudaMallocAsync((void**)&p, sizeof(double) * need, s));
+  cap = need;
+  return 0;
+}
+
 __global__ void inv_kernel(double* p, int64_t m) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = 1.0 / p[i];
@@ -229,13 +253,7 @@ int stage_inputs(Ctx& c, cudaStream_t s, int model, const double* y, const doubl
       st.y1 = (d == 2) ? y + m : nullptr;
     }
     if (o.sigma) {  // 1/sigma needs a scratch copy
-      if (c.in_cap < nw) {
-        if (c.d_in) cudaFree(c.d_in);
-        c.d_in = nullptr;
-        c.in_cap = 0;
-        CK(cudaMalloc(&c.d_in, sizeof(double) * nw));
-        c.in_cap = nw;
-      }
+      if (int e = ensure(c.d_in, c.in_cap, nw, s)) return e;
       CK(cudaMemcpyAsync(c.d_in, o.sigma, sizeof(double) * nw, cudaMemcpyDeviceToDevice, s));
       inv_kernel<<<c.nsm * 4, 256, 0, s>>>(c.d_in, m);
       CK(cudaGetLastError());
@@ -243,13 +261,7 @@ int stage_inputs(Ctx& c, cudaStream_t s, int model, const double* y, const doubl
     }
   } else {
     const size_t need = (size_t)m + ny + nw;
-    if (c.in_cap < need) {
-      if (c.d_in) cudaFree(c.d_in);
-      c.d_in = nullptr;
-      c.in_cap = 0;
-      CK(cudaMalloc(&c.d_in, sizeof(double) * need));
-      c.in_cap = need;
-    }
+    if (int e = ensure(c.d_in, c.in_cap, need, s)) return e;
     double* p = c.d_in;
     CK(cudaMemcpyAsync(p, z, sizeof(double) * m, cudaMemcpyHostToDevice, s));
     st.z = p;
@@ -452,6 +464,7 @@ static int pass_common(int32_t model, const double* y, const double* z, int64_t 
   a.partials = c->d_partials;
   a.ticket = c->d_ticket;
   a.out = out_dev_or_null ? out_dev_or_null : c->d_out;
+  a.err = (int*)c->d_scratch;
   if (o.comm) {
     a.use_comm = 1;
     fill_comm(a.comm, o.comm);
@@ -464,7 +477,16 @@ static int pass_common(int32_t model, const double* y, const double* z, int64_t 
     const int KS = residual_only ? 2 : tri_count(n) + 1;
     CK(cudaMemcpyAsync(host_out, a.out, sizeof(double) * KS, cudaMemcpyDeviceToHost, s));
   }
-  if (sync) CK(cudaStreamSynchronize(s));
+  if (sync) {
+    int err = 0;
+    CK(cudaMemcpyAsync(&err, a.err, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (err) {
+      CK(cudaMemsetAsync(a.err, 0, sizeof(int), s));
+      CK(cudaStreamSynchronize(s));
+      return err;
+    }
+  }
   return 0;
 }
 
@@ -561,14 +583,9 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
   // trace buffer
   if (o.trace_cap > 0) {
     if (!o.trace) return fail(JF_EINVAL);
-    if (c->trace_cap < o.trace_cap) {
-      if (c->d_trace) cudaFree(c->d_trace);
-      c->d_trace = nullptr;
-      c->trace_cap = 0;
-      if (cudaMalloc(&c->d_trace, sizeof(double) * TRACE_FIELDS * (size_t)o.trace_cap) != cudaSuccess)
-        return fail(JF_ENOMEM);
-      c->trace_cap = o.trace_cap;
-    }
+    size_t cap = (size_t)c->trace_cap * TRACE_FIELDS;
+    if (int e = ensure(c->d_trace, cap, (size_t)o.trace_cap * TRACE_FIELDS, s)) return fail(e);
+    c->trace_cap = (int)(cap / TRACE_FIELDS);
   }
 
   // ---- device state
@@ -713,8 +730,7 @@ extern "C" int32_t jf_trust_region_step(const double* hatG, const double* hatg, 
   cudaStream_t s;
   int r = acquire(o, c, lk, s);
   if (r) return r;
-  double* d;
-  CK(cudaMalloc(&d, sizeof(double) * (n * n + n + 2 * NMAX + 2)));
+  double* d = c->d_scratch + 8;
   double* dG = d;
   double* dg = d + n * n;
   double* dout = dg + n;
@@ -725,7 +741,6 @@ extern "C" int32_t jf_trust_region_step(const double* hatG, const double* hatg, 
   double hout[2 * NMAX + 2];
   CK(cudaMemcpyAsync(hout, dout, sizeof(hout), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  cudaFree(d);
   for (int j = 0; j < n; ++j) p[j] = hout[j];
   if (alpha_out) *alpha_out = hout[2 * NMAX];
   if (n_iter) *n_iter = (int32_t)hout[2 * NMAX + 1];
@@ -759,7 +774,7 @@ int32_t jf_comm_create(int32_t rank, int32_t nranks, int32_t device, jf_comm** c
     delete c;
     return JF_ENOMEM;
   }
-  if (cudaMemset(c->mbox, 0, mbox_bytes(nranks)) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+  if (cudaMemset(c->mbox, 0, mbox_bytes(nranks)) != cudaSuccess || cudaStreamSynchronize(0) != cudaSuccess) {
     cudaFree(c->mbox);
     delete c;
     return JF_ECUDA;
@@ -822,6 +837,16 @@ int32_t jf_comm_create_local(int32_t nranks, int32_t device, jf_comm** comms) {
   }
   for (int r = 0; r < nranks; ++r)
     for (int p = 0; p < nranks; ++p) cs[r]->peer[p] = cs[p]->mbox;
+  // initialise the emulated ranks' contexts now: a context created while a
+  // peer's pass kernel spins on its mailbox could otherwise wait on it
+  for (int r = 0; r < nranks; ++r) {
+    Ctx& c = g_ctx[64 + device * 8 + r];
+    std::lock_guard<std::mutex> g(c.mu);
+    if (int e = ctx_init(c, device)) {
+      for (auto* q : cs) jf_comm_destroy(q);
+      return e;
+    }
+  }
   for (int r = 0; r < nranks; ++r) comms[r] = cs[r];
   return 0;
 }

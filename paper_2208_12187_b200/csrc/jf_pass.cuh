@@ -157,9 +157,11 @@ __device__ __forceinline__ bool comm_combine(const CommDev& cm, unsigned long lo
   __syncthreads();
   if (threadIdx.x < R) {
     volatile unsigned long long* f = cm.mbox_flag[me] + threadIdx.x;
-    long long spins = 0;
+    unsigned long long t0, t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     while (*f < epoch) {
-      if (++spins > (1ll << 31)) {
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      if (t1 - t0 > 20000000000ull) {  // 20 s: a peer is gone
         timed_out = 1;
         break;
       }
@@ -334,6 +336,7 @@ __global__ void __launch_bounds__((PassCfg<Model, JAC>::TPB), (PassCfg<Model, JA
     const bool ok = comm_combine<KS, TPB>(a.comm, epoch, vec);
     if (threadIdx.x == 0 && a.epilogue == EPI_FIT) st->comm_epoch = epoch;
     if (!ok) {
+      if (threadIdx.x == 0 && a.epilogue != EPI_FIT && a.err) *a.err = -5;
       if (threadIdx.x == 0 && a.epilogue == EPI_FIT) {
         st->error = -5;
         st->status = -5;
