@@ -224,6 +224,18 @@ __device__ __forceinline__ Dual<N, A> dcos(const Dual<N, A>& a) {
   return r;
 }
 
+// exp(a) when the value e = exp(a.v) is already known (the grid-stride
+// recurrence of jf_pass.cuh supplies it): only the chain-rule partials remain.
+__device__ __forceinline__ double dexp_given(double /*a*/, double e) { return e; }
+template <int N, unsigned A>
+__device__ __forceinline__ Dual<N, A> dexp_given(const Dual<N, A>& a, double e) {
+  Dual<N, A> r;
+  r.v = e;
+#pragma unroll
+  for (int k = 0; k < Dual<N, A>::nnz; ++k) r.d[k] = e * a.d[k];
+  return r;
+}
+
 // value / partial accessors that also work on plain doubles
 __device__ __forceinline__ double value(double a) { return a; }
 template <int N, unsigned A>

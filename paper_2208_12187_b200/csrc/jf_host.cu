@@ -11,6 +11,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -694,7 +695,7 @@ int32_t jf_curve_fit(int32_t model, const double* y, const double* z, int64_t m,
 
 namespace {
 __global__ void tr_step_kernel(const double* hatG, const double* hatg, int n, int64_t m, double Delta,
-                               double alpha_in, double* out) {
+                               double alpha_in, double* out, int getenv_dbg) {
   __shared__ SolverSmem S;
   const int lane = threadIdx.x;
   for (int e = lane; e < n * n; e += 32) {
@@ -704,11 +705,15 @@ __global__ void tr_step_kernel(const double* hatG, const double* hatg, int n, in
   }
   __syncwarp();
   double lam;
-  warp_eig(S, n, lane, lam, 0);
+  const long long c0 = clock64();
+  const int sw = warp_eig(S, n, lane, lam, 0);
+  const long long c1 = clock64();
   const double g = lane < n ? hatg[lane] : 0.0;
   const double suf = wVtx(S.V, g, n, lane);
   double alpha = alpha_in, p;
   const int it = warp_solve_tr(S, n, m, lam, suf, Delta, alpha, p, lane, nullptr);
+  const long long c2 = clock64();
+  if (lane == 0 && getenv_dbg) printf("tr_step n=%d sweeps=%d eig_cycles=%lld solve_cycles=%lld iters=%d\n", n, sw, c1 - c0, c2 - c1, it);
   if (lane < n) out[lane] = p;
   if (lane < n) out[NMAX + lane] = lam;
   if (lane == 0) {
@@ -736,7 +741,7 @@ extern "C" int32_t jf_trust_region_step(const double* hatG, const double* hatg, 
   double* dout = dg + n;
   CK(cudaMemcpyAsync(dG, hatG, sizeof(double) * n * n, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(dg, hatg, sizeof(double) * n, cudaMemcpyHostToDevice, s));
-  tr_step_kernel<<<1, 32, 0, s>>>(dG, dg, n, m, Delta, alpha_in, dout);
+  tr_step_kernel<<<1, 32, 0, s>>>(dG, dg, n, m, Delta, alpha_in, dout, getenv("JF_DEBUG") != nullptr);
   CK(cudaGetLastError());
   double hout[2 * NMAX + 2];
   CK(cudaMemcpyAsync(hout, dout, sizeof(hout), cudaMemcpyDeviceToHost, s));

@@ -1,4 +1,6 @@
 // jf_k_gauss2d.cu — pass-kernel instances for ModelGauss2DRot (see jf_pass.cuh).
+#include <cstdlib>
+
 #include "jf_kernels.h"
 #include "jf_pass.cuh"
 
@@ -14,5 +16,17 @@ static Kernels make() {
   k.rtpb = PassCfg<ModelGauss2DRot, false>::TPB;
   return k;
 }
-Kernels kernels_gauss2d(int coord) { return coord == COORD_EXPLICIT ? make<COORD_EXPLICIT>() : make<COORD_GRID>(); }
+Kernels kernels_gauss2d(int coord) {
+  Kernels k = coord == COORD_EXPLICIT ? make<COORD_EXPLICIT>() : make<COORD_GRID>();
+  // development aid: alternative launch shapes of the grid J-pass (JF_JVARIANT=1..3)
+  if (coord == COORD_GRID) {
+    if (const char* v = getenv("JF_JVARIANT")) {
+      const int var = atoi(v);
+      if (var == 1) { k.jk = pass_kernel<ModelGauss2DRot, true, COORD_GRID, false, 4, 256, 1>; k.jtpb = 256; }
+      if (var == 2) { k.jk = pass_kernel<ModelGauss2DRot, true, COORD_GRID, false, 3, 256, 1>; k.jtpb = 256; }
+      if (var == 3) { k.jk = pass_kernel<ModelGauss2DRot, true, COORD_GRID, false, 1, 256, 2>; k.jtpb = 256; }
+    }
+  }
+  return k;
+}
 }  // namespace jf

@@ -30,6 +30,7 @@ __device__ __forceinline__ auto param(double v) {
 // ---------------------------------------------------------------- LINEAR (n=2)
 struct ModelLinear {
   static constexpr int N = 2, D = 1, CONST_COL = 1;
+  static constexpr int NEXP = 0;
   struct Pre {
     double x0, x1;
   };
@@ -44,6 +45,7 @@ struct ModelLinear {
 // ------------------------------------------------------------ EXP_DECAY (n=3)
 struct ModelExpDecay {
   static constexpr int N = 3, D = 1, CONST_COL = 2;
+  static constexpr int NEXP = 0;
   struct Pre {
     double a, b, c;
   };
@@ -67,6 +69,7 @@ struct PreGauss1D {
 };
 struct ModelGauss1D {
   static constexpr int N = 4, D = 1, CONST_COL = 3;
+  static constexpr int NEXP = 0;
   template <bool JAC>
   __device__ __forceinline__ static auto prologue(const double* x) {
     const auto s = param<JAC, N, 2>(x[2]);
@@ -122,10 +125,33 @@ struct Gauss2DComponent {
     const auto q = dx * (p.a * dx + p.b2 * dy) + p.c * (dy * dy);
     return param<JAC, N, B + 0>(p.A) * dexp(-q);
   }
+  // The same with E = exp(-q(X, Y)) supplied by the caller (row recurrence).
+  template <bool JAC, class P>
+  __device__ __forceinline__ static auto point_e(const P& p, double X, double Y, double E) {
+    const auto dx = X - param<JAC, N, B + 1>(p.x0);
+    const auto dy = Y - param<JAC, N, B + 2>(p.y0);
+    const auto q = dx * (p.a * dx + p.b2 * dy) + p.c * (dy * dy);
+    return param<JAC, N, B + 0>(p.A) * dexp_given(-q, E);
+  }
+  // Plain-double quantities of the row recurrence: q(X, Y) and the
+  // coefficients a, 2b and the centre.
+  template <class P>
+  __device__ __forceinline__ static double qval(const P& p, double X, double Y) {
+    const double dx = X - p.x0, dy = Y - p.y0;
+    return dx * (value(p.a) * dx + value(p.b2) * dy) + value(p.c) * (dy * dy);
+  }
+  template <class P>
+  __device__ __forceinline__ static void rec_coeffs(const P& p, double& a, double& b2, double& x0, double& y0) {
+    a = value(p.a);
+    b2 = value(p.b2);
+    x0 = p.x0;
+    y0 = p.y0;
+  }
 };
 
 struct ModelGauss2DRot {
   static constexpr int N = 7, D = 2, CONST_COL = 6;
+  static constexpr int NEXP = 1;  // exp factors with a quadratic argument (row recurrence)
   using G = Gauss2DComponent<N, 0>;
   template <class P>
   struct Pre {
@@ -141,11 +167,24 @@ struct ModelGauss2DRot {
   __device__ __forceinline__ static auto point(const P& p, double X, double Y) {
     return G::template point<JAC>(p.g, X, Y) + param<JAC, N, 6>(p.off);
   }
+  template <bool JAC, class P>
+  __device__ __forceinline__ static auto point_e(const P& p, double X, double Y, const double (&E)[NEXP]) {
+    return G::template point_e<JAC>(p.g, X, Y, E[0]) + param<JAC, N, 6>(p.off);
+  }
+  template <int g, class P>
+  __device__ __forceinline__ static double qval(const P& p, double X, double Y) {
+    return G::qval(p.g, X, Y);
+  }
+  template <int g, class P>
+  __device__ __forceinline__ static void rec_coeffs(const P& p, double& a, double& b2, double& x0, double& y0) {
+    G::rec_coeffs(p.g, a, b2, x0, y0);
+  }
 };
 
 // ---------------------------------------------------- GAUSS2D_ROT_X2 (n=13)
 struct ModelGauss2DRotX2 {
   static constexpr int N = 13, D = 2, CONST_COL = 12;
+  static constexpr int NEXP = 2;
   using G1 = Gauss2DComponent<N, 0>;
   using G2 = Gauss2DComponent<N, 6>;
   template <class P1, class P2>
@@ -164,6 +203,21 @@ struct ModelGauss2DRotX2 {
   __device__ __forceinline__ static auto point(const P& p, double X, double Y) {
     return (G1::template point<JAC>(p.g1, X, Y) + G2::template point<JAC>(p.g2, X, Y)) +
            param<JAC, N, 12>(p.off);
+  }
+  template <bool JAC, class P>
+  __device__ __forceinline__ static auto point_e(const P& p, double X, double Y, const double (&E)[NEXP]) {
+    return (G1::template point_e<JAC>(p.g1, X, Y, E[0]) + G2::template point_e<JAC>(p.g2, X, Y, E[1])) +
+           param<JAC, N, 12>(p.off);
+  }
+  template <int g, class P>
+  __device__ __forceinline__ static double qval(const P& p, double X, double Y) {
+    if constexpr (g == 0) return G1::qval(p.g1, X, Y);
+    else return G2::qval(p.g2, X, Y);
+  }
+  template <int g, class P>
+  __device__ __forceinline__ static void rec_coeffs(const P& p, double& a, double& b2, double& x0, double& y0) {
+    if constexpr (g == 0) G1::rec_coeffs(p.g1, a, b2, x0, y0);
+    else G2::rec_coeffs(p.g2, a, b2, x0, y0);
   }
 };
 

@@ -211,25 +211,128 @@ struct PointIter {
   }
 };
 
+// Implicit-grid pass with the row recurrence for exp (models with NEXP > 0).
+//
+// Work unit: a warp-chunk of 32 L consecutive pixels of one image row; lane l
+// owns pixels col0 + l + 32 k, k < L, so every load instruction of the warp
+// reads 32 consecutive doubles.  Along such a run the exponent of each
+// Gaussian factor is quadratic in k:  q(k+1) - q(k) = D (2a dx_k + 2b dy) + a D^2
+// with D = 32, so  E_{k+1} = E_k R_k,  R_{k+1} = R_k rho,  rho = exp(-2 a D^2):
+// two multiplications per point instead of an fp64 exp (two exps per chunk
+// start).  Relative error grows by a few ulp per step (<= ~4e-15 at L = 8).
+// A lane whose chunk start is outside a safe exponent range (|q| > 600 or a
+// step factor beyond e^300) evaluates exp directly for that chunk.
+template <class Model, bool JAC, bool WGT, int L, int TPB>
+__device__ __forceinline__ void grid_recur_loop(const PassArgs& a, const auto& pre,
+                                                double (&acc)[PassShape<Model, JAC>::KT], int& bad, int& cnt) {
+  constexpr int NE = Model::NEXP;
+  constexpr int CW = 32 * L;
+  constexpr double D = 32.0;
+  const int lane = threadIdx.x & 31;
+  const int W = (int)a.W;
+  const int64_t H = a.m / a.W;
+  const int cpr = (W + CW - 1) / CW;
+  const int64_t nch = H * (int64_t)cpr;
+  const int64_t nw = (int64_t)gridDim.x * (TPB / 32);
+  int64_t ch = (int64_t)blockIdx.x * (TPB / 32) + (threadIdx.x >> 5);
+  const double* __restrict__ z = a.z;
+  const double* __restrict__ ws = a.wsig;
+  double ra[NE], rb2[NE], rx0[NE], ry0[NE], rho[NE];
+#pragma unroll
+  for (int g = 0; g < NE; ++g) {
+    if (g == 0) Model::template rec_coeffs<0>(pre, ra[g], rb2[g], rx0[g], ry0[g]);
+    if constexpr (NE > 1) {
+      if (g == 1) Model::template rec_coeffs<1>(pre, ra[g], rb2[g], rx0[g], ry0[g]);
+    }
+    rho[g] = exp(-2.0 * ra[g] * D * D);
+  }
+  double zn[L], wn[L];
+  auto load = [&](int64_t c) {
+    if (c < nch) {
+      const int64_t row = c / cpr;
+      const int col = (int)(c - row * cpr) * CW + lane;
+      const double* zp = z + row * a.W + col;
+#pragma unroll
+      for (int k = 0; k < L; ++k) {
+        const bool v = col + 32 * k < W;
+        zn[k] = v ? __ldg(zp + 32 * k) : 0.0;
+        if constexpr (WGT) wn[k] = v ? __ldg(ws + row * a.W + col + 32 * k) : 0.0;
+      }
+    }
+  };
+  load(ch);
+  for (; ch < nch; ch += nw) {
+    double zc[L], wc[L];
+#pragma unroll
+    for (int k = 0; k < L; ++k) {
+      zc[k] = zn[k];
+      if constexpr (WGT) wc[k] = wn[k];
+    }
+    load(ch + nw);  // prefetch the next chunk
+    const int64_t row = ch / cpr;
+    const int col0 = (int)(ch - row * cpr) * CW + lane;
+    const double Y = (double)(row + a.row0);
+    const double X0 = (double)col0;
+    double E[NE], R[NE];
+    bool ok = true;
+#pragma unroll
+    for (int g = 0; g < NE; ++g) {
+      double q0;
+      if (g == 0) q0 = Model::template qval<0>(pre, X0, Y);
+      if constexpr (NE > 1) {
+        if (g == 1) q0 = Model::template qval<1>(pre, X0, Y);
+      }
+      const double argR = D * (2.0 * ra[g] * (X0 - rx0[g]) + rb2[g] * (Y - ry0[g])) + ra[g] * D * D;
+      ok = ok && fabs(q0) < 600.0 && fabs(argR) < 300.0 && 2.0 * ra[g] * D * D * L < 300.0;
+      E[g] = exp(-q0);
+      R[g] = exp(-argR);
+    }
+    const bool full = (int)(ch - row * cpr) * CW + CW <= W;  // warp-uniform
+    if (full && __all_sync(FULL, ok)) {
+#pragma unroll
+      for (int k = 0; k < L; ++k) {
+        const double X = X0 + 32.0 * k;
+        const auto h = Model::template point_e<JAC>(pre, X, Y, E);
+        accumulate<Model, JAC>(acc, bad, cnt, h, zc[k], WGT ? wc[k] : 1.0, WGT);
+#pragma unroll
+        for (int g = 0; g < NE; ++g) {
+          E[g] *= R[g];
+          R[g] *= rho[g];
+        }
+      }
+    } else {
+      // ragged row end or unsafe exponent range: direct evaluation
+#pragma unroll 1
+      for (int k = 0; k < L; ++k) {
+        if (col0 + 32 * k < W) {
+          const double X = X0 + 32.0 * k;
+          const auto h = Model::template point<JAC>(pre, X, Y);
+          accumulate<Model, JAC>(acc, bad, cnt, h, zc[k], WGT ? wc[k] : 1.0, WGT);
+        }
+      }
+    }
+  }
+}
+
 // Launch shape per (model, pass): points per thread per iteration (ILP) and
 // minimum resident blocks per SM (register budget).
 template <class Model, bool JAC>
 struct PassCfg {
   static constexpr bool BIG = JAC && Model::N >= 7;
-  static constexpr int P = JAC ? (Model::N == 7 ? 2 : 1) : 4;
-  static constexpr int TPB = (JAC && Model::N == 7) ? 384 : 256;
+  static constexpr int P = JAC ? (Model::N == 7 ? 4 : 1) : 4;
+  static constexpr int TPB = 256;
   static constexpr int MINB = BIG ? 1 : 2;
+  static constexpr int L = (JAC && Model::N > 7) ? 2 : 8;  // points per lane per warp-chunk (grid recurrence)
 };
 
 // The pass kernel.  epilogue == EPI_FIT: one pass of a fit (st is the state).
-template <class Model, bool JAC, int COORD, bool WGT>
-__global__ void __launch_bounds__((PassCfg<Model, JAC>::TPB), (PassCfg<Model, JAC>::MINB))
+template <class Model, bool JAC, int COORD, bool WGT, int P = PassCfg<Model, JAC>::P,
+          int TPB = PassCfg<Model, JAC>::TPB, int MINB = PassCfg<Model, JAC>::MINB>
+__global__ void __launch_bounds__(TPB, MINB)
     pass_kernel(const PassArgs* __restrict__ pa, FitState* __restrict__ st, cudaGraphConditionalHandle cond,
                 int use_cond) {
   using Sh = PassShape<Model, JAC>;
   constexpr int KT = Sh::KT, KS = Sh::KS;
-  constexpr int P = PassCfg<Model, JAC>::P;
-  constexpr int TPB = PassCfg<Model, JAC>::TPB;
   const PassArgs& a = *pa;
 
   // Phase predication inside a fit: run only when this pass type is wanted.
@@ -278,39 +381,62 @@ __global__ void __launch_bounds__((PassCfg<Model, JAC>::TPB), (PassCfg<Model, JA
       }
     }
   };
+  if constexpr (COORD == COORD_GRID && Model::NEXP > 0) {
+    grid_recur_loop<Model, JAC, WGT, PassCfg<Model, JAC>::L, TPB>(a, pre, acc, bad, cnt);
+  } else {
+  auto coords = [&](double& X, double& Y) {
+    if constexpr (COORD == COORD_GRID) {
+      X = (double)it.col;
+      Y = (double)(it.row + (int32_t)a.row0);
+    } else if constexpr (COORD == COORD_IMPLICIT_T) {
+      X = fma((double)(a.index0 + it.i), a.dt, a.t0);
+    }
+  };
+  auto eval = [&](double X, double Y, double zz, double ww) {
+    if constexpr (TWO) {
+      const auto h = Model::template point<JAC>(pre, X, Y);
+      accumulate<Model, JAC>(acc, bad, cnt, h, zz, ww, weighted);
+    } else {
+      const auto h = Model::template point<JAC>(pre, X);
+      accumulate<Model, JAC>(acc, bad, cnt, h, zz, ww, weighted);
+    }
+  };
+  // main loop: full groups of P points, straight-line (no per-point predicate)
+  const int64_t full_end = m - (int64_t)(P - 1) * S;
   issue(it.i);
-  while (it.i < m) {
+  while (it.i < full_end) {
     double cz[P], cw[P], cx[P], cy[P];
-    bool cv[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) {
-      cv[p] = it.i < m;
       cz[p] = qz[p];
       cw[p] = qw[p];
       if constexpr (EXPL) {
         cx[p] = qa[p];
         if constexpr (TWO) cy[p] = qb[p];
-      } else if constexpr (COORD == COORD_GRID) {
-        cx[p] = (double)it.col;
-        cy[p] = (double)(it.row + (int32_t)a.row0);
       } else {
-        cx[p] = fma((double)(a.index0 + it.i), a.dt, a.t0);
+        coords(cx[p], cy[p]);
       }
       it.advance();
     }
     issue(it.i);
 #pragma unroll
-    for (int p = 0; p < P; ++p) {
-      if (P == 1 || cv[p]) {
-        if constexpr (TWO) {
-          const auto h = Model::template point<JAC>(pre, cx[p], cy[p]);
-          accumulate<Model, JAC>(acc, bad, cnt, h, cz[p], cw[p], weighted);
-        } else {
-          const auto h = Model::template point<JAC>(pre, cx[p]);
-          accumulate<Model, JAC>(acc, bad, cnt, h, cz[p], cw[p], weighted);
-        }
+    for (int p = 0; p < P; ++p) eval(cx[p], cy[p], cz[p], cw[p]);
+  }
+  // tail: fewer than P points left for this thread
+  if constexpr (P > 1) {
+#pragma unroll 1
+    for (int p = 0; p < P - 1 && it.i < m; ++p) {
+      double X = 0.0, Y = 0.0;
+      if constexpr (EXPL) {
+        X = qa[p];
+        if constexpr (TWO) Y = qb[p];
+      } else {
+        coords(X, Y);
       }
+      eval(X, Y, qz[p], qw[p]);
+      it.advance();
     }
+  }
   }
   if constexpr (JAC) {
     constexpr int CC = Model::CONST_COL;

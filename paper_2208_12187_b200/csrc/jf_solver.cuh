@@ -138,7 +138,7 @@ static __device__ __forceinline__ double wbilin(const double (*M)[NMAX + 1], dou
 // two sweeps instead of six.  Rotations are skipped when
 // |a_pq| <= eps sqrt(|a_pp a_qq|) or |a_pq| <= 2^-60 max_i |a_ii|; the
 // sweep loop ends when a sweep applies none.
-static __device__ __noinline__ void warp_eig(SolverSmem& S, int n, int lane, double& lam_out, int warm) {
+static __device__ __noinline__ int warp_eig(SolverSmem& S, int n, int lane, double& lam_out, int warm) {
   const int N2 = (n + 1) & ~1;  // pad to even with a zero row / column
   if (!warm) {
     for (int e = lane; e < NMAX * NMAX; e += 32) {
@@ -176,8 +176,10 @@ static __device__ __noinline__ void warp_eig(SolverSmem& S, int n, int lane, dou
   double amax = (lane < n) ? fabs(S.A[lane][lane]) : 0.0;
   amax = wmax(amax);
   const double abs_tol = amax * 8.673617379884035e-19;  // 2^-60
+  int sweeps = 0;
   for (int sweep = 0; sweep < 40; ++sweep) {
     bool rotated = false;
+    ++sweeps;
     for (int r = 0; r < N2 - 1; ++r) {
       // pair k: (p, q) from the circle method
       if (lane < N2 / 2) {
@@ -270,6 +272,7 @@ static __device__ __noinline__ void warp_eig(SolverSmem& S, int n, int lane, dou
     if (lane == rj) sorted = lj;
   }
   lam_out = (lane < n) ? sorted : 0.0;
+  return sweeps;
 }
 
 // --------------------------------------------------- Alg. 2 + App. B on device

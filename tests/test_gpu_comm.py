@@ -22,10 +22,12 @@ def _run_ranks(R, fn):
     out = [None] * R
     err = [None] * R
 
+    streams = [torch.cuda.Stream() for _ in range(R)]
+
     def work(r):
         try:
             torch.cuda.set_device(0)
-            s = torch.cuda.Stream()
+            s = streams[r]
             with torch.cuda.stream(s):
                 out[r] = fn(r, s)
         except Exception as e:  # pragma: no cover
@@ -47,11 +49,15 @@ def test_sharded_pass_equals_whole_image(R):
     W, H = 512, 509
     pr = dg.make_gauss2d(W, H=H, seed=12)
     comms = jf.Comm.create_local(R, 0)
+    # every device allocation happens before any rank's kernel can spin on its
+    # mailbox (an allocation that synchronises would wait on the spinners)
+    zs = [torch.as_tensor(pr.z[dg.shard_rows(H, R, r)[0] * W:dg.shard_rows(H, R, r)[1] * W]).cuda()
+          for r in range(R)]
+    torch.cuda.synchronize()
     try:
         def fn(r, s):
             r0, r1 = dg.shard_rows(H, R, r)
-            z = torch.as_tensor(pr.z[r0 * W:r1 * W]).cuda()
-            return jf.jpass(pr.model, z, pr.p0, grid=(W, r1 - r0, r0), comm=comms[r], m_global=pr.m,
+            return jf.jpass(pr.model, zs[r], pr.p0, grid=(W, r1 - r0, r0), comm=comms[r], m_global=pr.m,
                             stream=s.cuda_stream)
         outs = _run_ranks(R, fn)
     finally:
@@ -73,11 +79,13 @@ def test_sharded_fit_matches_single_rank(R):
     pr = dg.make_gauss2d(W, H=H, seed=13)
     ref = jf.curve_fit(pr.model, pr.z, p0=pr.p0, grid=pr.grid)
     comms = jf.Comm.create_local(R, 0)
+    zs = [torch.as_tensor(pr.z[dg.shard_rows(H, R, r)[0] * W:dg.shard_rows(H, R, r)[1] * W]).cuda()
+          for r in range(R)]
+    torch.cuda.synchronize()
     try:
         def fn(r, s):
             r0, r1 = dg.shard_rows(H, R, r)
-            z = torch.as_tensor(pr.z[r0 * W:r1 * W]).cuda()
-            return jf.curve_fit(pr.model, z, p0=pr.p0, grid=(W, r1 - r0, r0), comm=comms[r], m_global=pr.m,
+            return jf.curve_fit(pr.model, zs[r], p0=pr.p0, grid=(W, r1 - r0, r0), comm=comms[r], m_global=pr.m,
                                 stream=s.cuda_stream)
         outs = _run_ranks(R, fn)
     finally:
