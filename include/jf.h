@@ -150,7 +150,7 @@ typedef struct jf_result {
   int32_t pad_;
   double t_upload_s, t_solve_s; /* host wall time of the H2D copies and of the solve           */
   double t_epilogue_s;          /* device time in the single-warp solver epilogues (globaltimer) */
-  double epilogue_cycles[4];    /* SM cycles in: eigensolver, LM-parameter solve, Coleman-Li step
+  double epilogue_cycles[8];    /* SM cycles in: eigensolver, trial solve, Coleman-Li step
                                    selection, whole solver step (diagnostics)                    */
 } jf_result;
 

@@ -51,7 +51,7 @@ class jf_result(C.Structure):
         ("active_mask", C.c_int8 * JF_MAX_N),
         ("kernel_launches", C.c_int32), ("pad_", C.c_int32),
         ("t_upload_s", C.c_double), ("t_solve_s", C.c_double),
-        ("t_epilogue_s", C.c_double), ("epilogue_cycles", C.c_double * 4),
+        ("t_epilogue_s", C.c_double), ("epilogue_cycles", C.c_double * 8),
     ]
 
 

@@ -20,9 +20,16 @@
 
 #include "../../include/jf.h"
 #include "jf_kernels.h"
-#include "jf_solver.cuh"
+#include "jf_state.cuh"
 
 using namespace jf;
+
+namespace jf {  // jf_solver.cu
+const void* solver_kernel_ptr();
+int launch_solver(FitState* st, const double* kv, cudaStream_t s);
+int launch_tr_step(const double* hatG, const double* hatg, int n, int64_t m, double Delta, double alpha_in,
+                   double* out, int dbg, cudaStream_t s);
+}  // namespace jf
 
 // A rank's view of the multi-GPU mailboxes (jf.h jf_comm_*).
 struct jf_comm {
@@ -369,23 +376,39 @@ int build_graph(Ctx& c, const PassPair& k, int policy, cudaGraphExec_t* out) {
   int use = 1;
   PassArgs* pa = c.d_args;
   FitState* st = c.d_state;
-  void* args[4] = {&pa, &st, &h, &use};
+  const double* kv = c.d_out;
+  void* pargs[4] = {&pa, &st, &h, &use};
+  void* sargs[4] = {&st, &kv, &h, &use};
   cudaKernelNodeParams kp;
   memset(&kp, 0, sizeof(kp));
-  kp.sharedMemBytes = 0;
-  kp.kernelParams = args;
+  cudaKernelNodeParams sp;
+  memset(&sp, 0, sizeof(sp));
+  sp.func = const_cast<void*>(solver_kernel_ptr());
+  sp.gridDim = dim3(1);
+  sp.blockDim = dim3(32);
+  sp.kernelParams = sargs;
+  // body: [r-pass -> solver ->] J-pass -> solver; each pass kernel runs only
+  // when the state's phase asks for it, each solver only after a pass ran
   cudaGraphNode_t prev = nullptr;
+  auto add = [&](const cudaKernelNodeParams& p) -> int {
+    cudaGraphNode_t nd;
+    CK(cudaGraphAddKernelNode(&nd, body, prev ? &prev : nullptr, prev ? 1 : 0, &p));
+    prev = nd;
+    return 0;
+  };
+  kp.kernelParams = pargs;
   if (policy == JF_POLICY_CONSERVATIVE) {
     kp.func = (void*)k.r;
     kp.gridDim = dim3(k.rgrid);
     kp.blockDim = dim3(k.rtpb);
-    CK(cudaGraphAddKernelNode(&prev, body, nullptr, 0, &kp));
+    if (int e = add(kp)) return e;
+    if (int e = add(sp)) return e;
   }
   kp.func = (void*)k.j;
   kp.gridDim = dim3(k.jgrid);
   kp.blockDim = dim3(k.jtpb);
-  cudaGraphNode_t jn;
-  CK(cudaGraphAddKernelNode(&jn, body, prev ? &prev : nullptr, prev ? 1 : 0, &kp));
+  if (int e = add(kp)) return e;
+  if (int e = add(sp)) return e;
   CK(cudaGraphInstantiate(out, g, 0));
   cudaGraphDestroy(g);
   return 0;
@@ -648,6 +671,7 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
       const bool jac = (o.policy == JF_POLICY_CONSERVATIVE) ? (h.phase != PH_TRIAL_R) : true;
       r = launch_pass(k, jac, s, c->d_args, c->d_state);
       if (r) return fail(r);
+      if (launch_solver(c->d_state, c->d_out, s)) return fail(JF_ECUDA);
       CK(cudaMemcpyAsync(&h, c->d_state, sizeof(h), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
       if (!h.cont) break;
@@ -660,7 +684,7 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
   // ---- result
   out->kernel_launches = launches;
   out->t_epilogue_s = h.epi_ns * 1e-9;
-  for (int q = 0; q < 4; ++q) out->epilogue_cycles[q] = (double)h.prof[q];
+  for (int q = 0; q < 8; ++q) out->epilogue_cycles[q] = (double)h.prof[q];
   out->nfev = h.nfev;
   out->njev = h.njev;
   out->nit = h.nit;
@@ -693,35 +717,6 @@ int32_t jf_curve_fit(int32_t model, const double* y, const double* z, int64_t m,
 // ----------------------------------------------------- subproblem test hook
 }  // extern "C"
 
-namespace {
-__global__ void tr_step_kernel(const double* hatG, const double* hatg, int n, int64_t m, double Delta,
-                               double alpha_in, double* out, int getenv_dbg) {
-  __shared__ SolverSmem S;
-  const int lane = threadIdx.x;
-  for (int e = lane; e < n * n; e += 32) {
-    const int i = e / n, j = e % n;
-    S.A[i][j] = hatG[e];
-    S.M[i][j] = hatG[e];
-  }
-  __syncwarp();
-  double lam;
-  const long long c0 = clock64();
-  const int sw = warp_eig(S, n, lane, lam, 0);
-  const long long c1 = clock64();
-  const double g = lane < n ? hatg[lane] : 0.0;
-  const double suf = wVtx(S.V, g, n, lane);
-  double alpha = alpha_in, p;
-  const int it = warp_solve_tr(S, n, m, lam, suf, Delta, alpha, p, lane, nullptr);
-  const long long c2 = clock64();
-  if (lane == 0 && getenv_dbg) printf("tr_step n=%d sweeps=%d eig_cycles=%lld solve_cycles=%lld iters=%d\n", n, sw, c1 - c0, c2 - c1, it);
-  if (lane < n) out[lane] = p;
-  if (lane < n) out[NMAX + lane] = lam;
-  if (lane == 0) {
-    out[2 * NMAX] = alpha;
-    out[2 * NMAX + 1] = it;
-  }
-}
-}  // namespace
 
 extern "C" int32_t jf_trust_region_step(const double* hatG, const double* hatg, int32_t n, int64_t m, double Delta,
                                         double alpha_in, const jf_opts* opts, double* p, double* alpha_out,
@@ -741,8 +736,7 @@ extern "C" int32_t jf_trust_region_step(const double* hatG, const double* hatg, 
   double* dout = dg + n;
   CK(cudaMemcpyAsync(dG, hatG, sizeof(double) * n * n, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(dg, hatg, sizeof(double) * n, cudaMemcpyHostToDevice, s));
-  tr_step_kernel<<<1, 32, 0, s>>>(dG, dg, n, m, Delta, alpha_in, dout, getenv("JF_DEBUG") != nullptr);
-  CK(cudaGetLastError());
+  if (launch_tr_step(dG, dg, n, m, Delta, alpha_in, dout, getenv("JF_DEBUG") != nullptr, s)) return JF_ECUDA;
   double hout[2 * NMAX + 2];
   CK(cudaMemcpyAsync(hout, dout, sizeof(hout), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));

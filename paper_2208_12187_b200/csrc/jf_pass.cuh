@@ -29,7 +29,7 @@
 #include "jf_common.cuh"
 #include "jf_dual.cuh"
 #include "jf_models.cuh"
-#include "jf_solver.cuh"
+#include "jf_state.cuh"
 
 namespace jf {
 
@@ -319,7 +319,7 @@ __device__ __forceinline__ void grid_recur_loop(const PassArgs& a, const auto& p
 template <class Model, bool JAC>
 struct PassCfg {
   static constexpr bool BIG = JAC && Model::N >= 7;
-  static constexpr int P = JAC ? (Model::N == 7 ? 4 : 1) : 4;
+  static constexpr int P = JAC ? (Model::N == 7 ? 4 : 1) : (Model::N > 7 ? 2 : 4);
   static constexpr int TPB = 256;
   static constexpr int MINB = BIG ? 1 : 2;
   static constexpr int L = (JAC && Model::N > 7) ? 2 : 8;  // points per lane per warp-chunk (grid recurrence)
@@ -478,29 +478,13 @@ __global__ void __launch_bounds__(TPB, MINB)
     for (int k = threadIdx.x; k < KS; k += TPB) a.out[k] = vec[k];
     return;
   }
-  // ---- fit epilogue: one warp runs the solver state machine on a shared-
-  // memory copy of the state (no global-latency chains), then writes it back.
-  if (threadIdx.x < 32) {
-    __shared__ SolverSmem S;
-    __shared__ FitState sst;
-    unsigned long long t0;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    constexpr int NW = sizeof(FitState) / 8;
-    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(st);
-    unsigned long long* dst = reinterpret_cast<unsigned long long*>(&sst);
-    for (int k = threadIdx.x; k < NW; k += 32) dst[k] = src[k];
-    __syncwarp();
-    fit_after_pass(&sst, S, vec, JAC);
-    __syncwarp();
-    unsigned long long t1;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-    if (threadIdx.x == 0) sst.epi_ns += (t1 - t0);
-    __syncwarp();
-    unsigned long long* back = reinterpret_cast<unsigned long long*>(st);
-    for (int k = threadIdx.x; k < NW; k += 32) back[k] = dst[k];
-    __syncwarp();
-    if (threadIdx.x == 0 && use_cond) cudaGraphSetConditional(cond, sst.cont ? 1u : 0u);
-  }
+  (void)cond;
+  (void)use_cond;
+  // ---- fit: hand the combined K-vector to the solver kernel (jf_solver.cu)
+  for (int k = threadIdx.x; k < KS; k += TPB) a.out[k] = vec[k];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) st->pass_ready = JAC ? 1 : 2;
 }
 
 }  // namespace jf

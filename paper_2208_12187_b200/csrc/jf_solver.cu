@@ -1,0 +1,130 @@
+// jf_solver.cu — the single-warp solver kernel and the
+// stand-alone subproblem hook (jf_trust_region_step).
+//
+// One launch of solver_kernel follows every pass kernel of a fit: it takes
+// the pass's combined K-vector, advances the device state machine of
+// jf_solver.cuh (accept/reject, radius, termination, the next trust-region
+// step) and sets the CUDA-graph WHILE condition.  Keeping it out of the pass
+// kernels leaves their register allocation to the data-parallel loop.
+#include <cstdio>
+
+#include "jf_solver.cuh"
+
+namespace jf {
+
+__global__ void __launch_bounds__(32, 1)
+    solver_kernel(FitState* __restrict__ st, const double* __restrict__ kv, cudaGraphConditionalHandle cond,
+                  int use_cond) {
+  __shared__ SolverSmem S;
+  __shared__ FitState sst;
+  const int lane = threadIdx.x;
+  int cont;
+  if (st->pass_ready != 0) {
+    unsigned long long t0, t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    // state and the pass's K-vector into shared memory: all loads issued
+    // before any is consumed (one memory latency, not one per element)
+    constexpr int NW = sizeof(FitState) / 8;
+    constexpr int PER = (NW + 31) / 32;
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(st);
+    unsigned long long* dst = reinterpret_cast<unsigned long long*>(&sst);
+    unsigned long long buf[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int k = lane + 32 * q;
+      buf[q] = (k < NW) ? __ldcg(src + k) : 0ull;
+    }
+    double kvb[(KMAX + 31) / 32];
+#pragma unroll
+    for (int q = 0; q < (KMAX + 31) / 32; ++q) {
+      const int k = lane + 32 * q;
+      kvb[q] = (k < KMAX) ? __ldcg(kv + k) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int k = lane + 32 * q;
+      if (k < NW) dst[k] = buf[q];
+    }
+#pragma unroll
+    for (int q = 0; q < (KMAX + 31) / 32; ++q) {
+      const int k = lane + 32 * q;
+      if (k < KMAX) S.kvs[k] = kvb[q];
+    }
+    __syncwarp();
+    const bool jac = sst.pass_ready == 1;
+    solver_step(&sst, S, S.kvs, jac);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    if (lane == 0) {
+      sst.pass_ready = 0;
+      sst.epi_ns += (t1 - t0);
+    }
+    __syncwarp();
+    unsigned long long* back = reinterpret_cast<unsigned long long*>(st);
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int k = lane + 32 * q;
+      if (k < NW) back[k] = dst[k];
+    }
+    cont = sst.cont;
+  } else {
+    cont = st->cont;
+  }
+  if (lane == 0 && use_cond) cudaGraphSetConditional(cond, cont ? 1u : 0u);
+}
+
+const void* solver_kernel_ptr() { return (const void*)solver_kernel; }
+
+int launch_solver(FitState* st, const double* kv, cudaStream_t s) {
+  solver_kernel<<<1, 32, 0, s>>>(st, kv, (cudaGraphConditionalHandle)0, 0);
+  return cudaGetLastError() == cudaSuccess ? 0 : -4;
+}
+
+__global__ void tr_step_kernel(const double* hatG, const double* hatg, int n, int64_t m, double Delta,
+                               double alpha_in, double* out, int dbg) {
+  __shared__ SolverSmem S;
+  const int lane = threadIdx.x;
+  for (int e = lane; e < n * n; e += 32) {
+    const int i = e / n, j = e % n;
+    S.A[i][j] = hatG[e];
+    S.M[i][j] = hatG[e];
+  }
+  __syncwarp();
+  const long long c0 = clock64();
+  const int sw = warp_eig(S, n, 0);
+  const long long c1 = clock64();
+  if (lane == 0) {
+    double suf[NMAX], p[NMAX];
+    for (int j = 0; j < n; ++j) {  // suf = V^T g_hat
+      double t = 0.0;
+      for (int i = 0; i < n; ++i) t = fma(S.V[i][j], hatg[i], t);
+      suf[j] = t;
+    }
+    double alpha = alpha_in;
+    int it = -1;
+    switch (n) {
+#define JF_TR_CASE(N) \
+  case N: it = solve_tr<N>(S, m, suf, Delta, alpha, p); break;
+      JF_TR_CASE(1) JF_TR_CASE(2) JF_TR_CASE(3) JF_TR_CASE(4) JF_TR_CASE(5) JF_TR_CASE(6) JF_TR_CASE(7)
+      JF_TR_CASE(8) JF_TR_CASE(9) JF_TR_CASE(10) JF_TR_CASE(11) JF_TR_CASE(12) JF_TR_CASE(13)
+      JF_TR_CASE(14) JF_TR_CASE(15) JF_TR_CASE(16)
+#undef JF_TR_CASE
+      default: break;
+    }
+    const long long c2 = clock64();
+    if (dbg) printf("tr_step n=%d sweeps=%d eig_cycles=%lld solve_cycles=%lld iters=%d\n", n, sw, c1 - c0, c2 - c1, it);
+    for (int j = 0; j < n; ++j) {
+      out[j] = p[j];
+      out[NMAX + j] = S.lam[j];
+    }
+    out[2 * NMAX] = alpha;
+    out[2 * NMAX + 1] = it;
+  }
+}
+
+int launch_tr_step(const double* hatG, const double* hatg, int n, int64_t m, double Delta, double alpha_in,
+                   double* out, int dbg, cudaStream_t s) {
+  tr_step_kernel<<<1, 32, 0, s>>>(hatG, hatg, n, m, Delta, alpha_in, out, dbg);
+  return cudaGetLastError() == cudaSuccess ? 0 : -4;
+}
+
+}  // namespace jf

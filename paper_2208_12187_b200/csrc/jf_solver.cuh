@@ -1,11 +1,11 @@
-// jf_solver.cuh — the n x n trust-region subproblem and the iteration control,
-// executed by ONE warp on the device.
+// jf_solver.cuh — the n x n trust-region subproblem and the iteration control
+// of a fit, run on the device between passes.
 //
 // Everything the paper runs "in NumPy on the CPU" between passes (P:226, P:343:
-// the alpha sub-problem and the radius logic) runs here, in the last block of
-// each pass kernel, so a fit never returns to the host between iterations.
+// the alpha sub-problem and the radius logic) runs here, in the solver kernel
+// that follows every pass kernel, so a fit never returns to the host.
 //
-//   Alg. 1  outer loop, Gauss-Newton trial p_t = -B^-1 g
+//   Alg. 1  outer loop; Gauss-Newton trial p_t = -B^-1 g (l.141)
 //   Alg. 2  LM parameter alpha: Eq. 13 phi, Eq. 14 Newton update,
 //                       safeguard max{0.001 u, sqrt(l u)}
 //   Alg. 3  accept / reject and radius update, Eq. 15 gain ratio
@@ -16,298 +16,268 @@
 // Readings R3-R27 of DESIGN.md §3 fix what the paper leaves open (SciPy TRF
 // semantics, P:42 / P:246), including the Coleman-Li bounded path (R19, R20).
 //
-// Warp conventions: vector element j lives in lane j (j < n; other lanes hold
-// 0); scalars are computed redundantly and identically by all 32 lanes (every
-// reduction is a commutative xor-butterfly, so all lanes see bit-identical
-// values); matrices live in shared memory.
+// Execution model: the work between passes is a few hundred flops on n <= 16
+// vectors, a chain of dependent steps.  It runs as plain scalar code on lane 0
+// over shared memory (no shuffle or barrier latency per step); the one
+// parallel kernel, the Jacobi eigensolver, uses the whole warp and is only
+// entered when a trial needs alpha > 0 or the rank test cannot be certified
+// from the Cholesky factor (gn_fastpath below).
 #pragma once
 
 #include <cfloat>
 #include <cmath>
 
 #include "jf_common.cuh"
+#include "jf_state.cuh"
 
 namespace jf {
 
-enum Phase : int32_t {
-  PH_INIT_J = 0,    // J-pass at x0
-  PH_TRIAL_J = 1,   // speculative policy: J-pass at a trial point
-  PH_TRIAL_R = 2,   // conservative policy: residual pass at a trial point
-  PH_ACCEPT_J = 3,  // conservative policy: J-pass at the accepted point
-  PH_DONE = 4
-};
-
-constexpr int TRACE_FIELDS = 12;
-constexpr int STATUS_NONE = -100;
-
-struct FitState {
-  // ---- configuration (written by the host before the first launch)
-  int32_t n, bounded, jacmode, max_nfev;
-  int32_t policy, trace_cap, pad0, pad1;
-  int64_t m_global;
-  double ftol, xtol, gtol;
-  double lb[NMAX], ub[NMAX], xs_inv[NMAX];
-  double* trace;
-  // ---- iteration state
-  int32_t phase, status, nfev, njev, nit, cont, error, trace_len;
-  int32_t full_rank, branch, launches, have_V;
-  unsigned long long comm_epoch;
-  unsigned long long epi_ns;  // device time spent in the solver epilogue (globaltimer)
-  long long prof[4];          // SM cycles: eig, solve_tr, select_step, fit_after_pass
-  double cost, cost_new, Delta, alpha, gnorm, theta, actual;
-  double pred, hn, step_norm, Delta_used, ratio, pad4;
-  double x[NMAX], x_eval[NMAX];
-  double g[NMAX], G[NMAX * NMAX], scale_inv[NMAX];
-  // hat space of the current iterate (reused by rejected trials, R15)
-  double d[NMAX], diag_h[NMAX], gh[NMAX], Gh[NMAX * NMAX], lam[NMAX], V[NMAX * NMAX], suf[NMAX];
-  double step[NMAX], step_h[NMAX];
-  double kv[KMAX];  // K-vector of the last pass
-};
+constexpr int MS = NMAX + 1;  // shared-memory matrix row stride
 
 struct SolverSmem {
-  double A[NMAX][NMAX + 1];
-  double V[NMAX][NMAX + 1];
-  double M[NMAX][NMAX + 1];  // scaled Gram (incl. diag_h) for quadratic forms
-  double T[NMAX][NMAX + 1];  // scratch
-  double c[NMAX], e[NMAX];
-  int partner[NMAX];
+  double A[NMAX][MS];   // eigensolver input / output (diagonal)
+  double V[NMAX][MS];   // eigenvectors (columns)
+  double M[NMAX][MS];   // B_hat (incl. diag_h): quadratic forms
+  double T[NMAX][MS];   // scratch (Cholesky factor, warm-start product)
+  double M2[NMAX][MS];  // scratch
+  double lam[NMAX];     // eigenvalues, descending
+  double w1[NMAX], w2[NMAX], w3[NMAX], w4[NMAX], w5[NMAX];
+  double cinv[NMAX];
+  double kvs[KMAX];  // the pass's K-vector (shared-memory copy)
+  int need_eig, need_trial, fast;
 };
 
-// ------------------------------------------------------------ warp helpers
-static __device__ __forceinline__ double wsum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-  return v;
+// ------------------------------------------------------ scalar vector helpers
+template <int n>
+__device__ __forceinline__ double vdot(const double* a, const double* b) {
+  double s = 0.0;
+  for (int j = 0; j < n; ++j) s = fma(a[j], b[j], s);
+  return s;
 }
-static __device__ __forceinline__ double wmin(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(FULL, v, o));
-  return v;
-}
-static __device__ __forceinline__ double wmax(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, o));
-  return v;
-}
-static __device__ __forceinline__ bool wall(bool b) { return __all_sync(FULL, b); }
-static __device__ __forceinline__ bool wany(bool b) { return __any_sync(FULL, b); }
-static __device__ __forceinline__ double lanev(double v, int src) { return __shfl_sync(FULL, v, src); }
-static __device__ __forceinline__ double wdot(double a, double b) { return wsum(a * b); }
-static __device__ __forceinline__ double wnorm(double a) { return sqrt(wsum(a * a)); }
-
-// y = M x for an n x n matrix in shared memory (row-major, stride NMAX+1).
-static __device__ __forceinline__ double wmatvec(const double (*M)[NMAX + 1], double x, int n, int lane) {
-  double y = 0.0;
-  for (int k = 0; k < n; ++k) {
-    const double xk = lanev(x, k);
-    if (lane < n) y = fma(M[lane][k], xk, y);
+template <int n>
+__device__ __forceinline__ double vnorm(const double* a) { return sqrt(vdot<n>(a, a)); }
+// y = M x (row-major, stride MS)
+template <int n>
+__device__ __forceinline__ void vmatvec(const double (*M)[MS], const double* x, double* y) {
+  for (int i = 0; i < n; ++i) {
+    double s = 0.0;
+    for (int k = 0; k < n; ++k) s = fma(M[i][k], x[k], s);
+    y[i] = s;
   }
-  return lane < n ? y : 0.0;
 }
-// y = V x (V columns are eigenvectors)
-static __device__ __forceinline__ double wVx(const double (*V)[NMAX + 1], double x, int n, int lane) {
-  return wmatvec(V, x, n, lane);
-}
-// y = V^T x
-static __device__ __forceinline__ double wVtx(const double (*V)[NMAX + 1], double x, int n, int lane) {
-  double y = 0.0;
-  for (int k = 0; k < n; ++k) {
-    const double xk = lanev(x, k);
-    if (lane < n) y = fma(V[k][lane], xk, y);
+// x^T M x
+template <int n>
+__device__ __forceinline__ double vquad(const double (*M)[MS], const double* x) {
+  double s = 0.0;
+  for (int i = 0; i < n; ++i) {
+    double r = 0.0;
+    for (int k = 0; k < n; ++k) r = fma(M[i][k], x[k], r);
+    s = fma(x[i], r, s);
   }
-  return lane < n ? y : 0.0;
-}
-// s^T M s
-static __device__ __forceinline__ double wquad(const double (*M)[NMAX + 1], double s, int n, int lane) {
-  return wdot(s, wmatvec(M, s, n, lane));
-}
-// u^T M v
-static __device__ __forceinline__ double wbilin(const double (*M)[NMAX + 1], double u, double v, int n, int lane) {
-  return wdot(u, wmatvec(M, v, n, lane));
+  return s;
 }
 
 // ---------------------------------------------------- symmetric eigensolver
-// Parallel (round-robin) cyclic Jacobi on the n x n symmetric matrix in S.A:
-// on return lam (lane j, j < n) holds the eigenvalues sorted descending and
-// the columns of S.V the matching orthonormal eigenvectors.  This is App. B's
-// SVD of the scaled Jacobian computed through its Gram matrix (c.1b).
+// Parallel (round-robin) cyclic Jacobi on the n x n symmetric matrix in S.A,
+// the whole warp cooperating: on return S.lam holds the eigenvalues sorted
+// descending and the columns of S.V the matching orthonormal eigenvectors —
+// App. B's SVD of the scaled Jacobian computed through its Gram (c.1b).
 //
-// warm != 0: S.V holds an orthogonal matrix V0 on entry (the previous
-// iterate's eigenvectors); the sweeps run on V0^T A V0, which is nearly
-// diagonal between consecutive iterations, and accumulate onto V0 — one or
-// two sweeps instead of six.  Rotations are skipped when
-// |a_pq| <= eps sqrt(|a_pp a_qq|) or |a_pq| <= 2^-60 max_i |a_ii|; the
-// sweep loop ends when a sweep applies none.
-static __device__ __noinline__ int warp_eig(SolverSmem& S, int n, int lane, double& lam_out, int warm) {
-  const int N2 = (n + 1) & ~1;  // pad to even with a zero row / column
+// Register-resident: lane j owns column j of A and of V (n padded to an even
+// N2 with a zero row/column).  Round r of a sweep rotates the N2/2 disjoint
+// pairs of the circle schedule (partner of i: 2r - i mod N2-1, N2-1 <-> r)
+// at once: both lanes of a pair compute the same rotation, the column update
+// takes the partner's column by shuffle, the row update every pair's (c, s);
+// the round loop is unrolled so every row index is static.
+//
+// warm != 0: S.V holds an orthogonal V0 on entry (an earlier iterate's
+// eigenvectors); the sweeps run on V0^T A V0 and accumulate onto V0.  A
+// rotation is skipped when |a_pq| <= eps sqrt(|a_pp a_qq|) or |a_pq| <=
+// 2^-60 max_i |a_ii|; the sweeps stop when one applies none.
+template <int N2>
+__device__ __forceinline__ int jacobi_regs(double (&a)[N2], double (&v)[N2], int lane, double abs_tol) {
+  int sweeps = 0;
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    ++sweeps;
+    bool any = false;
+#pragma unroll
+    for (int r = 0; r < N2 - 1; ++r) {
+      int pj;
+      if (lane == N2 - 1) pj = r;
+      else if (lane == r) pj = N2 - 1;
+      else pj = ((2 * r - lane) % (N2 - 1) + (N2 - 1)) % (N2 - 1);
+      const bool act = lane < N2;
+      if (!act) pj = lane;
+      double dj = 0.0, apq = 0.0;
+#pragma unroll
+      for (int i = 0; i < N2; ++i) {
+        if (i == lane) dj = a[i];
+        if (i == pj) apq = a[i];
+      }
+      const double dq = __shfl_sync(FULL, dj, pj);
+      const bool lo = lane < pj;
+      const double app = lo ? dj : dq, aqq = lo ? dq : dj;
+      double c = 1.0, s = 0.0;
+      const double aa = fabs(apq);
+      bool rot = false;
+      if (act && !(aa <= abs_tol || aa <= 1.1102230246251565e-16 * sqrt(fabs(app) * fabs(aqq)))) {
+        // t = tan(phi), the smaller root: 2 apq sgn(d) / (|d| + sqrt(d^2 + 4 apq^2)), d = aqq - app
+        const double d = aqq - app;
+        const double t = (2.0 * apq) * (d >= 0.0 ? 1.0 : -1.0) / (fabs(d) + sqrt(fma(d, d, 4.0 * apq * apq)));
+        c = rsqrt(fma(t, t, 1.0));
+        s = t * c;
+        rot = true;
+      }
+      // P[p][p] = P[q][q] = c, P[p][q] = s, P[q][p] = -s;  e_j = P[partner j][j]
+      const double e = lo ? -s : s;
+      if (!__any_sync(FULL, rot)) continue;
+      any = true;
+#pragma unroll
+      for (int i = 0; i < N2; ++i) {  // B = A P
+        const double pc = __shfl_sync(FULL, a[i], pj);
+        a[i] = fma(c, a[i], e * pc);
+      }
+      double na[N2];
+#pragma unroll
+      for (int i = 0; i < N2; ++i) {  // A' = P^T B
+        const int pi = (i == N2 - 1) ? r : (i == r ? N2 - 1 : ((2 * r - i) % (N2 - 1) + (N2 - 1)) % (N2 - 1));
+        const double ci = __shfl_sync(FULL, c, i), ei = __shfl_sync(FULL, e, i);
+        na[i] = fma(ci, a[i], ei * a[pi]);
+      }
+#pragma unroll
+      for (int i = 0; i < N2; ++i) a[i] = (rot && i == pj) ? 0.0 : na[i];
+#pragma unroll
+      for (int i = 0; i < N2; ++i) {  // V' = V P
+        const double pv = __shfl_sync(FULL, v[i], pj);
+        v[i] = fma(c, v[i], e * pv);
+      }
+    }
+    if (!any) break;
+  }
+  return sweeps;
+}
+
+template <int N2>
+__device__ __forceinline__ int eig_regs(SolverSmem& S, int n, int lane, double abs_tol) {
+  double a[N2], v[N2];
+#pragma unroll
+  for (int i = 0; i < N2; ++i) {
+    a[i] = (lane < n && i < n) ? S.A[i][lane] : 0.0;
+    v[i] = (lane < n && i < n) ? S.V[i][lane] : ((i == lane) ? 1.0 : 0.0);
+  }
+  const int sw = jacobi_regs<N2>(a, v, lane, abs_tol);
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < N2; ++i) {
+    if (lane < n && i < n) {
+      S.V[i][lane] = v[i];
+      if (i == lane) S.A[i][i] = a[i];
+    }
+  }
+  __syncwarp();
+  return sw;
+}
+
+// All 32 lanes.  In: S.A (n x n symmetric), S.V = V0 if warm.  Out: S.lam, S.V.
+__device__ __noinline__ int warp_eig(SolverSmem& S, int n, int warm) {
+  const int lane = threadIdx.x & 31;
   if (!warm) {
     for (int e = lane; e < NMAX * NMAX; e += 32) {
       const int i = e / NMAX, j = e % NMAX;
-      if (i >= n || j >= n) S.A[i][j] = 0.0;
       S.V[i][j] = (i == j) ? 1.0 : 0.0;
     }
     __syncwarp();
   } else {
-    // T = A V0, then A = V0^T T (lane-parallel over elements)
-    for (int e = lane; e < n * n; e += 32) {
+    for (int e = lane; e < n * n; e += 32) {  // T = A V0
       const int i = e / n, j = e % n;
       double t = 0.0;
       for (int k = 0; k < n; ++k) t = fma(S.A[i][k], S.V[k][j], t);
       S.T[i][j] = t;
     }
     __syncwarp();
-    for (int e = lane; e < NMAX * NMAX; e += 32) {
-      const int i = e / NMAX, j = e % NMAX;
-      double t = 0.0;
-      if (i < n && j < n) {
+    for (int e = lane; e < n * n; e += 32) {  // V0^T T (upper half)
+      const int i = e / n, j = e % n;
+      if (i <= j) {
+        double t = 0.0;
         for (int k = 0; k < n; ++k) t = fma(S.V[k][i], S.T[k][j], t);
+        S.M2[i][j] = t;
       }
-      S.A[i][j] = t;
-      if (i >= n || j >= n) S.V[i][j] = (i == j) ? 1.0 : 0.0;
     }
     __syncwarp();
-    // exact symmetry
     for (int e = lane; e < n * n; e += 32) {
       const int i = e / n, j = e % n;
-      if (i < j) S.A[j][i] = S.A[i][j];
+      S.A[i][j] = (i <= j) ? S.M2[i][j] : S.M2[j][i];  // exactly symmetric
     }
     __syncwarp();
   }
-  double amax = (lane < n) ? fabs(S.A[lane][lane]) : 0.0;
-  amax = wmax(amax);
+  double amax = 0.0;
+  for (int i = 0; i < n; ++i) amax = fmax(amax, fabs(S.A[i][i]));
   const double abs_tol = amax * 8.673617379884035e-19;  // 2^-60
-  int sweeps = 0;
-  for (int sweep = 0; sweep < 40; ++sweep) {
-    bool rotated = false;
-    ++sweeps;
-    for (int r = 0; r < N2 - 1; ++r) {
-      // pair k: (p, q) from the circle method
-      if (lane < N2 / 2) {
-        int p, q;
-        if (lane == 0) {
-          p = r;
-          q = N2 - 1;
-        } else {
-          p = (r + lane) % (N2 - 1);
-          q = (r - lane + (N2 - 1)) % (N2 - 1);
-        }
-        if (p > q) {
-          const int t = p;
-          p = q;
-          q = t;
-        }
-        const double apq = S.A[p][q], app = S.A[p][p], aqq = S.A[q][q];
-        double c = 1.0, s = 0.0;
-        const double aa = fabs(apq);
-        const bool tiny = aa <= abs_tol || aa <= 1.1102230246251565e-16 * sqrt(fabs(app) * fabs(aqq));
-        if (!tiny) {
-          // t = tan(phi), the smaller root: t = 2 apq sgn(d) / (|d| + sqrt(d^2 + 4 apq^2)), d = aqq - app
-          const double d = aqq - app;
-          const double t = (2.0 * apq) * (d >= 0.0 ? 1.0 : -1.0) / (fabs(d) + sqrt(fma(d, d, 4.0 * apq * apq)));
-          c = rsqrt(fma(t, t, 1.0));
-          s = t * c;
-          rotated = true;
-        }
-        // P[p][p] = c, P[p][q] = s, P[q][p] = -s, P[q][q] = c; A' = P^T A P
-        S.c[p] = c;
-        S.c[q] = c;
-        S.e[p] = -s;  // P[q][p]
-        S.e[q] = s;   // P[p][q]
-        S.partner[p] = q;
-        S.partner[q] = p;
-      }
-      __syncwarp();
-      rotated = wany(rotated);
-      if (!rotated) continue;
-      // write phase: A' = P^T A P, V' = V P (each lane owns up to 8 elements)
-      double newA[8], newV[8];
-      int cnt = 0;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int e = lane + 32 * k;
-        if (e < N2 * N2) {
-          const int i = e / N2, j = e % N2;
-          const int ib = S.partner[i], jb = S.partner[j];
-          const double ci = S.c[i], ei = S.e[i], cj = S.c[j], ej = S.e[j];
-          newA[k] = ci * (cj * S.A[i][j] + ej * S.A[i][jb]) + ei * (cj * S.A[ib][j] + ej * S.A[ib][jb]);
-          newV[k] = cj * S.V[i][j] + ej * S.V[i][jb];
-        }
-      }
-      (void)cnt;
-      __syncwarp();
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int e = lane + 32 * k;
-        if (e < N2 * N2) {
-          const int i = e / N2, j = e % N2;
-          S.A[i][j] = (S.partner[i] == j && i != j) ? 0.0 : newA[k];
-          S.V[i][j] = newV[k];
-        }
-      }
-      __syncwarp();
-    }
-    if (!__any_sync(FULL, rotated)) break;
+  const int N2 = (n + 1) & ~1;
+  int sweeps;
+  switch (N2) {
+    case 2: sweeps = eig_regs<2>(S, n, lane, abs_tol); break;
+    case 4: sweeps = eig_regs<4>(S, n, lane, abs_tol); break;
+    case 6: sweeps = eig_regs<6>(S, n, lane, abs_tol); break;
+    case 8: sweeps = eig_regs<8>(S, n, lane, abs_tol); break;
+    case 10: sweeps = eig_regs<10>(S, n, lane, abs_tol); break;
+    case 12: sweeps = eig_regs<12>(S, n, lane, abs_tol); break;
+    case 14: sweeps = eig_regs<14>(S, n, lane, abs_tol); break;
+    default: sweeps = eig_regs<16>(S, n, lane, abs_tol); break;
   }
-  // sort descending (ties by index); permute V columns accordingly
-  double lam = (lane < n) ? S.A[lane][lane] : 0.0;
+  // sort descending (ties by index); permute the columns of V accordingly
   int rank = 0;
+  const double lj = (lane < n) ? S.A[lane][lane] : 0.0;
   for (int k = 0; k < n; ++k) {
-    const double lk = lanev(lam, k);
-    if (lane < n && (lk > lam || (lk == lam && k < lane))) ++rank;
+    const double lk = S.A[k][k];
+    if (lane < n && (lk > lj || (lk == lj && k < lane))) ++rank;
   }
   for (int e = lane; e < n * n; e += 32) {
     const int i = e / n, j = e % n;
     S.T[i][j] = S.V[i][j];
   }
   __syncwarp();
-  for (int j = 0; j < n; ++j) {
-    const int rj = __shfl_sync(FULL, rank, j);
-    if (lane < n) S.V[lane][rj] = S.T[lane][j];
+  if (lane < n) {
+    S.lam[rank] = lj;
+    for (int i = 0; i < n; ++i) S.V[i][rank] = S.T[i][lane];
   }
   __syncwarp();
-  double sorted = 0.0;
-  for (int j = 0; j < n; ++j) {
-    const int rj = __shfl_sync(FULL, rank, j);
-    const double lj = lanev(lam, j);
-    if (lane == rj) sorted = lj;
-  }
-  lam_out = (lane < n) ? sorted : 0.0;
   return sweeps;
 }
 
-// --------------------------------------------------- Alg. 2 + App. B on device
-// Inputs: lam (descending eigenvalues of B_hat, lane j), V (S.V), suf = V^T g_hat
-// (lane j), radius Delta, warm-start alpha, m (number of residuals, R6).
-// Output: p (lane j), alpha, number of Moré iterations (0 = Gauss-Newton).
-static __device__ __noinline__ int warp_solve_tr(const SolverSmem& S, int n, int64_t m, double lam, double suf, double Delta,
-                             double& alpha, double& p_out, int lane, int* full_rank_out) {
-  const bool act = lane < n;
-  const double s = act ? sqrt(fmax(lam, 0.0)) : 0.0;
-  const double s2 = s * s;
-  const double s_max = lanev(s, 0), s_min = lanev(s, n - 1);
-  const bool full_rank = (m >= n) && (s_min > DBL_EPSILON * (double)m * s_max);  // R6
-  if (full_rank_out) *full_rank_out = full_rank ? 1 : 0;
-  if (full_rank) {
-    // Alg. 1 l.141: p_t = -V (uf / s), uf = suf / s
-    const double coef = act ? (suf / s) / s : 0.0;
-    const double p = -wVx(S.V, coef, n, lane);
-    if (wnorm(p) <= Delta) {  // Alg. 1 l.142
-      p_out = p;
+// --------------------------------------------------- Alg. 2 + App. B (scalar)
+// In: S.lam (descending eigenvalues of B_hat), S.V, suf = V^T g_hat, radius
+// Delta, warm-start alpha, m (number of residuals, R6).  Out: p, alpha;
+// returns the number of Moré iterations (0 = Gauss-Newton step).
+template <int n>
+__device__ __noinline__ int solve_tr(SolverSmem& S, int64_t m, const double* suf, double Delta, double& alpha, double* p) {
+  double* s = S.w4;  // singular values s = sqrt(max(lam, 0))
+  double* coef = S.w5;
+  for (int j = 0; j < n; ++j) s[j] = sqrt(fmax(S.lam[j], 0.0));
+  const bool full_rank = (m >= n) && (s[n - 1] > DBL_EPSILON * (double)m * s[0]);  // R6
+  if (full_rank) {  // Alg. 1 l.141: p_t = -V (uf / s), uf = suf / s
+    for (int j = 0; j < n; ++j) coef[j] = -((suf[j] / s[j]) / s[j]);
+    vmatvec<n>(S.V, coef, p);
+    if (vnorm<n>(p) <= Delta) {  // Alg. 1 l.142
       alpha = 0.0;
       return 0;
     }
   }
-  // phi(alpha) = ||suf / (s^2 + alpha)|| - Delta;  phi' per R11
-  auto phi_d = [&](double a, double& phi, double& dphi) {
-    const double den = s2 + a;
-    const double q = act ? suf / den : 0.0;
-    const double pn = sqrt(wsum(q * q));
-    phi = pn - Delta;
-    const double t = act ? suf * suf / (den * den * den) : 0.0;
-    dphi = -wsum(t) / pn;
-  };
-  double u = sqrt(wsum(act ? suf * suf : 0.0)) / Delta;  // Alg. 2 l.160
+  double u = vnorm<n>(suf) / Delta;  // Alg. 2 l.160
   double l = 0.0;
+  // phi(alpha) = ||suf / (s^2 + alpha)|| - Delta  (Eq. 13);  phi' per R11
+  auto phi_d = [&](double a, double& phi, double& dphi) {
+    double pn2 = 0.0, t = 0.0;
+    for (int j = 0; j < n; ++j) {
+      const double den = s[j] * s[j] + a;
+      const double q = suf[j] / den;
+      pn2 = fma(q, q, pn2);
+      t += suf[j] * suf[j] / (den * den * den);
+    }
+    const double pn = sqrt(pn2);
+    phi = pn - Delta;
+    dphi = -t / pn;
+  };
   if (full_rank) {
     double phi, dphi;
     phi_d(0.0, phi, dphi);
@@ -321,29 +291,91 @@ static __device__ __noinline__ int warp_solve_tr(const SolverSmem& S, int n, int
     phi_d(alpha, phi, dphi);
     if (phi < 0.0) u = alpha;  // Alg. 2 l.173
     const double ratio = phi / dphi;
-    l = fmax(l, alpha - ratio);                          // Alg. 2 l.172
-    alpha = alpha - ((phi + Delta) / Delta) * ratio;     // Eq. 14
-    if (fabs(phi) < 0.01 * Delta) break;                 // R9
+    l = fmax(l, alpha - ratio);                       // Alg. 2 l.172
+    alpha = alpha - ((phi + Delta) / Delta) * ratio;  // Eq. 14
+    if (fabs(phi) < 0.01 * Delta) break;              // R9
   }
-  const double coef = act ? suf / (s2 + alpha) : 0.0;
-  double p = -wVx(S.V, coef, n, lane);  // Eq. B4 (sign R8)
-  p = p * (Delta / wnorm(p));           // R12
-  p_out = act ? p : 0.0;
+  for (int j = 0; j < n; ++j) coef[j] = -(suf[j] / (s[j] * s[j] + alpha));  // Eq. B4 (sign R8)
+  vmatvec<n>(S.V, coef, p);
+  const double sc = Delta / vnorm<n>(p);  // R12
+  for (int j = 0; j < n; ++j) p[j] *= sc;
   return it + 1;
 }
 
+// ------------------------------------------- Alg. 1 l.141: p_t = -B^-1 g
+// The Gauss-Newton trial of Alg. 1 by a Cholesky solve of the
+// scaled Gram, B_hat p = -g_hat.  App. B obtains the same p from the SVD; the
+// SVD (here: the eigendecomposition) is only needed when the trial is
+// rejected (||p|| > Delta) and Alg. 2 searches for alpha > 0, or when the rank
+// test R6 (s_min > EPS m s_max) cannot be certified.  The certificate is
+// conservative: s_max^2 <= trace(B_hat) and s_min^2 >= 1 / ||L^-1||_F^2
+// (B_hat = L L^T), so 1/||L^-1||_F > 2 EPS m sqrt(trace) implies R6.
+// Returns 1 with p when the certified trial lies inside the trust region.
+template <int n>
+__device__ __noinline__ int gn_fastpath(SolverSmem& S, int64_t m, const double* gh, double Delta, double* p) {
+  double(*L)[MS] = S.T;
+  double tr = 0.0;
+  for (int i = 0; i < n; ++i) {
+    tr += S.M[i][i];
+    for (int j = 0; j <= i; ++j) L[i][j] = S.M[i][j];
+  }
+  for (int k = 0; k < n; ++k) {  // left-looking Cholesky, lower triangle
+    double d = L[k][k];
+    for (int j = 0; j < k; ++j) d = fma(-L[k][j], L[k][j], d);
+    if (!(d > 0.0)) return 0;
+    const double r = rsqrt(d);
+    L[k][k] = d * r;
+    S.cinv[k] = r;
+    for (int i = k + 1; i < n; ++i) {
+      double t = L[i][k];
+      for (int j = 0; j < k; ++j) t = fma(-L[i][j], L[k][j], t);
+      L[i][k] = t * r;
+    }
+  }
+  double fro = 0.0;  // ||L^-1||_F^2, column by column
+  double* y = S.w1;
+  for (int c = 0; c < n; ++c) {
+    for (int i = c; i < n; ++i) {
+      double t = (i == c) ? 1.0 : 0.0;
+      for (int k = c; k < i; ++k) t = fma(-L[i][k], y[k], t);
+      y[i] = t * S.cinv[i];
+      fro = fma(y[i], y[i], fro);
+    }
+  }
+  if (!(m >= n && rsqrt(fro) > 2.0 * DBL_EPSILON * (double)m * sqrt(tr))) return 0;
+  double* w = S.w2;  // L w = -g_hat
+  for (int i = 0; i < n; ++i) {
+    double t = -gh[i];
+    for (int k = 0; k < i; ++k) t = fma(-L[i][k], w[k], t);
+    w[i] = t * S.cinv[i];
+  }
+  for (int i = n - 1; i >= 0; --i) {  // L^T p = w
+    double t = w[i];
+    for (int k = i + 1; k < n; ++k) t = fma(-L[k][i], p[k], t);
+    p[i] = t * S.cinv[i];
+  }
+  return vnorm<n>(p) <= Delta ? 1 : 0;
+}
+
 // --------------------------------------------------- Coleman-Li helpers (R19)
-// Smallest t >= 0 with x + t s on a bound; hit pattern sign(s_j) where attained.
-static __device__ __forceinline__ double w_step_to_bound(double x, double s, double lb, double ub, bool act, int& hit) {
-  double st = INFINITY;
-  if (act && s != 0.0) st = fmax((lb - x) / s, (ub - x) / s);
-  const double t = wmin(st);
-  hit = (act && st == t) ? (s > 0.0 ? 1 : (s < 0.0 ? -1 : 0)) : 0;
-  return t;
+// Smallest t >= 0 with x + t s on a bound; hits[j] = sign(s_j) where attained.
+__device__ __forceinline__ double step_to_bound(const double* x, const double* s, const double* lb, const double* ub,
+                                                int n, int* hits) {
+  double tmin = INFINITY;
+  double st[NMAX];
+  for (int j = 0; j < n; ++j) {
+    st[j] = INFINITY;
+    if (s[j] != 0.0) st[j] = fmax((lb[j] - x[j]) / s[j], (ub[j] - x[j]) / s[j]);
+    tmin = fmin(tmin, st[j]);
+  }
+  if (hits) {
+    for (int j = 0; j < n; ++j) hits[j] = (st[j] == tmin) ? (s[j] > 0.0 ? 1 : (s[j] < 0.0 ? -1 : 0)) : 0;
+  }
+  return tmin;
 }
 
 // 1-D quadratic minimiser on [lo, hi]: candidates lo, hi, vertex (R20)
-static __device__ __forceinline__ void min_quad_1d(double a, double b, double lo, double hi, double c, double& t_out,
+__device__ __forceinline__ void min_quad_1d(double a, double b, double lo, double hi, double c, double& t_out,
                                             double& y_out) {
   double ts[3] = {lo, hi, 0.0};
   int nt = 2;
@@ -351,15 +383,13 @@ static __device__ __forceinline__ void min_quad_1d(double a, double b, double lo
     const double ext = -0.5 * b / a;
     if (lo < ext && ext < hi) ts[nt++] = ext;
   }
-  double best = INFINITY;
-  double bt = lo;
-  bool first = true;
-  for (int k = 0; k < nt; ++k) {
+  double best = ts[0] * (a * ts[0] + b) + c;
+  double bt = ts[0];
+  for (int k = 1; k < nt; ++k) {
     const double y = ts[k] * (a * ts[k] + b) + c;
-    if (first || y < best) {
+    if (y < best) {
       best = y;
       bt = ts[k];
-      first = false;
     }
   }
   t_out = bt;
@@ -367,43 +397,49 @@ static __device__ __forceinline__ void min_quad_1d(double a, double b, double lo
 }
 
 // Q(s) = 1/2 s^T B s + g^T s  (B = B_hat incl. diag_h; R13)
-static __device__ __forceinline__ double w_eval_quad(const SolverSmem& S, double gh, double s, int n, int lane) {
-  return 0.5 * wquad(S.M, s, n, lane) + wdot(s, gh);
+template <int n>
+__device__ __forceinline__ double eval_quad(const SolverSmem& S, const double* gh, const double* s) {
+  return 0.5 * vquad<n>(S.M, s) + vdot<n>(s, gh);
 }
 
-// Coleman-Li step selection (R19, R20).  In: p_h (lane), d, x, lb, ub, g_hat.
-// Out: step (original space), step_h (hat space), predicted reduction, branch.
-static __device__ __noinline__ void w_select_step(const SolverSmem& S, int n, int lane, double x, double lb, double ub, double gh,
-                              double d, double p_h, double Delta, double theta, double& step, double& step_h,
-                              double& pred, int& branch) {
-  const bool act = lane < n;
-  double p = d * p_h;
-  const bool inb = wall(!act || ((x + p) >= lb && (x + p) <= ub));
+// Coleman-Li step selection (R19, R20).  In: p_h, d, x, lb, ub, g_hat.
+// Out: step (original space), step_h (hat space), predicted reduction, branch
+// (0 interior, 1 reflected, 2 truncated, 3 scaled gradient).
+template <int n>
+__device__ __noinline__ void select_step(SolverSmem& S, const double* x, const double* lb, const double* ub, const double* gh, const double* d, const double* p_h, double Delta, double theta, double* step, double* step_h, double& pred, int& branch) {
+  double p[NMAX], ph[NMAX], r_h[NMAX], r[NMAX], xb[NMAX], ag_h[NMAX], ag[NMAX], tmp[NMAX];
+  bool inb = true;
+  for (int j = 0; j < n; ++j) {
+    p[j] = d[j] * p_h[j];
+    const double xn = x[j] + p[j];
+    inb = inb && xn >= lb[j] && xn <= ub[j];
+  }
   if (inb) {
-    step = p;
-    step_h = p_h;
-    pred = -w_eval_quad(S, gh, p_h, n, lane);
+    for (int j = 0; j < n; ++j) {
+      step[j] = p[j];
+      step_h[j] = p_h[j];
+    }
+    pred = -eval_quad<n>(S, gh, p_h);
     branch = 0;
     return;
   }
-  int hit;
-  const double t_b = w_step_to_bound(x, p, lb, ub, act, hit);
-  double r_h = (hit != 0) ? -p_h : p_h;
-  double r = d * r_h;
-  p = p * t_b;
-  double ph = p_h * t_b;
-  const double x_b = x + p;
-  // to_tr: the positive root of ||ph + t r_h|| = Delta (stable form)
-  double to_tr;
+  int hits[NMAX];
+  const double t_b = step_to_bound(x, p, lb, ub, n, hits);
+  for (int j = 0; j < n; ++j) {
+    r_h[j] = hits[j] ? -p_h[j] : p_h[j];
+    r[j] = d[j] * r_h[j];
+    p[j] *= t_b;
+    ph[j] = p_h[j] * t_b;
+    xb[j] = x[j] + p[j];
+  }
+  double to_tr;  // positive root of ||ph + t r_h|| = Delta (stable form)
   {
-    const double a = wdot(r_h, r_h), b = wdot(ph, r_h), c = wdot(ph, ph) - Delta * Delta;
+    const double a = vdot<n>(r_h, r_h), b = vdot<n>(ph, r_h), c = vdot<n>(ph, ph) - Delta * Delta;
     const double dd = sqrt(b * b - a * c);
     const double q = -(b + copysign(dd, b));
-    const double t1 = q / a, t2 = c / q;
-    to_tr = fmax(t1, t2);
+    to_tr = fmax(q / a, c / q);
   }
-  int hit2;
-  const double to_bd = w_step_to_bound(x_b, r, lb, ub, act, hit2);
+  const double to_bd = step_to_bound(xb, r, lb, ub, n, nullptr);
   const double rs = fmin(to_bd, to_tr);
   double lo, hi;
   if (rs > 0.0) {
@@ -414,61 +450,69 @@ static __device__ __noinline__ void w_select_step(const SolverSmem& S, int n, in
     hi = -1.0;
   }
   double r_val;
-  if (lo <= hi) {
-    // Q(ph + t r_h) = a t^2 + b t + c
-    const double Mr = wmatvec(S.M, r_h, n, lane);
-    const double a = 0.5 * wdot(r_h, Mr);
-    const double b = wdot(gh, r_h) + wdot(ph, Mr);
-    const double c = 0.5 * wquad(S.M, ph, n, lane) + wdot(gh, ph);
+  if (lo <= hi) {  // Q(ph + t r_h) = a t^2 + b t + c
+    vmatvec<n>(S.M, r_h, tmp);
+    const double a = 0.5 * vdot<n>(r_h, tmp);
+    const double b = vdot<n>(gh, r_h) + vdot<n>(ph, tmp);
+    const double c = 0.5 * vquad<n>(S.M, ph) + vdot<n>(gh, ph);
     double rt;
     min_quad_1d(a, b, lo, hi, c, rt, r_val);
-    r_h = ph + rt * r_h;
-    r = r_h * d;
+    for (int j = 0; j < n; ++j) {
+      r_h[j] = ph[j] + rt * r_h[j];
+      r[j] = r_h[j] * d[j];
+    }
   } else {
     r_val = INFINITY;
   }
-  p = p * theta;
-  ph = ph * theta;
-  const double p_val = w_eval_quad(S, gh, ph, n, lane);
-  double ag_h = -gh;
-  double ag = d * ag_h;
-  const double t_tr = Delta / wnorm(ag_h);
-  int hit3;
-  const double t_bd = w_step_to_bound(x, ag, lb, ub, act, hit3);
+  for (int j = 0; j < n; ++j) {
+    p[j] *= theta;
+    ph[j] *= theta;
+  }
+  const double p_val = eval_quad<n>(S, gh, ph);
+  for (int j = 0; j < n; ++j) {
+    ag_h[j] = -gh[j];
+    ag[j] = d[j] * ag_h[j];
+  }
+  const double t_tr = Delta / vnorm<n>(ag_h);
+  const double t_bd = step_to_bound(x, ag, lb, ub, n, nullptr);
   const double stride = (t_bd < t_tr) ? theta * t_bd : t_tr;
   double at, ag_val;
   {
-    const double a = 0.5 * wquad(S.M, ag_h, n, lane);
-    const double b = wdot(gh, ag_h);
+    const double a = 0.5 * vquad<n>(S.M, ag_h);
+    const double b = vdot<n>(gh, ag_h);
     min_quad_1d(a, b, 0.0, stride, 0.0, at, ag_val);
   }
-  ag_h = ag_h * at;
-  ag = ag * at;
+  for (int j = 0; j < n; ++j) {
+    ag_h[j] *= at;
+    ag[j] *= at;
+  }
+  const double* ss;
+  const double* sh;
   if (p_val < r_val && p_val < ag_val) {
-    step = p;
-    step_h = ph;
+    ss = p;
+    sh = ph;
     pred = -p_val;
     branch = 2;
   } else if (r_val < p_val && r_val < ag_val) {
-    step = r;
-    step_h = r_h;
+    ss = r;
+    sh = r_h;
     pred = -r_val;
     branch = 1;
   } else {
-    step = ag;
-    step_h = ag_h;
+    ss = ag;
+    sh = ag_h;
     pred = -ag_val;
     branch = 3;
   }
-  if (!act) {
-    step = 0.0;
-    step_h = 0.0;
+  for (int j = 0; j < n; ++j) {
+    step[j] = ss[j];
+    step_h[j] = sh[j];
   }
 }
 
 // rstep = 0 strict feasibility (R19): x <= lb -> nextafter(lb, ub), x >= ub ->
 // nextafter(ub, lb); still outside -> midpoint.
-static __device__ __forceinline__ double strict_feasible0(double x, double lb, double ub) {
+__device__ __forceinline__ double strict_feasible0(double x, double lb, double ub) {
   double xn = x;
   if (x <= lb) xn = nextafter(lb, ub);
   else if (x >= ub) xn = nextafter(ub, lb);
@@ -476,59 +520,8 @@ static __device__ __forceinline__ double strict_feasible0(double x, double lb, d
   return xn;
 }
 
-// ----------------------------------------------------------- control logic
-static __device__ __forceinline__ void st_trace(FitState* st, int lane, double cost_new, double ratio) {
-  if (st->trace_cap > 0 && st->trace_len < st->trace_cap) {
-    if (lane == 0) {
-      double* rec = st->trace + (int64_t)st->trace_len * TRACE_FIELDS;
-      rec[0] = st->nit;
-      rec[1] = st->nfev;
-      rec[2] = st->njev;
-      rec[3] = st->cost;
-      rec[4] = cost_new;
-      rec[5] = st->Delta_used;
-      rec[6] = st->alpha;
-      rec[7] = ratio;
-      rec[8] = st->hn;
-      rec[9] = st->step_norm;
-      rec[10] = st->pred;
-      rec[11] = st->bounded ? st->branch : -1;
-    }
-    __syncwarp();
-    if (lane == 0) st->trace_len = st->trace_len + 1;
-    __syncwarp();
-  }
-}
-
-// Unpack the K-vector into (cost, g, G) at the current iterate.
-static __device__ __forceinline__ void st_take_pass(FitState* st, const double* kv, int n, int lane) {
-  if (lane < n) {
-    st->g[lane] = kv[tri_slot(n, lane, n)];
-    for (int k = 0; k < n; ++k) {
-      const int a = lane < k ? lane : k, b = lane < k ? k : lane;
-      st->G[lane * NMAX + k] = kv[tri_slot(n, a, b)];
-    }
-  }
-  if (lane == 0) st->cost = 0.5 * kv[tri_slot(n, n, n)];
-  __syncwarp();
-}
-
-// scale_inv from the Gram diagonal (reading R3: column norms of J = sqrt(G_jj))
-static __device__ __forceinline__ void st_update_scale(FitState* st, int n, int lane, bool first) {
-  if (lane < n) {
-    double si = sqrt(st->G[lane * NMAX + lane]);
-    if (first) {
-      if (si == 0.0) si = 1.0;
-    } else {
-      si = fmax(si, st->scale_inv[lane]);
-    }
-    st->scale_inv[lane] = si;
-  }
-  __syncwarp();
-}
-
 // Coleman-Li vector v, dv (R19)
-static __device__ __forceinline__ void cl_vector(double x, double g, double lb, double ub, double& v, double& dv) {
+__device__ __forceinline__ void cl_vector(double x, double g, double lb, double ub, double& v, double& dv) {
   v = 1.0;
   dv = 0.0;
   if (g < 0.0 && isfinite(ub)) {
@@ -541,243 +534,247 @@ static __device__ __forceinline__ void cl_vector(double x, double g, double lb, 
   }
 }
 
-// Solve the subproblem for the current hat space and stage the trial point
-// in st->x_eval (Alg. 1 l.141-148 / Alg. 2 / select_step).  Then set the phase
-// of the next pass.
-static __device__ void st_make_trial(FitState* st, SolverSmem& S, int n, int lane) {
-  const bool act = lane < n;
-  // restore the hat space (S.V, S.M) from global state
-  for (int e = lane; e < n * n; e += 32) {
-    const int i = e / n, j = e % n;
-    S.V[i][j] = st->V[i * NMAX + j];
-    S.M[i][j] = st->Gh[i * NMAX + j];
+// ======================================================= the state machine
+// Everything below runs on lane 0 only (st and S are in shared memory).
+
+__device__ __forceinline__ void st_trace(FitState* st, double cost_new, double ratio) {
+  if (st->trace_cap > 0 && st->trace_len < st->trace_cap) {
+    double* rec = st->trace + (int64_t)st->trace_len * TRACE_FIELDS;
+    rec[0] = st->nit;
+    rec[1] = st->nfev;
+    rec[2] = st->njev;
+    rec[3] = st->cost;
+    rec[4] = cost_new;
+    rec[5] = st->Delta_used;
+    rec[6] = st->alpha;
+    rec[7] = ratio;
+    rec[8] = st->hn;
+    rec[9] = st->step_norm;
+    rec[10] = st->pred;
+    rec[11] = st->bounded ? st->branch : -1;
+    st->trace_len = st->trace_len + 1;
   }
-  __syncwarp();
-  const double lam = act ? st->lam[lane] : 0.0;
-  const double suf = act ? st->suf[lane] : 0.0;
+}
+
+// (cost, g, G) at the current iterate from a J-pass K-vector.
+template <int n>
+__device__ __forceinline__ void st_take_pass(FitState* st, const double* kv) {
+  for (int j = 0; j < n; ++j) {
+    st->g[j] = kv[tri_slot(n, j, n)];
+    for (int k = j; k < n; ++k) {
+      const double v = kv[tri_slot(n, j, k)];
+      st->G[j * NMAX + k] = v;
+      st->G[k * NMAX + j] = v;
+    }
+  }
+  st->cost = 0.5 * kv[tri_slot(n, n, n)];
+}
+
+// scale_inv from the Gram diagonal (reading R3: column norms of J = sqrt(G_jj))
+template <int n>
+__device__ __forceinline__ void st_update_scale(FitState* st, bool first) {
+  for (int j = 0; j < n; ++j) {
+    double si = sqrt(st->G[j * NMAX + j]);
+    if (first) {
+      if (si == 0.0) si = 1.0;
+    } else {
+      si = fmax(si, st->scale_inv[j]);
+    }
+    st->scale_inv[j] = si;
+  }
+}
+
+// Trial, part 1: the Gauss-Newton fast path; sets S.need_eig when Alg. 2 or
+// the exact rank test needs the eigendecomposition (computed by the warp).
+template <int n>
+__device__ __noinline__ void st_trial_begin(FitState* st, SolverSmem& S) {
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) S.M[i][j] = st->Gh[i * NMAX + j];
+  S.need_trial = 1;
+  S.fast = 0;
+  S.need_eig = 0;
+  if (!st->have_eig) {
+    const long long c0 = clock64();
+    S.fast = gn_fastpath<n>(S, st->m_global, st->gh, st->Delta, S.w3);
+    st->prof[1] += clock64() - c0;
+    if (!S.fast) S.need_eig = 1;
+  }
+}
+
+// Trial, part 2: Alg. 2 (if not fast), the Coleman-Li selection, the trial
+// point x_new staged in x_eval, and the phase of the next pass.
+template <int n>
+__device__ __noinline__ void st_trial_finish(FitState* st, SolverSmem& S) {
   const double Delta = st->Delta;
   double alpha = st->alpha;
-  double p_h;
-  const long long c0 = clock64();
-  warp_solve_tr(S, n, st->m_global, lam, suf, Delta, alpha, p_h, lane, nullptr);
-  if (lane == 0) st->prof[1] += clock64() - c0;
-  const double x = act ? st->x[lane] : 0.0;
-  const double d = act ? st->d[lane] : 0.0;
-  const double gh = act ? st->gh[lane] : 0.0;
-  double step, step_h, pred, x_new;
+  double* p_h = S.w3;
+  if (S.fast) {
+    alpha = 0.0;  // Alg. 1 l.142-144: p_k = p_t (SciPy returns alpha = 0)
+  } else {
+    if (S.need_eig) {  // the warp just computed it: keep it for retried trials
+      for (int j = 0; j < n; ++j) {
+        st->lam[j] = S.lam[j];
+        for (int i = 0; i < n; ++i) st->V[i * NMAX + j] = S.V[i][j];
+      }
+      for (int j = 0; j < n; ++j) {  // S^T U^T r = V^T g_hat (c.1b)
+        double t = 0.0;
+        for (int i = 0; i < n; ++i) t = fma(S.V[i][j], st->gh[i], t);
+        st->suf[j] = t;
+      }
+      st->have_eig = 1;
+      st->have_V = 1;
+    } else {
+      for (int j = 0; j < n; ++j) {
+        S.lam[j] = st->lam[j];
+        for (int i = 0; i < n; ++i) S.V[i][j] = st->V[i * NMAX + j];
+      }
+    }
+    const long long c0 = clock64();
+    solve_tr<n>(S, st->m_global, st->suf, Delta, alpha, p_h);
+    st->prof[2] += clock64() - c0;
+  }
+  double pred;
   int branch = -1;
   if (st->bounded) {
-    const double lb = act ? st->lb[lane] : 0.0, ub = act ? st->ub[lane] : 0.0;
-    const long long c1 = clock64();
-    w_select_step(S, n, lane, x, lb, ub, gh, d, p_h, Delta, st->theta, step, step_h, pred, branch);
-    if (lane == 0) st->prof[2] += clock64() - c1;
-    x_new = act ? strict_feasible0(x + step, lb, ub) : 0.0;
+    select_step<n>(S, st->x, st->lb, st->ub, st->gh, st->d, p_h, Delta, st->theta, st->step, st->step_h, pred, branch);
+    for (int j = 0; j < n; ++j) st->x_eval[j] = strict_feasible0(st->x[j] + st->step[j], st->lb[j], st->ub[j]);
   } else {
-    step_h = p_h;
-    pred = -w_eval_quad(S, gh, step_h, n, lane);  // Eq. 15 denominator (R13)
-    step = d * step_h;                            // Alg. 3 l.185: w = D^-1 p
-    x_new = x + step;
+    for (int j = 0; j < n; ++j) st->step_h[j] = p_h[j];
+    pred = -eval_quad<n>(S, st->gh, p_h);  // Eq. 15 denominator (R13)
+    for (int j = 0; j < n; ++j) {
+      st->step[j] = st->d[j] * p_h[j];  // Alg. 3 l.185: w = D^-1 p
+      st->x_eval[j] = st->x[j] + st->step[j];
+    }
   }
-  const double hn = wnorm(act ? step_h : 0.0);
-  const double sn = wnorm(act ? step : 0.0);
-  if (act) {
-    st->x_eval[lane] = x_new;
-    st->step[lane] = step;
-    st->step_h[lane] = step_h;
-  }
-  if (lane == 0) {
-    st->alpha = alpha;
-    st->pred = pred;
-    st->hn = hn;
-    st->step_norm = sn;
-    st->Delta_used = Delta;
-    st->branch = branch;
-    st->phase = (st->policy == 1) ? PH_TRIAL_R : PH_TRIAL_J;
-  }
-  __syncwarp();
+  st->alpha = alpha;
+  st->pred = pred;
+  st->hn = vnorm<n>(st->step_h);
+  st->step_norm = vnorm<n>(st->step);
+  st->Delta_used = Delta;
+  st->branch = branch;
+  st->phase = (st->policy == 1) ? PH_TRIAL_R : PH_TRIAL_J;
+  S.need_trial = 0;
 }
 
 // Alg. 1 loop top: termination by gtol / max_nfev, then the hat space of the
-// new iterate (Eq. 7-8, App. B) and the first trial.
-static __device__ void st_outer_top(FitState* st, SolverSmem& S, int n, int lane) {
-  const bool act = lane < n;
-  const double x = act ? st->x[lane] : 0.0;
-  const double g = act ? st->g[lane] : 0.0;
-  const double lb = act ? st->lb[lane] : 0.0, ub = act ? st->ub[lane] : 0.0;
-  double v = 1.0, dv = 0.0;
-  double gnorm;
-  if (st->bounded) {
-    if (act) cl_vector(x, g, lb, ub, v, dv);
-    gnorm = wmax(act ? fabs(g * v) : 0.0);
-  } else {
-    gnorm = wmax(act ? fabs(g) : 0.0);
+// new iterate (Eq. 7-8).  Requests a trial unless the fit is over.
+template <int n>
+__device__ __noinline__ void st_outer_top(FitState* st, SolverSmem& S) {
+  double gnorm = 0.0;
+  double v[NMAX], dv[NMAX];
+  for (int j = 0; j < n; ++j) {
+    v[j] = 1.0;
+    dv[j] = 0.0;
+    if (st->bounded) cl_vector(st->x[j], st->g[j], st->lb[j], st->ub[j], v[j], dv[j]);
+    gnorm = fmax(gnorm, fabs(st->g[j] * v[j]));
   }
-  int status = st->status;
-  if (gnorm < st->gtol) status = 1;  // R16
-  if (lane == 0) {
-    st->gnorm = gnorm;
-    st->status = status;
-  }
-  __syncwarp();
-  if (status != STATUS_NONE || st->nfev == st->max_nfev) {
-    if (lane == 0) {
-      if (status == STATUS_NONE) st->status = 0;
-      st->phase = PH_DONE;
-      st->cont = 0;
-    }
-    __syncwarp();
+  if (gnorm < st->gtol) st->status = 1;  // R16
+  st->gnorm = gnorm;
+  if (st->status != STATUS_NONE || st->nfev == st->max_nfev) {
+    if (st->status == STATUS_NONE) st->status = 0;
+    st->phase = PH_DONE;
+    st->cont = 0;
     return;
   }
-  const double si = act ? st->scale_inv[lane] : 1.0;
-  double d, diag_h = 0.0;
-  if (st->bounded) {
-    if (dv != 0.0) v *= si;
-    d = sqrt(v) / si;          // R19: d = v^0.5 * scale
-    diag_h = g * dv / si;      // C = diag(g * scale) Jv
-  } else {
-    d = 1.0 / si;              // Eq. 8: J_hat = J D^-1
+  for (int j = 0; j < n; ++j) {
+    const double si = st->scale_inv[j];
+    if (st->bounded) {
+      double vj = v[j];
+      if (dv[j] != 0.0) vj *= si;
+      st->d[j] = sqrt(vj) / si;              // R19: d = v^0.5 * scale
+      st->diag_h[j] = st->g[j] * dv[j] / si;  // C = diag(g * scale) Jv
+    } else {
+      st->d[j] = 1.0 / si;  // Eq. 8: J_hat = J D^-1
+      st->diag_h[j] = 0.0;
+    }
+    st->gh[j] = st->d[j] * st->g[j];
   }
-  if (!act) {
-    d = 0.0;
-    diag_h = 0.0;
-  }
-  const double gh = d * g;
-  if (act) {
-    st->d[lane] = d;
-    st->diag_h[lane] = diag_h;
-    st->gh[lane] = gh;
-  }
-  __syncwarp();
-  // B_hat = d G d (+ diag_h): the scaled Gram (Eq. 8), eigensolver input S.A
-  // and quadratic-form matrix S.M
-  for (int e = lane; e < n * n; e += 32) {
-    const int i = e / n, j = e % n;
-    double b = st->d[i] * st->G[i * NMAX + j] * st->d[j];
-    if (i == j) b += st->diag_h[i];
-    S.A[i][j] = b;
-    S.M[i][j] = b;
-    st->Gh[i * NMAX + j] = b;
-  }
-  const int warm = st->have_V;
-  if (warm) {
-    for (int e = lane; e < NMAX * NMAX; e += 32) {
-      const int i = e / NMAX, j = e % NMAX;
-      S.V[i][j] = (i < n && j < n) ? st->V[i * NMAX + j] : 0.0;
+  for (int i = 0; i < n; ++i) {  // B_hat = d G d (+ diag_h)
+    for (int j = 0; j < n; ++j) {
+      double b = st->d[i] * st->G[i * NMAX + j] * st->d[j];
+      if (i == j) b += st->diag_h[i];
+      st->Gh[i * NMAX + j] = b;
     }
   }
-  __syncwarp();
-  double lam;
-  const long long c0 = clock64();
-  warp_eig(S, n, lane, lam, warm);
-  if (lane == 0) st->prof[0] += clock64() - c0;
-  const double suf = wVtx(S.V, gh, n, lane);  // S^T U^T r = V^T g_hat (c.1b)
-  if (act) {
-    st->lam[lane] = lam;
-    st->suf[lane] = suf;
-  }
-  for (int e = lane; e < n * n; e += 32) {
-    const int i = e / n, j = e % n;
-    st->V[i * NMAX + j] = S.V[i][j];
-  }
-  if (lane == 0) {
-    st->theta = fmax(0.995, 1.0 - gnorm);
-    st->actual = -1.0;
-    st->have_V = 1;
-  }
-  __syncwarp();
-  st_make_trial(st, S, n, lane);
+  st->theta = fmax(0.995, 1.0 - gnorm);
+  st->actual = -1.0;
+  st->have_eig = 0;
+  st_trial_begin<n>(st, S);
 }
 
 // Initialisation after the J-pass at x0 (Alg. 1 l.137-138; R3, R4, R18).
-static __device__ void st_init(FitState* st, SolverSmem& S, const double* kv, int n, int lane) {
-  const bool act = lane < n;
+template <int n>
+__device__ __noinline__ void st_init(FitState* st, SolverSmem& S, const double* kv) {
   if (kv[tri_count(n)] != 0.0) {  // R18: residuals at x0 must be finite
-    if (lane == 0) {
-      st->error = -3;
-      st->status = -3;
-      st->phase = PH_DONE;
-      st->cont = 0;
-    }
-    __syncwarp();
+    st->error = -3;
+    st->status = -3;
+    st->phase = PH_DONE;
+    st->cont = 0;
     return;
   }
-  st_take_pass(st, kv, n, lane);
-  if (lane == 0) {
-    st->nfev = 1;
-    st->njev = 1;
-    st->nit = 0;
-    st->alpha = 0.0;
-    st->status = STATUS_NONE;
-  }
+  st_take_pass<n>(st, kv);
+  st->nfev = 1;
+  st->njev = 1;
+  st->nit = 0;
+  st->alpha = 0.0;
+  st->status = STATUS_NONE;
   if (st->jacmode) {
-    st_update_scale(st, n, lane, true);
-  } else if (act) {
-    st->scale_inv[lane] = st->xs_inv[lane];
-  }
-  __syncwarp();
-  const double x = act ? st->x[lane] : 0.0;
-  const double si = act ? st->scale_inv[lane] : 0.0;
-  double Delta;
-  if (st->bounded) {  // R4
-    double v = 1.0, dv = 0.0;
-    if (act) cl_vector(x, st->g[lane], st->lb[lane], st->ub[lane], v, dv);
-    if (dv != 0.0) v *= si;
-    Delta = wnorm(act ? x * si / sqrt(v) : 0.0);
+    st_update_scale<n>(st, true);
   } else {
-    Delta = wnorm(act ? x * si : 0.0);
+    for (int j = 0; j < n; ++j) st->scale_inv[j] = st->xs_inv[j];
   }
+  double s2 = 0.0;  // R4: Delta0 = ||x0 * scale_inv (/ sqrt(v))||
+  for (int j = 0; j < n; ++j) {
+    double t = st->x[j] * st->scale_inv[j];
+    if (st->bounded) {
+      double v, dv;
+      cl_vector(st->x[j], st->g[j], st->lb[j], st->ub[j], v, dv);
+      if (dv != 0.0) v *= st->scale_inv[j];
+      t /= sqrt(v);
+    }
+    s2 = fma(t, t, s2);
+  }
+  double Delta = sqrt(s2);
   if (Delta == 0.0) Delta = 1.0;
-  if (lane == 0) st->Delta = Delta;
-  __syncwarp();
-  st_outer_top(st, S, n, lane);
+  st->Delta = Delta;
+  st_outer_top<n>(st, S);
 }
 
-// End of the inner (retry) loop: accept or keep x, count the iteration.
-// For the conservative policy an accepted step first needs the J-pass at x_new.
-static __device__ void st_end_inner(FitState* st, SolverSmem& S, int n, int lane, bool have_jac) {
-  const bool act = lane < n;
+// End of the inner (retry) loop: accept or keep x, count the iteration.  For
+// the conservative policy an accepted step first needs the J-pass at x_new.
+template <int n>
+__device__ __noinline__ void st_end_inner(FitState* st, SolverSmem& S, bool have_jac) {
   if (st->actual > 0.0) {
+    for (int j = 0; j < n; ++j) st->x[j] = st->x_eval[j];
     if (!have_jac) {  // conservative: J at the new x (counts as njev there)
-      if (act) st->x[lane] = st->x_eval[lane];
-      if (lane == 0) {
-        st->cost = st->cost_new;
-        st->phase = PH_ACCEPT_J;
-      }
-      __syncwarp();
+      st->cost = st->cost_new;
+      st->phase = PH_ACCEPT_J;
       return;
     }
-    if (act) st->x[lane] = st->x_eval[lane];
-    __syncwarp();
-    st_take_pass(st, st->kv, n, lane);
-    if (lane == 0) {
-      st->cost = st->cost_new;  // SciPy keeps the trial's cost
-      st->njev = st->njev + 1;
-    }
-    __syncwarp();
-    if (st->jacmode) st_update_scale(st, n, lane, false);
+    st_take_pass<n>(st, st->kv);
+    st->cost = st->cost_new;  // SciPy keeps the trial's cost
+    st->njev = st->njev + 1;
+    if (st->jacmode) st_update_scale<n>(st, false);
   }
-  if (lane == 0) st->nit = st->nit + 1;  // R27
-  __syncwarp();
-  st_outer_top(st, S, n, lane);
+  st->nit = st->nit + 1;  // R27
+  st_outer_top<n>(st, S);
 }
 
 // After a trial pass at x_eval (speculative J-pass or conservative r-pass).
-static __device__ void st_after_trial(FitState* st, SolverSmem& S, const double* kv, int n, int lane, bool jac) {
+template <int n>
+__device__ __noinline__ void st_after_trial(FitState* st, SolverSmem& S, const double* kv, bool jac) {
   const double rr = jac ? kv[tri_slot(n, n, n)] : kv[0];
   const double bad = jac ? kv[tri_count(n)] : kv[1];
-  if (lane == 0) st->nfev = st->nfev + 1;
-  __syncwarp();
+  st->nfev = st->nfev + 1;
   if (bad != 0.0) {  // R17: shrink and retry, no termination test
-    if (lane == 0) st->Delta = 0.25 * st->hn;
-    __syncwarp();
-    st_trace(st, lane, NAN, NAN);
+    st->Delta = 0.25 * st->hn;
+    st_trace(st, NAN, NAN);
     if (st->nfev < st->max_nfev) {
-      st_make_trial(st, S, n, lane);
+      st_trial_begin<n>(st, S);
       return;
     }
-    if (lane == 0) st->actual = -1.0;
-    __syncwarp();
-    st_end_inner(st, S, n, lane, jac);
+    st->actual = -1.0;
+    st_end_inner<n>(st, S, jac);
     return;
   }
   const double cost_new = 0.5 * rr;
@@ -790,68 +787,99 @@ static __device__ void st_after_trial(FitState* st, SolverSmem& S, const double*
   double Delta_new = st->Delta;  // Alg. 3 with SciPy's rules (R15)
   if (ratio < 0.25) Delta_new = 0.25 * st->hn;
   else if (ratio > 0.75 && st->hn > 0.95 * st->Delta) Delta_new = 2.0 * st->Delta;
-  // termination (R16), x_norm of the pre-step x
-  const bool act = lane < n;
-  const double xnorm = wnorm(act ? st->x[lane] : 0.0);
+  const double xnorm = vnorm<n>(st->x);  // termination (R16), pre-step x
   const bool ft = actual < st->ftol * st->cost && ratio > 0.25;
   const bool xt = st->step_norm < st->xtol * (st->xtol + xnorm);
   const int status = (ft && xt) ? 4 : (ft ? 2 : (xt ? 3 : STATUS_NONE));
-  if (lane == 0) {
-    st->cost_new = cost_new;
-    st->actual = actual;
-    st->ratio = ratio;
-  }
-  __syncwarp();
-  st_trace(st, lane, cost_new, ratio);
+  st->cost_new = cost_new;
+  st->actual = actual;
+  st->ratio = ratio;
+  st_trace(st, cost_new, ratio);
   if (status != STATUS_NONE) {
-    if (lane == 0) st->status = status;
-    __syncwarp();
-    st_end_inner(st, S, n, lane, jac);
+    st->status = status;
+    st_end_inner<n>(st, S, jac);
     return;
   }
-  if (lane == 0) {
-    st->alpha = st->alpha * (st->Delta / Delta_new);  // R5
-    st->Delta = Delta_new;
-  }
-  __syncwarp();
+  st->alpha = st->alpha * (st->Delta / Delta_new);  // R5
+  st->Delta = Delta_new;
   if (actual <= 0.0 && st->nfev < st->max_nfev) {
-    st_make_trial(st, S, n, lane);  // R15: same hat space, new radius
+    st_trial_begin<n>(st, S);  // R15: same hat space, new radius
     return;
   }
-  st_end_inner(st, S, n, lane, jac);
+  st_end_inner<n>(st, S, jac);
 }
 
-// Entry point: called by warp 0 of the last block of every pass kernel in a
-// fit, with the combined K-vector of the pass that just finished.
-static __device__ __noinline__ void fit_after_pass(FitState* st, SolverSmem& S, const double* kv, bool jac) {
-  const int lane = threadIdx.x & 31;
-  const long long cstart = clock64();
-  const int n = st->n;
+// Lane 0: advance the state machine with the K-vector of the pass that just
+// finished.  A requested trial is left half done (S.need_trial) for
+// solver_step: warp eigensolver if S.need_eig, then st_trial_finish.
+template <int n>
+__device__ __noinline__ void fit_after_pass(FitState* st, SolverSmem& S, const double* kv, bool jac) {
   const int KS = jac ? tri_count(n) + 1 : 2;
-  for (int k = lane; k < KS; k += 32) st->kv[k] = kv[k];
-  if (lane == 0) st->launches = st->launches + 1;
-  __syncwarp();
+  for (int k = 0; k < KS; ++k) st->kv[k] = kv[k];
+  st->launches = st->launches + 1;
+  S.need_trial = 0;
+  S.need_eig = 0;
   const int phase = st->phase;
   if (phase == PH_INIT_J) {
-    st_init(st, S, kv, n, lane);
+    st_init<n>(st, S, st->kv);
   } else if (phase == PH_TRIAL_J && jac) {
-    st_after_trial(st, S, kv, n, lane, true);
+    st_after_trial<n>(st, S, st->kv, true);
   } else if (phase == PH_TRIAL_R && !jac) {
-    st_after_trial(st, S, kv, n, lane, false);
+    st_after_trial<n>(st, S, st->kv, false);
   } else if (phase == PH_ACCEPT_J && jac) {
-    st_take_pass(st, kv, n, lane);  // g, G at the accepted x (cost kept: SciPy)
-    if (lane == 0) {
-      st->cost = st->cost_new;
-      st->njev = st->njev + 1;
+    st_take_pass<n>(st, st->kv);  // g, G at the accepted x (cost kept: SciPy)
+    st->cost = st->cost_new;
+    st->njev = st->njev + 1;
+    if (st->jacmode) st_update_scale<n>(st, false);
+    st->nit = st->nit + 1;
+    st_outer_top<n>(st, S);
+  }
+}
+
+// Whole warp: one solver step after a pass (state machine on lane 0, the
+// eigensolver on all lanes when a trial needs it).
+__device__ __forceinline__ void solver_step(FitState* st, SolverSmem& S, const double* kv, bool jac) {
+  const int lane = threadIdx.x & 31;
+  const long long c0 = clock64();
+  const int nn = st->n;
+  // n is a template constant in each instance (the built-in models' n): the
+  // n-loops unroll and the small vectors live in registers
+  if (lane == 0) {
+    switch (nn) {
+      case 2: fit_after_pass<2>(st, S, kv, jac); break;
+      case 3: fit_after_pass<3>(st, S, kv, jac); break;
+      case 4: fit_after_pass<4>(st, S, kv, jac); break;
+      case 7: fit_after_pass<7>(st, S, kv, jac); break;
+      case 13: fit_after_pass<13>(st, S, kv, jac); break;
+      default: break;
     }
-    __syncwarp();
-    if (st->jacmode) st_update_scale(st, n, lane, false);
-    if (lane == 0) st->nit = st->nit + 1;
-    __syncwarp();
-    st_outer_top(st, S, n, lane);
   }
   __syncwarp();
-  if (lane == 0) st->prof[3] += clock64() - cstart;
+  if (S.need_trial && S.need_eig) {
+    const int n = st->n;
+    const int warm = st->have_V;
+    for (int e = lane; e < n * n; e += 32) {
+      const int i = e / n, j = e % n;
+      S.A[i][j] = S.M[i][j];
+      if (warm) S.V[i][j] = st->V[i * NMAX + j];
+    }
+    __syncwarp();
+    const long long c1 = clock64();
+    warp_eig(S, n, warm);
+    if (lane == 0) st->prof[0] += clock64() - c1;
+  }
+  __syncwarp();
+  if (lane == 0 && S.need_trial) {
+    switch (nn) {
+      case 2: st_trial_finish<2>(st, S); break;
+      case 3: st_trial_finish<3>(st, S); break;
+      case 4: st_trial_finish<4>(st, S); break;
+      case 7: st_trial_finish<7>(st, S); break;
+      case 13: st_trial_finish<13>(st, S); break;
+      default: break;
+    }
+  }
+  if (lane == 0) st->prof[3] += clock64() - c0;
   __syncwarp();
 }
 

@@ -1,0 +1,48 @@
+// jf_state.cuh — the device-resident state of one fit and
+// the phases of the pass / solver alternation.  Shared by the pass kernels
+// (which read the phase and the point to evaluate) and the solver kernel.
+#pragma once
+
+#include "jf_common.cuh"
+
+namespace jf {
+
+enum Phase : int32_t {
+  PH_INIT_J = 0,    // J-pass at x0
+  PH_TRIAL_J = 1,   // speculative policy: J-pass at a trial point
+  PH_TRIAL_R = 2,   // conservative policy: residual pass at a trial point
+  PH_ACCEPT_J = 3,  // conservative policy: J-pass at the accepted point
+  PH_DONE = 4
+};
+
+constexpr int TRACE_FIELDS = 12;
+constexpr int STATUS_NONE = -100;
+
+struct FitState {
+  // ---- configuration (written by the host before the first launch)
+  int32_t n, bounded, jacmode, max_nfev;
+  int32_t policy, trace_cap, pad0, pad1;
+  int64_t m_global;
+  double ftol, xtol, gtol;
+  double lb[NMAX], ub[NMAX], xs_inv[NMAX];
+  double* trace;
+  // ---- iteration state
+  int32_t phase, status, nfev, njev, nit, cont, error, trace_len;
+  int32_t full_rank, branch, launches, have_V;
+  int32_t pass_ready;  // set by a pass kernel's last block: 1 J-pass, 2 r-pass result in kv_in
+  int32_t have_eig;    // eigendecomposition of the current B_hat computed (lazy, per iteration)
+  unsigned long long comm_epoch;
+  unsigned long long epi_ns;  // device time spent in the solver epilogue (globaltimer)
+  long long prof[8];          // SM cycles: eig, trial solve, select_step, fit_after_pass, after_trial,
+                              // accept (take_pass + scale), outer_top (pre-trial), trial finish
+  double cost, cost_new, Delta, alpha, gnorm, theta, actual;
+  double pred, hn, step_norm, Delta_used, ratio, pad4;
+  double x[NMAX], x_eval[NMAX];
+  double g[NMAX], G[NMAX * NMAX], scale_inv[NMAX];
+  // hat space of the current iterate (reused by rejected trials, R15)
+  double d[NMAX], diag_h[NMAX], gh[NMAX], Gh[NMAX * NMAX], lam[NMAX], V[NMAX * NMAX], suf[NMAX];
+  double step[NMAX], step_h[NMAX];
+  double kv[KMAX];  // K-vector of the last pass
+};
+
+}  // namespace jf
