@@ -175,6 +175,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="host-driven loop instead of the CUDA graph (ncu cannot see kernels inside conditional graph nodes)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -209,7 +211,7 @@ def main():
     comm = None
     if world > 1:
         comm = jf.Comm.from_process_group(rank, world, local, dist)
-    kw = dict(grid=grid, p0=pr_full.p0, stream=stream.cuda_stream)
+    kw = dict(grid=grid, p0=pr_full.p0, stream=stream.cuda_stream, use_graph=not args.no_graph)
     if comm is not None:
         kw.update(comm=comm, m_global=m_total)
 
@@ -307,7 +309,8 @@ def main():
                                    + (f", {W_IMG}-row band per rank" if world > 1 else ""),
                        "m": m_total, "passes_per_fit": passes / args.steps, "nfev": res.nfev, "njev": res.njev,
                        "status": res.status, "cost": res.cost, "l2": "flushed (256 MB write) between steps",
-                       "policy": "speculative", "driver": "CUDA graph, conditional WHILE node",
+                       "policy": "speculative",
+                       "driver": "host loop" if args.no_graph else "CUDA graph, conditional WHILE node",
                        "parallelism": f"dp{world}"},
             "roofline": roofline,
             "e2e": e2e,

@@ -152,6 +152,9 @@ typedef struct jf_result {
   double t_epilogue_s;          /* device time in the single-warp solver epilogues (globaltimer) */
   double epilogue_cycles[8];    /* SM cycles in: eigensolver, trial solve, Coleman-Li step
                                    selection, whole solver step (diagnostics)                    */
+  int32_t timeline_len, pad2_;
+  double timeline_ns[64];       /* device timeline of the fit (ns from the first event): pass
+                                   kernel start, pass end (last block), solver start, solver end */
 } jf_result;
 
 /* Fill *opts with the defaults above.  opts must be non-NULL. */

@@ -52,6 +52,7 @@ class jf_result(C.Structure):
         ("kernel_launches", C.c_int32), ("pad_", C.c_int32),
         ("t_upload_s", C.c_double), ("t_solve_s", C.c_double),
         ("t_epilogue_s", C.c_double), ("epilogue_cycles", C.c_double * 8),
+        ("timeline_len", C.c_int32), ("pad2_", C.c_int32), ("timeline_ns", C.c_double * 64),
     ]
 
 

@@ -125,6 +125,7 @@ class FitResult:
     t_solve_s: float
     t_epilogue_s: float
     epilogue_cycles: tuple = ()
+    timeline_ns: tuple = ()
     trace: np.ndarray = field(default_factory=lambda: np.zeros((0, L.JF_TRACE_FIELDS)))
 
 
@@ -154,7 +155,8 @@ def curve_fit(model, z, y=None, *, grid=None, p0=None, lb=None, ub=None, sigma=N
         gram=np.array(res.gram[: n * n]).reshape(n, n), status=res.status, nfev=res.nfev, njev=res.njev,
         nit=res.nit, active_mask=np.array(res.active_mask[:n], dtype=np.int64),
         kernel_launches=res.kernel_launches, t_upload_s=res.t_upload_s, t_solve_s=res.t_solve_s,
-        t_epilogue_s=res.t_epilogue_s, epilogue_cycles=tuple(res.epilogue_cycles))
+        t_epilogue_s=res.t_epilogue_s, epilogue_cycles=tuple(res.epilogue_cycles),
+        timeline_ns=tuple(res.timeline_ns[:res.timeline_len]))
     if tr is not None:
         out.trace = tr[: res.trace_len].copy()
     return out

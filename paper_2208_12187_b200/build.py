@@ -76,7 +76,8 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
                 log = f.result()
                 if verbose and log:
                     sys.stderr.write(f"== {os.path.basename(futs[f])}\n{log}")
-    if todo or not os.path.exists(LIB):
+    stale_lib = (not os.path.exists(LIB)) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs)
+    if todo or stale_lib:
         cmd = [nvcc(), *ARCH, "-shared", "-o", LIB + ".tmp", *objs]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

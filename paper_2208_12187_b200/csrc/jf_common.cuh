@@ -58,7 +58,7 @@ struct PassArgs {
   double* out;          // combined K-vector (EPI_NONE)
   int* err;             // EPI_NONE: set to JF_ECOMM (-5) if the cross-rank combine failed
   int32_t use_comm;     // 1: combine across ranks through the mailboxes
-  int32_t pad_;
+  int32_t fuse_solver;  // reserved (0): the solver step runs in its own kernel (jf_solver.cu)
   CommDev comm;
 };
 

@@ -389,11 +389,31 @@ int build_graph(Ctx& c, const PassPair& k, int policy, cudaGraphExec_t* out) {
   sp.kernelParams = sargs;
   // body: [r-pass -> solver ->] J-pass -> solver; each pass kernel runs only
   // when the state's phase asks for it, each solver only after a pass ran
+  // solver nodes depend programmatically on the pass before them (PDL): the
+  // solver kernel is scheduled while the pass drains and waits in
+  // griddepcontrol.wait for its results, hiding the launch latency
   cudaGraphNode_t prev = nullptr;
-  auto add = [&](const cudaKernelNodeParams& p) -> int {
+  bool prev_is_pass = false;
+  auto add = [&](const cudaKernelNodeParams& p, bool is_solver) -> int {
     cudaGraphNode_t nd;
-    CK(cudaGraphAddKernelNode(&nd, body, prev ? &prev : nullptr, prev ? 1 : 0, &p));
+    if (prev && is_solver && prev_is_pass) {
+      cudaGraphNodeParams np = {};
+      np.type = cudaGraphNodeTypeKernel;
+      np.kernel.func = p.func;
+      np.kernel.gridDim = p.gridDim;
+      np.kernel.blockDim = p.blockDim;
+      np.kernel.sharedMemBytes = p.sharedMemBytes;
+      np.kernel.kernelParams = p.kernelParams;
+      cudaGraphEdgeData ed = {};
+      ed.from_port = cudaGraphKernelNodePortProgrammatic;
+      ed.to_port = cudaGraphKernelNodePortDefault;
+      ed.type = cudaGraphDependencyTypeProgrammatic;
+      CK(cudaGraphAddNode_v2(&nd, body, &prev, &ed, 1, &np));
+    } else {
+      CK(cudaGraphAddKernelNode(&nd, body, prev ? &prev : nullptr, prev ? 1 : 0, &p));
+    }
     prev = nd;
+    prev_is_pass = !is_solver;
     return 0;
   };
   kp.kernelParams = pargs;
@@ -401,14 +421,14 @@ int build_graph(Ctx& c, const PassPair& k, int policy, cudaGraphExec_t* out) {
     kp.func = (void*)k.r;
     kp.gridDim = dim3(k.rgrid);
     kp.blockDim = dim3(k.rtpb);
-    if (int e = add(kp)) return e;
-    if (int e = add(sp)) return e;
+    if (int e = add(kp, false)) return e;
+    if (int e = add(sp, true)) return e;
   }
   kp.func = (void*)k.j;
   kp.gridDim = dim3(k.jgrid);
   kp.blockDim = dim3(k.jtpb);
-  if (int e = add(kp)) return e;
-  if (int e = add(sp)) return e;
+  if (int e = add(kp, false)) return e;
+  if (int e = add(sp, true)) return e;
   CK(cudaGraphInstantiate(out, g, 0));
   cudaGraphDestroy(g);
   return 0;
@@ -640,6 +660,7 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
   PassArgs a;
   fill_args(a, sg, m, o);
   a.epilogue = EPI_FIT;
+  a.fuse_solver = 0;
   a.partials = c->d_partials;
   a.ticket = c->d_ticket;
   a.out = c->d_out;
@@ -678,13 +699,15 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
     }
   }
   out->t_solve_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-  launches = h.launches;
+  launches = h.kernels;
   if (o.comm) o.comm->epoch = h.comm_epoch;
 
   // ---- result
   out->kernel_launches = launches;
   out->t_epilogue_s = h.epi_ns * 1e-9;
   for (int q = 0; q < 8; ++q) out->epilogue_cycles[q] = (double)h.prof[q];
+  out->timeline_len = h.tl_n < 64 ? h.tl_n : 64;
+  for (int q = 0; q < out->timeline_len; ++q) out->timeline_ns[q] = (double)(h.tl[q] - h.tl[0]);
   out->nfev = h.nfev;
   out->njev = h.njev;
   out->nit = h.nit;

@@ -255,8 +255,8 @@ __device__ __forceinline__ void grid_recur_loop(const PassArgs& a, const auto& p
 #pragma unroll
       for (int k = 0; k < L; ++k) {
         const bool v = col + 32 * k < W;
-        zn[k] = v ? __ldg(zp + 32 * k) : 0.0;
-        if constexpr (WGT) wn[k] = v ? __ldg(ws + row * a.W + col + 32 * k) : 0.0;
+        zn[k] = v ? __ldcs(zp + 32 * k) : 0.0;
+        if constexpr (WGT) wn[k] = v ? __ldcs(ws + row * a.W + col + 32 * k) : 0.0;
       }
     }
   };
@@ -302,7 +302,7 @@ __device__ __forceinline__ void grid_recur_loop(const PassArgs& a, const auto& p
       }
     } else {
       // ragged row end or unsafe exponent range: direct evaluation
-#pragma unroll 1
+#pragma unroll
       for (int k = 0; k < L; ++k) {
         if (col0 + 32 * k < W) {
           const double X = X0 + 32.0 * k;
@@ -322,7 +322,7 @@ struct PassCfg {
   static constexpr int P = JAC ? (Model::N == 7 ? 4 : 1) : (Model::N > 7 ? 2 : 4);
   static constexpr int TPB = 256;
   static constexpr int MINB = BIG ? 1 : 2;
-  static constexpr int L = (JAC && Model::N > 7) ? 2 : 8;  // points per lane per warp-chunk (grid recurrence)
+  static constexpr int L = JAC ? (Model::N > 7 ? 2 : 8) : 16;  // points per lane per warp-chunk (grid recurrence)
 };
 
 // The pass kernel.  epilogue == EPI_FIT: one pass of a fit (st is the state).
@@ -331,12 +331,24 @@ template <class Model, bool JAC, int COORD, bool WGT, int P = PassCfg<Model, JAC
 __global__ void __launch_bounds__(TPB, MINB)
     pass_kernel(const PassArgs* __restrict__ pa, FitState* __restrict__ st, cudaGraphConditionalHandle cond,
                 int use_cond) {
+  (void)cond;
+  (void)use_cond;
   using Sh = PassShape<Model, JAC>;
   constexpr int KT = Sh::KT, KS = Sh::KS;
   const PassArgs& a = *pa;
 
   // Phase predication inside a fit: run only when this pass type is wanted.
   if (a.epilogue == EPI_FIT) {
+    // the solver kernel after this pass may be scheduled now (PDL); it waits
+    // for this grid's completion in griddepcontrol.wait
+    asm volatile("griddepcontrol.launch_dependents;");
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      atomicAdd(&st->kernels, 1);
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      const int k = atomicAdd(&st->tl_n, 1);
+      if (k < 64) st->tl[k] = t;
+    }
     const int ph = st->phase;
     const bool want = JAC ? (ph == PH_INIT_J || ph == PH_TRIAL_J || ph == PH_ACCEPT_J) : (ph == PH_TRIAL_R);
     if (!want) return;
@@ -373,11 +385,11 @@ __global__ void __launch_bounds__(TPB, MINB)
     for (int p = 0; p < P; ++p) {
       const int64_t idx = base + p * S;
       const bool v = idx < m;
-      qz[p] = v ? __ldg(z + idx) : 0.0;
-      qw[p] = (v && weighted) ? __ldg(ws + idx) : 1.0;
+      qz[p] = v ? __ldcs(z + idx) : 0.0;
+      qw[p] = (v && weighted) ? __ldcs(ws + idx) : 1.0;
       if constexpr (EXPL) {
-        qa[p] = v ? __ldg(y0 + idx) : 0.0;
-        if constexpr (TWO) qb[p] = v ? __ldg(y1 + idx) : 0.0;
+        qa[p] = v ? __ldcs(y0 + idx) : 0.0;
+        if constexpr (TWO) qb[p] = v ? __ldcs(y1 + idx) : 0.0;
       }
     }
   };
@@ -478,13 +490,18 @@ __global__ void __launch_bounds__(TPB, MINB)
     for (int k = threadIdx.x; k < KS; k += TPB) a.out[k] = vec[k];
     return;
   }
-  (void)cond;
-  (void)use_cond;
+
   // ---- fit: hand the combined K-vector to the solver kernel (jf_solver.cu)
   for (int k = threadIdx.x; k < KS; k += TPB) a.out[k] = vec[k];
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) st->pass_ready = JAC ? 1 : 2;
+  if (threadIdx.x == 0) {
+    st->pass_ready = JAC ? 1 : 2;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const int k = atomicAdd(&st->tl_n, 1);
+    if (k < 64) st->tl[k] = t;
+  }
 }
 
 }  // namespace jf

@@ -18,58 +18,16 @@ __global__ void __launch_bounds__(32, 1)
   __shared__ SolverSmem S;
   __shared__ FitState sst;
   const int lane = threadIdx.x;
-  int cont;
+  (void)lane;
+  // PDL: wait for the pass kernel before us (a no-op for a plain launch)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (lane == 0) atomicAdd(&st->kernels, 1);
+  __syncwarp();
   if (st->pass_ready != 0) {
-    unsigned long long t0, t1;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    // state and the pass's K-vector into shared memory: all loads issued
-    // before any is consumed (one memory latency, not one per element)
-    constexpr int NW = sizeof(FitState) / 8;
-    constexpr int PER = (NW + 31) / 32;
-    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(st);
-    unsigned long long* dst = reinterpret_cast<unsigned long long*>(&sst);
-    unsigned long long buf[PER];
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const int k = lane + 32 * q;
-      buf[q] = (k < NW) ? __ldcg(src + k) : 0ull;
-    }
-    double kvb[(KMAX + 31) / 32];
-#pragma unroll
-    for (int q = 0; q < (KMAX + 31) / 32; ++q) {
-      const int k = lane + 32 * q;
-      kvb[q] = (k < KMAX) ? __ldcg(kv + k) : 0.0;
-    }
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const int k = lane + 32 * q;
-      if (k < NW) dst[k] = buf[q];
-    }
-#pragma unroll
-    for (int q = 0; q < (KMAX + 31) / 32; ++q) {
-      const int k = lane + 32 * q;
-      if (k < KMAX) S.kvs[k] = kvb[q];
-    }
-    __syncwarp();
-    const bool jac = sst.pass_ready == 1;
-    solver_step(&sst, S, S.kvs, jac);
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-    if (lane == 0) {
-      sst.pass_ready = 0;
-      sst.epi_ns += (t1 - t0);
-    }
-    __syncwarp();
-    unsigned long long* back = reinterpret_cast<unsigned long long*>(st);
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const int k = lane + 32 * q;
-      if (k < NW) back[k] = dst[k];
-    }
-    cont = sst.cont;
-  } else {
-    cont = st->cont;
+    solver_run<0>(st, S, sst, kv, st->pass_ready == 1, cond, use_cond);
+  } else if (lane == 0 && use_cond) {
+    cudaGraphSetConditional(cond, st->cont ? 1u : 0u);
   }
-  if (lane == 0 && use_cond) cudaGraphSetConditional(cond, cont ? 1u : 0u);
 }
 
 const void* solver_kernel_ptr() { return (const void*)solver_kernel; }

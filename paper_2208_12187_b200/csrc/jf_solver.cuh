@@ -179,7 +179,7 @@ __device__ __forceinline__ int eig_regs(SolverSmem& S, int n, int lane, double a
 }
 
 // All 32 lanes.  In: S.A (n x n symmetric), S.V = V0 if warm.  Out: S.lam, S.V.
-__device__ __noinline__ int warp_eig(SolverSmem& S, int n, int warm) {
+static __device__ __noinline__ int warp_eig(SolverSmem& S, int n, int warm) {
   const int lane = threadIdx.x & 31;
   if (!warm) {
     for (int e = lane; e < NMAX * NMAX; e += 32) {
@@ -838,25 +838,13 @@ __device__ __noinline__ void fit_after_pass(FitState* st, SolverSmem& S, const d
 
 // Whole warp: one solver step after a pass (state machine on lane 0, the
 // eigensolver on all lanes when a trial needs it).
-__device__ __forceinline__ void solver_step(FitState* st, SolverSmem& S, const double* kv, bool jac) {
+template <int n>
+__device__ __forceinline__ void solver_step_n(FitState* st, SolverSmem& S, const double* kv, bool jac) {
   const int lane = threadIdx.x & 31;
   const long long c0 = clock64();
-  const int nn = st->n;
-  // n is a template constant in each instance (the built-in models' n): the
-  // n-loops unroll and the small vectors live in registers
-  if (lane == 0) {
-    switch (nn) {
-      case 2: fit_after_pass<2>(st, S, kv, jac); break;
-      case 3: fit_after_pass<3>(st, S, kv, jac); break;
-      case 4: fit_after_pass<4>(st, S, kv, jac); break;
-      case 7: fit_after_pass<7>(st, S, kv, jac); break;
-      case 13: fit_after_pass<13>(st, S, kv, jac); break;
-      default: break;
-    }
-  }
+  if (lane == 0) fit_after_pass<n>(st, S, kv, jac);
   __syncwarp();
   if (S.need_trial && S.need_eig) {
-    const int n = st->n;
     const int warm = st->have_V;
     for (int e = lane; e < n * n; e += 32) {
       const int i = e / n, j = e % n;
@@ -869,18 +857,89 @@ __device__ __forceinline__ void solver_step(FitState* st, SolverSmem& S, const d
     if (lane == 0) st->prof[0] += clock64() - c1;
   }
   __syncwarp();
-  if (lane == 0 && S.need_trial) {
-    switch (nn) {
-      case 2: st_trial_finish<2>(st, S); break;
-      case 3: st_trial_finish<3>(st, S); break;
-      case 4: st_trial_finish<4>(st, S); break;
-      case 7: st_trial_finish<7>(st, S); break;
-      case 13: st_trial_finish<13>(st, S); break;
+  if (lane == 0 && S.need_trial) st_trial_finish<n>(st, S);
+  if (lane == 0) st->prof[3] += clock64() - c0;
+  __syncwarp();
+}
+
+// Whole warp: one solver step after a pass (state machine on lane 0, the
+// eigensolver on all lanes when a trial needs it).  NC = 0: dispatch on st->n.
+template <int NC>
+__device__ __forceinline__ void solver_step(FitState* st, SolverSmem& S, const double* kv, bool jac) {
+  if constexpr (NC > 0) {
+    solver_step_n<NC>(st, S, kv, jac);
+  } else {
+    switch (st->n) {
+      case 2: solver_step_n<2>(st, S, kv, jac); break;
+      case 3: solver_step_n<3>(st, S, kv, jac); break;
+      case 4: solver_step_n<4>(st, S, kv, jac); break;
+      case 7: solver_step_n<7>(st, S, kv, jac); break;
+      case 13: solver_step_n<13>(st, S, kv, jac); break;
       default: break;
     }
   }
-  if (lane == 0) st->prof[3] += clock64() - c0;
+}
+
+// Whole warp: load the fit state and the pass's K-vector (global, just
+// written by the pass) into shared memory — every load issued before any is
+// consumed — run one solver step, write the state back, set the CUDA-graph
+// WHILE condition.  Used by the solver kernel and by the fused J-pass.
+template <int NC>
+__device__ __forceinline__ void solver_run(FitState* __restrict__ st, SolverSmem& S, FitState& sst, const double* kv,
+                                           bool jac, cudaGraphConditionalHandle cond, int use_cond) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long t0, t1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  if (lane == 0) {
+    const int k = atomicAdd(&st->tl_n, 1);
+    if (k < 64) st->tl[k] = t0;
+  }
   __syncwarp();
+  constexpr int NW = sizeof(FitState) / 8;
+  constexpr int PER = (NW + 31) / 32;
+  constexpr int KPER = (KMAX + 31) / 32;
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(st);
+  unsigned long long* dst = reinterpret_cast<unsigned long long*>(&sst);
+  unsigned long long buf[PER];
+  double kvb[KPER];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int k = lane + 32 * q;
+    buf[q] = (k < NW) ? __ldcg(src + k) : 0ull;
+  }
+#pragma unroll
+  for (int q = 0; q < KPER; ++q) {
+    const int k = lane + 32 * q;
+    kvb[q] = (k < KMAX) ? __ldcg(kv + k) : 0.0;
+  }
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int k = lane + 32 * q;
+    if (k < NW) dst[k] = buf[q];
+  }
+#pragma unroll
+  for (int q = 0; q < KPER; ++q) {
+    const int k = lane + 32 * q;
+    if (k < KMAX) S.kvs[k] = kvb[q];
+  }
+  __syncwarp();
+  solver_step<NC>(&sst, S, S.kvs, jac);
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+  if (lane == 0) {
+    sst.pass_ready = 0;
+    sst.epi_ns += (t1 - t0);
+    const int k = sst.tl_n;
+    if (k < 64) sst.tl[k] = t1;
+    sst.tl_n = k + 1;
+  }
+  __syncwarp();
+  unsigned long long* back = reinterpret_cast<unsigned long long*>(st);
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int k = lane + 32 * q;
+    if (k < NW) back[k] = dst[k];
+  }
+  if (lane == 0 && use_cond) cudaGraphSetConditional(cond, sst.cont ? 1u : 0u);
 }
 
 }  // namespace jf

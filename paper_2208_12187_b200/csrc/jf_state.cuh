@@ -29,6 +29,9 @@ struct FitState {
   // ---- iteration state
   int32_t phase, status, nfev, njev, nit, cont, error, trace_len;
   int32_t full_rank, branch, launches, have_V;
+  int32_t kernels;     // kernel launches of this fit (pass kernels incl. predicated-out ones + solver kernels)
+  int32_t tl_n;        // timeline entries written
+  unsigned long long tl[64];  // device timeline (globaltimer ns): pass start/end, solver start/end
   int32_t pass_ready;  // set by a pass kernel's last block: 1 J-pass, 2 r-pass result in kv_in
   int32_t have_eig;    // eigendecomposition of the current B_hat computed (lazy, per iteration)
   unsigned long long comm_epoch;

@@ -32,4 +32,6 @@ for mode in ("graph", "hostloop"):
         torch.cuda.synchronize(); t0 = time.perf_counter()
         r = jf.curve_fit(pr.model, z, p0=pr.p0, grid=pr.grid, use_graph=(mode == "graph"), stream=s.cuda_stream)
         torch.cuda.synchronize(); t1 = time.perf_counter()
+    tl = np.array(r.timeline_ns) / 1e3
+    print("timeline us:", " ".join(f"{v:.1f}" for v in tl))
     print(mode, "fit", r.status, r.nfev, r.njev, r.cost, f"{(t1-t0)*1e3:.3f} ms", r.kernel_launches, f"epi {r.t_epilogue_s*1e6:.1f} us", [int(c) for c in r.epilogue_cycles])
