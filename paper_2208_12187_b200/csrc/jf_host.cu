@@ -186,6 +186,7 @@ PassPair select_pass(Ctx& c, const Kernels& k, bool weighted, int64_t m) {
   p.jtpb = k.jtpb;
   p.rtpb = k.rtpb;
   p.jgrid = grid_for(c, p.j, p.jtpb, m);
+  if (k.jsplit) p.jgrid = p.jgrid < 2 ? 2 : p.jgrid + (p.jgrid & 1);  // two equal halves
   p.rgrid = grid_for(c, p.r, p.rtpb, m);
   return p;
 }

@@ -11,6 +11,7 @@ static Kernels make() {
   k.jkw = pass_kernel<ModelExpDecay, true, C, true>;
   k.rkw = pass_kernel<ModelExpDecay, false, C, true>;
   k.jtpb = PassCfg<ModelExpDecay, true>::TPB;
+  k.jsplit = PassCfg<ModelExpDecay, true>::SPLIT;
   k.rtpb = PassCfg<ModelExpDecay, false>::TPB;
   return k;
 }

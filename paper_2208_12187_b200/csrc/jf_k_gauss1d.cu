@@ -11,6 +11,7 @@ static Kernels make() {
   k.jkw = pass_kernel<ModelGauss1D, true, C, true>;
   k.rkw = pass_kernel<ModelGauss1D, false, C, true>;
   k.jtpb = PassCfg<ModelGauss1D, true>::TPB;
+  k.jsplit = PassCfg<ModelGauss1D, true>::SPLIT;
   k.rtpb = PassCfg<ModelGauss1D, false>::TPB;
   return k;
 }

@@ -13,6 +13,7 @@ static Kernels make() {
   k.jkw = pass_kernel<ModelGauss2DRot, true, C, true>;
   k.rkw = pass_kernel<ModelGauss2DRot, false, C, true>;
   k.jtpb = PassCfg<ModelGauss2DRot, true>::TPB;
+  k.jsplit = PassCfg<ModelGauss2DRot, true>::SPLIT;
   k.rtpb = PassCfg<ModelGauss2DRot, false>::TPB;
   return k;
 }

@@ -11,6 +11,7 @@ static Kernels make() {
   k.jkw = pass_kernel<ModelGauss2DRotX2, true, C, true>;
   k.rkw = pass_kernel<ModelGauss2DRotX2, false, C, true>;
   k.jtpb = PassCfg<ModelGauss2DRotX2, true>::TPB;
+  k.jsplit = PassCfg<ModelGauss2DRotX2, true>::SPLIT;
   k.rtpb = PassCfg<ModelGauss2DRotX2, false>::TPB;
   return k;
 }

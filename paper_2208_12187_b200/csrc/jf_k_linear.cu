@@ -11,6 +11,7 @@ static Kernels make() {
   k.jkw = pass_kernel<ModelLinear, true, C, true>;
   k.rkw = pass_kernel<ModelLinear, false, C, true>;
   k.jtpb = PassCfg<ModelLinear, true>::TPB;
+  k.jsplit = PassCfg<ModelLinear, true>::SPLIT;
   k.rtpb = PassCfg<ModelLinear, false>::TPB;
   return k;
 }

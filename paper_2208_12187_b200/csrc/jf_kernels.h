@@ -13,6 +13,7 @@ struct Kernels {
   KernelFn jkw = nullptr;  // weighted variants (App. C)
   KernelFn rkw = nullptr;
   int jtpb = 256, rtpb = 256;  // threads per block of the J / r kernels
+  bool jsplit = false;         // J grid split in two halves (even grid >= 2)
 };
 Kernels kernels_linear(int coord);
 Kernels kernels_exp_decay(int coord);

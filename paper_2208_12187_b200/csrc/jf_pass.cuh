@@ -45,11 +45,24 @@ struct MinBlocks {
   static constexpr int value = Model::N <= 7 ? 2 : 1;
 };
 
-// Accumulate one point's contribution.  CONST_COL: a parameter whose partial
-// is identically 1 (the offset); unweighted, its diagonal slot is the point
-// count, kept as an integer instead of an fp64 add per point.
-template <class Model, bool JAC, class H>
-__device__ __forceinline__ void accumulate(double (&acc)[PassShape<Model, JAC>::KT], int& bad, int& cnt,
+// A contiguous range [RL, RH) of rows j of the W^T W upper triangle (slots
+// (j, k), j <= k <= n).  The n = 13 J-pass splits the triangle in two parts
+// computed by the two halves of the grid, so each thread holds ~half the
+// 105 accumulators (the model is evaluated by both halves).
+__host__ __device__ constexpr int part_count(int n, int rl, int rh) {
+  return rl >= rh ? 0 : (n + 1 - rl) + part_count(n, rl + 1, rh);
+}
+template <class Model, bool JAC, int RL, int RH>
+struct Part {
+  static constexpr int K = JAC ? part_count(Model::N, RL, RH) : 1;
+};
+
+// Accumulate one point's contribution to the part's slots.  CONST_COL: a
+// parameter whose partial is identically 1 (the offset); unweighted, its
+// diagonal slot is the point count, kept as an integer (cnt).  The non-finite
+// count is kept by the part that starts at row 0.
+template <class Model, bool JAC, int RL, int RH, class H>
+__device__ __forceinline__ void accumulate(double (&acc)[Part<Model, JAC, RL, RH>::K], int& bad, int& cnt,
                                            const H& h, double z, double wsig, bool weighted) {
   constexpr int N = Model::N;
   if constexpr (JAC) {
@@ -64,11 +77,11 @@ __device__ __forceinline__ void accumulate(double (&acc)[PassShape<Model, JAC>::
 #pragma unroll
       for (int j = 0; j <= N; ++j) w[j] *= wsig;  // App. C Eq. C13-C16
     }
-    bad += isfinite(w[N]) ? 0 : 1;
+    if constexpr (RL == 0) bad += isfinite(w[N]) ? 0 : 1;
     ++cnt;
     int s = 0;
 #pragma unroll
-    for (int j = 0; j <= N; ++j) {
+    for (int j = RL; j < RH; ++j) {
 #pragma unroll
       for (int k = j; k <= N; ++k) {
         if (j == CC && k == CC) {
@@ -87,18 +100,36 @@ __device__ __forceinline__ void accumulate(double (&acc)[PassShape<Model, JAC>::
   }
 }
 
-// Block-level combine of per-thread accumulators into partials[blockIdx.x].
-template <int KT, int TPB>
-__device__ __forceinline__ void block_partial(double (&acc)[KT], int bad, double* __restrict__ part,
-                                              double (*red)[KT + 1]) {
+// Block-level combine of one part's per-thread accumulators into the block's
+// full partial K-vector (slots outside the part are zero).
+template <class Model, bool JAC, int RL, int RH, int TPB>
+__device__ __forceinline__ void block_partial_part(double (&acc)[Part<Model, JAC, RL, RH>::K], int bad,
+                                                   double* __restrict__ part,
+                                                   double (*red)[PassShape<Model, JAC>::KT + 1]) {
+  constexpr int N = Model::N;
+  constexpr int KT = PassShape<Model, JAC>::KT;
   constexpr int NW = TPB / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int k = lane; k < KT + 1; k += 32) red[warp][k] = 0.0;
+  __syncwarp();
+  if constexpr (JAC) {
+    int s = 0;
 #pragma unroll
-  for (int k = 0; k < KT; ++k) {
-    double v = acc[k];
+    for (int j = RL; j < RH; ++j) {
+#pragma unroll
+      for (int k = j; k <= N; ++k) {
+        double v = acc[s];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+        if (lane == 0) red[warp][tri_slot(N, j, k)] = v;
+        ++s;
+      }
+    }
+  } else {
+    double v = acc[0];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-    if (lane == 0) red[warp][k] = v;
+    if (lane == 0) red[warp][0] = v;
   }
   const int b = __reduce_add_sync(FULL, bad);
   if (lane == 0) red[warp][KT] = (double)b;
@@ -222,9 +253,10 @@ struct PointIter {
 // start).  Relative error grows by a few ulp per step (<= ~4e-15 at L = 8).
 // A lane whose chunk start is outside a safe exponent range (|q| > 600 or a
 // step factor beyond e^300) evaluates exp directly for that chunk.
-template <class Model, bool JAC, bool WGT, int L, int TPB>
+template <class Model, bool JAC, bool WGT, int L, int TPB, int RL, int RH>
 __device__ __forceinline__ void grid_recur_loop(const PassArgs& a, const auto& pre,
-                                                double (&acc)[PassShape<Model, JAC>::KT], int& bad, int& cnt) {
+                                                double (&acc)[Part<Model, JAC, RL, RH>::K], int& bad, int& cnt,
+                                                int blk, int nblk) {
   constexpr int NE = Model::NEXP;
   constexpr int CW = 32 * L;
   constexpr double D = 32.0;
@@ -233,8 +265,8 @@ __device__ __forceinline__ void grid_recur_loop(const PassArgs& a, const auto& p
   const int64_t H = a.m / a.W;
   const int cpr = (W + CW - 1) / CW;
   const int64_t nch = H * (int64_t)cpr;
-  const int64_t nw = (int64_t)gridDim.x * (TPB / 32);
-  int64_t ch = (int64_t)blockIdx.x * (TPB / 32) + (threadIdx.x >> 5);
+  const int64_t nw = (int64_t)nblk * (TPB / 32);
+  int64_t ch = (int64_t)blk * (TPB / 32) + (threadIdx.x >> 5);
   const double* __restrict__ z = a.z;
   const double* __restrict__ ws = a.wsig;
   double ra[NE], rb2[NE], rx0[NE], ry0[NE], rho[NE];
@@ -293,7 +325,7 @@ __device__ __forceinline__ void grid_recur_loop(const PassArgs& a, const auto& p
       for (int k = 0; k < L; ++k) {
         const double X = X0 + 32.0 * k;
         const auto h = Model::template point_e<JAC>(pre, X, Y, E);
-        accumulate<Model, JAC>(acc, bad, cnt, h, zc[k], WGT ? wc[k] : 1.0, WGT);
+        accumulate<Model, JAC, RL, RH>(acc, bad, cnt, h, zc[k], WGT ? wc[k] : 1.0, WGT);
 #pragma unroll
         for (int g = 0; g < NE; ++g) {
           E[g] *= R[g];
@@ -307,7 +339,7 @@ __device__ __forceinline__ void grid_recur_loop(const PassArgs& a, const auto& p
         if (col0 + 32 * k < W) {
           const double X = X0 + 32.0 * k;
           const auto h = Model::template point<JAC>(pre, X, Y);
-          accumulate<Model, JAC>(acc, bad, cnt, h, zc[k], WGT ? wc[k] : 1.0, WGT);
+          accumulate<Model, JAC, RL, RH>(acc, bad, cnt, h, zc[k], WGT ? wc[k] : 1.0, WGT);
         }
       }
     }
@@ -322,52 +354,26 @@ struct PassCfg {
   static constexpr int P = JAC ? (Model::N == 7 ? 4 : 1) : (Model::N > 7 ? 2 : 4);
   static constexpr int TPB = 256;
   static constexpr int MINB = BIG ? 1 : 2;
-  static constexpr int L = JAC ? (Model::N > 7 ? 2 : 8) : 16;  // points per lane per warp-chunk (grid recurrence)
+  static constexpr int L = JAC ? (Model::N > 7 ? 2 : 8) : (Model::N > 7 ? 8 : 16);  // points per lane per warp-chunk (grid recurrence)
+  static constexpr bool SPLIT = JAC && Model::N > 7;  // two-part triangle (see run_part)
 };
 
-// The pass kernel.  epilogue == EPI_FIT: one pass of a fit (st is the state).
-template <class Model, bool JAC, int COORD, bool WGT, int P = PassCfg<Model, JAC>::P,
-          int TPB = PassCfg<Model, JAC>::TPB, int MINB = PassCfg<Model, JAC>::MINB>
-__global__ void __launch_bounds__(TPB, MINB)
-    pass_kernel(const PassArgs* __restrict__ pa, FitState* __restrict__ st, cudaGraphConditionalHandle cond,
-                int use_cond) {
-  (void)cond;
-  (void)use_cond;
-  using Sh = PassShape<Model, JAC>;
-  constexpr int KT = Sh::KT, KS = Sh::KS;
-  const PassArgs& a = *pa;
-
-  // Phase predication inside a fit: run only when this pass type is wanted.
-  if (a.epilogue == EPI_FIT) {
-    // the solver kernel after this pass may be scheduled now (PDL); it waits
-    // for this grid's completion in griddepcontrol.wait
-    asm volatile("griddepcontrol.launch_dependents;");
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      atomicAdd(&st->kernels, 1);
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      const int k = atomicAdd(&st->tl_n, 1);
-      if (k < 64) st->tl[k] = t;
-    }
-    const int ph = st->phase;
-    const bool want = JAC ? (ph == PH_INIT_J || ph == PH_TRIAL_J || ph == PH_ACCEPT_J) : (ph == PH_TRIAL_R);
-    if (!want) return;
-  }
-  const double* xs = (a.epilogue == EPI_FIT) ? st->x_eval : a.x;
-  double xv[Model::N];
+// One part [RL, RH) of the triangle over all points, by blocks [blk of nblk]:
+// the per-thread loop (grid recurrence or generic prefetching loop) and the
+// block partial into a.partials[blockIdx.x].
+template <class Model, bool JAC, int COORD, bool WGT, int P, int TPB, int RL, int RH, class Pre>
+__device__ __forceinline__ void run_part(const PassArgs& a, const Pre& pre, int blk, int nblk,
+                                         double (*red)[PassShape<Model, JAC>::KT + 1]) {
+  constexpr int KP = Part<Model, JAC, RL, RH>::K;
+  double acc[KP];
 #pragma unroll
-  for (int j = 0; j < Model::N; ++j) xv[j] = xs[j];
-  const auto pre = Model::template prologue<JAC>(xv);
-
-  double acc[KT];
-#pragma unroll
-  for (int k = 0; k < KT; ++k) acc[k] = 0.0;
+  for (int k = 0; k < KP; ++k) acc[k] = 0.0;
   int bad = 0, cnt = 0;
 
   const int64_t m = a.m;
-  const int64_t S = (int64_t)gridDim.x * TPB;
+  const int64_t S = (int64_t)nblk * TPB;
   PointIter<COORD> it;
-  it.init(a, (int64_t)blockIdx.x * TPB + threadIdx.x, S);
+  it.init(a, (int64_t)blk * TPB + threadIdx.x, S);
   const double* __restrict__ z = a.z;
   const double* __restrict__ y0 = a.y0;
   const double* __restrict__ y1 = a.y1;
@@ -394,7 +400,7 @@ __global__ void __launch_bounds__(TPB, MINB)
     }
   };
   if constexpr (COORD == COORD_GRID && Model::NEXP > 0) {
-    grid_recur_loop<Model, JAC, WGT, PassCfg<Model, JAC>::L, TPB>(a, pre, acc, bad, cnt);
+    grid_recur_loop<Model, JAC, WGT, PassCfg<Model, JAC>::L, TPB, RL, RH>(a, pre, acc, bad, cnt, blk, nblk);
   } else {
   auto coords = [&](double& X, double& Y) {
     if constexpr (COORD == COORD_GRID) {
@@ -407,10 +413,10 @@ __global__ void __launch_bounds__(TPB, MINB)
   auto eval = [&](double X, double Y, double zz, double ww) {
     if constexpr (TWO) {
       const auto h = Model::template point<JAC>(pre, X, Y);
-      accumulate<Model, JAC>(acc, bad, cnt, h, zz, ww, weighted);
+      accumulate<Model, JAC, RL, RH>(acc, bad, cnt, h, zz, ww, weighted);
     } else {
       const auto h = Model::template point<JAC>(pre, X);
-      accumulate<Model, JAC>(acc, bad, cnt, h, zz, ww, weighted);
+      accumulate<Model, JAC, RL, RH>(acc, bad, cnt, h, zz, ww, weighted);
     }
   };
   // main loop: full groups of P points, straight-line (no per-point predicate)
@@ -452,14 +458,64 @@ __global__ void __launch_bounds__(TPB, MINB)
   }
   if constexpr (JAC) {
     constexpr int CC = Model::CONST_COL;
-    if (!weighted) acc[tri_slot(Model::N, CC, CC)] = (double)cnt;
+    if constexpr (CC >= RL && CC < RH) {
+      if (!weighted) acc[tri_slot(Model::N, CC, CC) - tri_slot(Model::N, RL, RL)] = (double)cnt;
+    }
   }
+  block_partial_part<Model, JAC, RL, RH, TPB>(acc, bad, a.partials, red);
+
+}
+
+// The pass kernel.  epilogue == EPI_FIT: one pass of a fit (st is the state).
+template <class Model, bool JAC, int COORD, bool WGT, int P = PassCfg<Model, JAC>::P,
+          int TPB = PassCfg<Model, JAC>::TPB, int MINB = PassCfg<Model, JAC>::MINB>
+__global__ void __launch_bounds__(TPB, MINB)
+    pass_kernel(const PassArgs* __restrict__ pa, FitState* __restrict__ st, cudaGraphConditionalHandle cond,
+                int use_cond) {
+  (void)cond;
+  (void)use_cond;
+  using Sh = PassShape<Model, JAC>;
+  constexpr int KT = Sh::KT, KS = Sh::KS;
+  const PassArgs& a = *pa;
+
+  // Phase predication inside a fit: run only when this pass type is wanted.
+  if (a.epilogue == EPI_FIT) {
+    // the solver kernel after this pass may be scheduled now (PDL); it waits
+    // for this grid's completion in griddepcontrol.wait
+    asm volatile("griddepcontrol.launch_dependents;");
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      atomicAdd(&st->kernels, 1);
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      const int k = atomicAdd(&st->tl_n, 1);
+      if (k < 64) st->tl[k] = t;
+    }
+    const int ph = st->phase;
+    const bool want = JAC ? (ph == PH_INIT_J || ph == PH_TRIAL_J || ph == PH_ACCEPT_J) : (ph == PH_TRIAL_R);
+    if (!want) return;
+  }
+  const double* xs = (a.epilogue == EPI_FIT) ? st->x_eval : a.x;
+  double xv[Model::N];
+#pragma unroll
+  for (int j = 0; j < Model::N; ++j) xv[j] = xs[j];
+  const auto pre = Model::template prologue<JAC>(xv);
 
   __shared__ double red[TPB / 32][KT + 1];
   __shared__ double vec[KMAX];
   __shared__ double scratch[TPB];
   __shared__ unsigned int is_last;
-  block_partial<KT, TPB>(acc, bad, a.partials, red);
+  constexpr int NP1 = Model::N + 1;
+  if constexpr (JAC && Model::N > 7) {
+    // split triangle: rows [0, 4) by the first half of the grid, [4, n+1) by the second
+    const int half = gridDim.x / 2;
+    if ((int)blockIdx.x < half) {
+      run_part<Model, JAC, COORD, WGT, P, TPB, 0, 4>(a, pre, blockIdx.x, half, red);
+    } else {
+      run_part<Model, JAC, COORD, WGT, P, TPB, 4, NP1>(a, pre, blockIdx.x - half, gridDim.x - half, red);
+    }
+  } else {
+    run_part<Model, JAC, COORD, WGT, P, TPB, 0, (JAC ? NP1 : 1)>(a, pre, blockIdx.x, gridDim.x, red);
+  }
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) is_last = (atomicAdd(a.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
