@@ -673,7 +673,19 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
   CK(cudaMemcpyAsync(c->d_state, &h, sizeof(h), cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(c->d_args, &a, sizeof(a), cudaMemcpyHostToDevice, s));
   int launches = 0;
-  if (o.use_graph) {
+  // small m: the whole fit in one single-block kernel (state in shared memory)
+  const int n64_est = 10 + 8 * n + (n + 1) * (n + 2) / 2;
+  double small_budget = 1.0e6;
+  if (const char* e = getenv("JF_SMALL_WORK")) small_budget = atof(e);
+  const bool small = !o.comm && o.policy == JF_POLICY_SPECULATIVE && kk.small &&
+                     (double)m * n64_est <= small_budget;
+  if (small) {
+    SmallFitFn f = sg.wsig ? kk.smallw : kk.small;
+    f<<<1, 256, 0, s>>>(c->d_args, c->d_state);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(&h, c->d_state, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  } else if (o.use_graph) {
     GraphKey key{(const void*)k.j, o.policy, k.jgrid, k.rgrid};
     auto it = c->graphs.find(key);
     cudaGraphExec_t ge;

@@ -12,6 +12,8 @@ static Kernels make() {
   k.rkw = pass_kernel<ModelExpDecay, false, C, true>;
   k.jtpb = PassCfg<ModelExpDecay, true>::TPB;
   k.jsplit = PassCfg<ModelExpDecay, true>::SPLIT;
+  k.small = fit_small_kernel<ModelExpDecay, C, false>;
+  k.smallw = fit_small_kernel<ModelExpDecay, C, true>;
   k.rtpb = PassCfg<ModelExpDecay, false>::TPB;
   return k;
 }

@@ -12,6 +12,8 @@ static Kernels make() {
   k.rkw = pass_kernel<ModelGauss1D, false, C, true>;
   k.jtpb = PassCfg<ModelGauss1D, true>::TPB;
   k.jsplit = PassCfg<ModelGauss1D, true>::SPLIT;
+  k.small = fit_small_kernel<ModelGauss1D, C, false>;
+  k.smallw = fit_small_kernel<ModelGauss1D, C, true>;
   k.rtpb = PassCfg<ModelGauss1D, false>::TPB;
   return k;
 }

@@ -14,6 +14,8 @@ static Kernels make() {
   k.rkw = pass_kernel<ModelGauss2DRot, false, C, true>;
   k.jtpb = PassCfg<ModelGauss2DRot, true>::TPB;
   k.jsplit = PassCfg<ModelGauss2DRot, true>::SPLIT;
+  k.small = fit_small_kernel<ModelGauss2DRot, C, false>;
+  k.smallw = fit_small_kernel<ModelGauss2DRot, C, true>;
   k.rtpb = PassCfg<ModelGauss2DRot, false>::TPB;
   return k;
 }

@@ -12,6 +12,8 @@ static Kernels make() {
   k.rkw = pass_kernel<ModelGauss2DRotX2, false, C, true>;
   k.jtpb = PassCfg<ModelGauss2DRotX2, true>::TPB;
   k.jsplit = PassCfg<ModelGauss2DRotX2, true>::SPLIT;
+  k.small = fit_small_kernel<ModelGauss2DRotX2, C, false>;
+  k.smallw = fit_small_kernel<ModelGauss2DRotX2, C, true>;
   k.rtpb = PassCfg<ModelGauss2DRotX2, false>::TPB;
   return k;
 }

@@ -12,6 +12,8 @@ static Kernels make() {
   k.rkw = pass_kernel<ModelLinear, false, C, true>;
   k.jtpb = PassCfg<ModelLinear, true>::TPB;
   k.jsplit = PassCfg<ModelLinear, true>::SPLIT;
+  k.small = fit_small_kernel<ModelLinear, C, false>;
+  k.smallw = fit_small_kernel<ModelLinear, C, true>;
   k.rtpb = PassCfg<ModelLinear, false>::TPB;
   return k;
 }

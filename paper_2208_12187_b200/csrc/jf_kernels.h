@@ -7,6 +7,7 @@
 namespace jf {
 struct FitState;
 using KernelFn = void (*)(const PassArgs*, FitState*, cudaGraphConditionalHandle, int);
+using SmallFitFn = void (*)(const PassArgs*, FitState*);
 struct Kernels {
   KernelFn jk = nullptr;   // J-pass (value + dual Jacobian + fused Gram)
   KernelFn rk = nullptr;   // residual-only pass
@@ -14,6 +15,8 @@ struct Kernels {
   KernelFn rkw = nullptr;
   int jtpb = 256, rtpb = 256;  // threads per block of the J / r kernels
   bool jsplit = false;         // J grid split in two halves (even grid >= 2)
+  SmallFitFn small = nullptr;  // whole-fit single-block kernel (small m), unweighted / weighted
+  SmallFitFn smallw = nullptr;
 };
 Kernels kernels_linear(int coord);
 Kernels kernels_exp_decay(int coord);

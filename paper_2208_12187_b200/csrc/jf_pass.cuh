@@ -29,6 +29,7 @@
 #include "jf_common.cuh"
 #include "jf_dual.cuh"
 #include "jf_models.cuh"
+#include "jf_solver.cuh"
 #include "jf_state.cuh"
 
 namespace jf {
@@ -363,7 +364,7 @@ struct PassCfg {
 // block partial into a.partials[blockIdx.x].
 template <class Model, bool JAC, int COORD, bool WGT, int P, int TPB, int RL, int RH, class Pre>
 __device__ __forceinline__ void run_part(const PassArgs& a, const Pre& pre, int blk, int nblk,
-                                         double (*red)[PassShape<Model, JAC>::KT + 1]) {
+                                         double (*red)[PassShape<Model, JAC>::KT + 1], double* part_out) {
   constexpr int KP = Part<Model, JAC, RL, RH>::K;
   double acc[KP];
 #pragma unroll
@@ -462,7 +463,7 @@ __device__ __forceinline__ void run_part(const PassArgs& a, const Pre& pre, int 
       if (!weighted) acc[tri_slot(Model::N, CC, CC) - tri_slot(Model::N, RL, RL)] = (double)cnt;
     }
   }
-  block_partial_part<Model, JAC, RL, RH, TPB>(acc, bad, a.partials, red);
+  block_partial_part<Model, JAC, RL, RH, TPB>(acc, bad, part_out, red);
 
 }
 
@@ -509,12 +510,12 @@ __global__ void __launch_bounds__(TPB, MINB)
     // split triangle: rows [0, 4) by the first half of the grid, [4, n+1) by the second
     const int half = gridDim.x / 2;
     if ((int)blockIdx.x < half) {
-      run_part<Model, JAC, COORD, WGT, P, TPB, 0, 4>(a, pre, blockIdx.x, half, red);
+      run_part<Model, JAC, COORD, WGT, P, TPB, 0, 4>(a, pre, blockIdx.x, half, red, a.partials);
     } else {
-      run_part<Model, JAC, COORD, WGT, P, TPB, 4, NP1>(a, pre, blockIdx.x - half, gridDim.x - half, red);
+      run_part<Model, JAC, COORD, WGT, P, TPB, 4, NP1>(a, pre, blockIdx.x - half, gridDim.x - half, red, a.partials);
     }
   } else {
-    run_part<Model, JAC, COORD, WGT, P, TPB, 0, (JAC ? NP1 : 1)>(a, pre, blockIdx.x, gridDim.x, red);
+    run_part<Model, JAC, COORD, WGT, P, TPB, 0, (JAC ? NP1 : 1)>(a, pre, blockIdx.x, gridDim.x, red, a.partials);
   }
   __threadfence();
   __syncthreads();
@@ -557,6 +558,52 @@ __global__ void __launch_bounds__(TPB, MINB)
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     const int k = atomicAdd(&st->tl_n, 1);
     if (k < 64) st->tl[k] = t;
+  }
+}
+
+// ---------------------------------------------------------------- small m
+// The whole fit in ONE single-block kernel, for small m (the regime where
+// launch latency, not the data pass, dominates; Gpufit "runs
+// entirely in CUDA" and wins below v = 3e4).  The state lives in shared
+// memory for the whole fit; every iteration: the block's J-pass over all m
+// points (the same run_part as the grid kernels, one block) -> warp 0 runs
+// the solver step -> barrier.  Speculative policy (a J-pass per trial).
+template <class Model, int COORD, bool WGT>
+__global__ void __launch_bounds__(256, 1) fit_small_kernel(const PassArgs* __restrict__ pa, FitState* __restrict__ gst) {
+  constexpr int TPB = 256;
+  constexpr int KT = PassShape<Model, true>::KT;
+  constexpr int NP1 = Model::N + 1;
+  constexpr int P = (Model::N <= 4) ? 2 : 1;
+  __shared__ FitState st;
+  __shared__ SolverSmem S;
+  __shared__ double red[TPB / 32][KT + 1];
+  __shared__ double kvec[KT + 1];
+  const PassArgs& a = *pa;
+  {
+    constexpr int NW = sizeof(FitState) / 8;
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(gst);
+    unsigned long long* dst = reinterpret_cast<unsigned long long*>(&st);
+    for (int k = threadIdx.x; k < NW; k += TPB) dst[k] = src[k];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) st.kernels = st.kernels + 1;
+  for (int iter = 0; iter < 4 * st.max_nfev + 8; ++iter) {
+    __syncthreads();
+    if (!st.cont) break;
+    double xv[Model::N];
+#pragma unroll
+    for (int j = 0; j < Model::N; ++j) xv[j] = st.x_eval[j];
+    const auto pre = Model::template prologue<true>(xv);
+    run_part<Model, true, COORD, WGT, P, TPB, 0, NP1>(a, pre, 0, 1, red, kvec);
+    __syncthreads();
+    if (threadIdx.x < 32) solver_step<Model::N>(&st, S, kvec, true);
+  }
+  __syncthreads();
+  {
+    constexpr int NW = sizeof(FitState) / 8;
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(&st);
+    unsigned long long* dst = reinterpret_cast<unsigned long long*>(gst);
+    for (int k = threadIdx.x; k < NW; k += TPB) dst[k] = src[k];
   }
 }
 
