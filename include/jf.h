@@ -143,6 +143,8 @@ typedef struct jf_result {
   double optimality;            /* ||g||_inf (bounded: ||g * v||_inf) at x                     */
   double grad[JF_MAX_N];        /* g = J^T r at x (Eq. 4)                                      */
   double gram[JF_MAX_N * JF_MAX_N]; /* G = J^T J at x, n*n row-major (Eq. 5)                   */
+  double pcov[JF_MAX_N * JF_MAX_N]; /* parameter covariance (curve_fit's pcov): pinv(G) *
+                                   2 cost/(m-n), singular values below eps*max(m,n)*s_max dropped */
   int32_t status, nfev, njev, nit;
   int32_t n, trace_len;
   int8_t active_mask[JF_MAX_N]; /* -1 lower, +1 upper, 0 free (bounded fits; R19)              */

@@ -469,4 +469,20 @@ def fit(model, y, z, p0=None, lb=None, ub=None, ftol=1e-8, xtol=1e-8, gtol=1e-8,
         status = 0
     act = active_set(x, lb, ub, xtol) if bounded else np.zeros(n, dtype=np.int64)
     return dict(x=x, cost=cost, grad=g, gram=J.T.dot(J), optimality=gnorm, status=status,
-                nfev=nfev, njev=njev, nit=nit, active_mask=act, m=m, n=n)
+                nfev=nfev, njev=njev, nit=nit, active_mask=act, m=m, n=n, pcov=pcov(J, cost))
+
+
+def pcov(J, cost):
+    """Parameter covariance as curve_fit returns it with the fit (reading for
+    SURVEY A29 / N3): Moore-Penrose inverse of J^T J through the SVD of J,
+    singular values <= EPS max(m, n) s_max discarded, scaled by the residual
+    variance 2 cost / (m - n) (m > n; else +inf)."""
+    m, n = J.shape
+    _, s, VT = np.linalg.svd(J, full_matrices=False)
+    keep = s > EPS * max(m, n) * s[0]
+    s = s[keep]
+    VT = VT[: s.size]
+    P = (VT.T / s**2).dot(VT)
+    if m > n:
+        return P * (2.0 * cost / (m - n))
+    return np.full((n, n), np.inf)

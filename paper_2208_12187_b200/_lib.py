@@ -46,6 +46,7 @@ class jf_result(C.Structure):
     _fields_ = [
         ("x", C.c_double * JF_MAX_N), ("cost", C.c_double), ("optimality", C.c_double),
         ("grad", C.c_double * JF_MAX_N), ("gram", C.c_double * (JF_MAX_N * JF_MAX_N)),
+        ("pcov", C.c_double * (JF_MAX_N * JF_MAX_N)),
         ("status", C.c_int32), ("nfev", C.c_int32), ("njev", C.c_int32), ("nit", C.c_int32),
         ("n", C.c_int32), ("trace_len", C.c_int32),
         ("active_mask", C.c_int8 * JF_MAX_N),

@@ -115,6 +115,7 @@ class FitResult:
     optimality: float
     grad: np.ndarray
     gram: np.ndarray
+    pcov: np.ndarray
     status: int
     nfev: int
     njev: int
@@ -152,7 +153,8 @@ def curve_fit(model, z, y=None, *, grid=None, p0=None, lb=None, ub=None, sigma=N
         raise JFError(rc, "jf_curve_fit")
     out = FitResult(
         x=np.array(res.x[:n]), cost=res.cost, optimality=res.optimality, grad=np.array(res.grad[:n]),
-        gram=np.array(res.gram[: n * n]).reshape(n, n), status=res.status, nfev=res.nfev, njev=res.njev,
+        gram=np.array(res.gram[: n * n]).reshape(n, n), pcov=np.array(res.pcov[: n * n]).reshape(n, n),
+        status=res.status, nfev=res.nfev, njev=res.njev,
         nit=res.nit, active_mask=np.array(res.active_mask[:n], dtype=np.int64),
         kernel_launches=res.kernel_launches, t_upload_s=res.t_upload_s, t_solve_s=res.t_solve_s,
         t_epilogue_s=res.t_epilogue_s, epilogue_cycles=tuple(res.epilogue_cycles),

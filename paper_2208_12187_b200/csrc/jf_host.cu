@@ -729,7 +729,10 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
   for (int j = 0; j < n; ++j) {
     out->x[j] = h.x[j];
     out->grad[j] = h.g[j];
-    for (int q = 0; q < n; ++q) out->gram[j * n + q] = h.G[j * NMAX + q];
+    for (int q = 0; q < n; ++q) {
+      out->gram[j * n + q] = h.G[j * NMAX + q];
+      out->pcov[j * n + q] = h.pcov[j * NMAX + q];
+    }
   }
   if (bounded) active_mask_host(h.x, L, U, n, o.xtol, out->active_mask);
   out->trace_len = h.trace_len < o.trace_cap ? h.trace_len : o.trace_cap;

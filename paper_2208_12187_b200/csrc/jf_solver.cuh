@@ -838,6 +838,41 @@ __device__ __noinline__ void fit_after_pass(FitState* st, SolverSmem& S, const d
 
 // Whole warp: one solver step after a pass (state machine on lane 0, the
 // eigensolver on all lanes when a trial needs it).
+// Whole warp, once at the end of a fit: the parameter covariance curve_fit
+// returns with the parameters: the Moore-Penrose
+// inverse of J^T J at the final x, discarding singular values of J below
+// EPS * max(m, n) * s_max, scaled by 2 cost / (m - n) (m > n; else +inf).
+// J^T J = V diag(s^2) V^T is the final pass's Gram (the same eigensolver as
+// the trust-region subproblem).
+template <int n>
+__device__ __noinline__ void st_pcov(FitState* st, SolverSmem& S) {
+  const int lane = threadIdx.x & 31;
+  for (int e = lane; e < n * n; e += 32) {
+    const int i = e / n, j = e % n;
+    S.A[i][j] = st->G[i * NMAX + j];
+  }
+  __syncwarp();
+  warp_eig(S, n, 0);
+  if (lane == 0) {
+    const int64_t m = st->m_global;
+    const double smax = sqrt(fmax(S.lam[0], 0.0));
+    const double thr = DBL_EPSILON * (double)(m > n ? m : n) * smax;
+    const double s_sq = (m > n) ? 2.0 * st->cost / (double)(m - n) : INFINITY;
+    for (int i = 0; i < n; ++i) {
+      for (int j = 0; j < n; ++j) {
+        double t = 0.0;
+        for (int k = 0; k < n; ++k) {
+          const double sk = sqrt(fmax(S.lam[k], 0.0));
+          if (sk > thr) t += S.V[i][k] * S.V[j][k] / (sk * sk);
+        }
+        st->pcov[i * NMAX + j] = t * s_sq;
+      }
+    }
+    st->pcov_done = 1;
+  }
+  __syncwarp();
+}
+
 template <int n>
 __device__ __forceinline__ void solver_step_n(FitState* st, SolverSmem& S, const double* kv, bool jac) {
   const int lane = threadIdx.x & 31;
@@ -858,6 +893,8 @@ __device__ __forceinline__ void solver_step_n(FitState* st, SolverSmem& S, const
   }
   __syncwarp();
   if (lane == 0 && S.need_trial) st_trial_finish<n>(st, S);
+  __syncwarp();
+  if (!st->cont && st->error == 0 && !st->pcov_done) st_pcov<n>(st, S);
   if (lane == 0) st->prof[3] += clock64() - c0;
   __syncwarp();
 }

@@ -46,6 +46,8 @@ struct FitState {
   double d[NMAX], diag_h[NMAX], gh[NMAX], Gh[NMAX * NMAX], lam[NMAX], V[NMAX * NMAX], suf[NMAX];
   double step[NMAX], step_h[NMAX];
   double kv[KMAX];  // K-vector of the last pass
+  double pcov[NMAX * NMAX];  // parameter covariance at the final x (curve_fit's pcov)
+  int32_t pcov_done, pad7;
 };
 
 }  // namespace jf

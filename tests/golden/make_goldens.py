@@ -34,6 +34,7 @@ def main():
         out[key] = dict(status=r["status"], nfev=r["nfev"], njev=r["njev"], nit=r["nit"], cost=r["cost"],
                         x=[float(v) for v in r["x"]], active_mask=[int(v) for v in r["active_mask"]],
                         trace=[[float(v) for v in row] for row in tr],
+                        pcov=[[float(v) for v in row] for row in r["pcov"]],
                         source="oracle/trf.py fit on datagen inputs (tests/golden/make_goldens.py)")
         print(key, r["status"], r["nfev"], r["njev"], r["cost"], flush=True)
         json.dump(out, open(path, "w"), indent=1)

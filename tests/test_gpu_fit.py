@@ -32,6 +32,9 @@ def check_fit(res, ref, trace=None, ref_trace=None):
     x = ref["x"]
     assert np.all(np.abs(res.x - x) <= 1e-6 * np.maximum(np.abs(x), 1e-3 * np.max(np.abs(x))))
     assert res.cost == pytest.approx(ref["cost"], rel=1e-9)
+    if "pcov" in ref:  # curve_fit's covariance at the final x (N3)
+        pc = np.asarray(ref["pcov"])
+        assert np.allclose(res.pcov, pc, rtol=1e-6, atol=1e-9 * np.max(np.abs(pc)))
     if ref_trace is not None:
         tr = np.array(ref_trace)
         assert trace.shape == tr.shape

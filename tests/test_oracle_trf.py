@@ -300,3 +300,18 @@ def test_weighted_fit_equivalences():
                         jac=lambda x: models.jac(pr.model, y, x) / sig[:, None], method="trf",
                         tr_solver="exact", x_scale="jac")
     assert d["nfev"] == ref.nfev and np.allclose(d["x"], ref.x, rtol=1e-10)
+
+
+def test_pcov_matches_curve_fit_library():
+    """pcov: the oracle's covariance equals SciPy curve_fit's."""
+    from scipy.optimize import curve_fit as sp_curve_fit
+    pr = dg.make_gauss1d(2000)
+    res = trf.fit(pr.model, pr.t, pr.z, pr.p0)
+    f = lambda t, *p: models.h(pr.model, t, np.array(p))
+    popt, pc = sp_curve_fit(f, pr.t, pr.z, p0=pr.p0, method="trf", jac=lambda t, *p: models.jac(pr.model, t, np.array(p)),
+                            x_scale="jac")
+    assert np.allclose(res["x"], popt, rtol=1e-10)
+    assert np.allclose(res["pcov"], pc, rtol=1e-8, atol=1e-14 * np.max(np.abs(pc)))
+    # full rank: pcov = inv(J^T J) * s^2
+    J = models.jac(pr.model, pr.t, res["x"])
+    assert np.allclose(res["pcov"], np.linalg.inv(J.T @ J) * 2 * res["cost"] / (pr.m - 4), rtol=1e-9)
