@@ -81,9 +81,12 @@ typedef enum {
 typedef enum { JF_XSCALE_JAC = 0, JF_XSCALE_ONES = 1, JF_XSCALE_ARRAY = 2 } jf_xscale;
 
 /* How the per-pass reduction feeds App. B's SVD:
- *  GRAM: fp64 Gram G = J^T J, eigendecomposition of the scaled Gram on device
- *  TSQR: per-block Householder R of [J | r], SVD of the scaled R on device
- *  AUTO: GRAM (TSQR when the scaled Gram's condition number estimate exceeds 1e6) */
+ *  GRAM: fp64 Gram G = J^T J; Cholesky Gauss-Newton trial, eigendecomposition
+ *        of the scaled Gram when Alg. 2 needs alpha > 0
+ *  TSQR: R factor of W = [J | r] by CholeskyQR2 (a Gram pass, then a pass
+ *        accumulating (W R1^-1)^T (W R1^-1); R = chol(.) R1), SVD of the scaled
+ *        R by one-sided Jacobi (two passes per accepted step)
+ *  AUTO: TSQR if cond(J D^-1)^2 estimated at x0 exceeds 1e6, else GRAM */
 typedef enum { JF_SOLVE_AUTO = 0, JF_SOLVE_GRAM = 1, JF_SOLVE_TSQR = 2 } jf_solver;
 
 /* Which pass evaluates a trial point x + w (Eq. 15 needs f(x+w)):
@@ -112,7 +115,7 @@ typedef struct jf_opts {
   int32_t max_nfev;             /* 0 -> 100*n (R16)                                            */
   int32_t x_scale_mode;         /* jf_xscale, default JF_XSCALE_JAC                           */
   const double* x_scale;        /* host, n entries, used iff x_scale_mode == JF_XSCALE_ARRAY  */
-  int32_t solver;               /* jf_solver, default JF_SOLVE_GRAM                           */
+  int32_t solver;               /* jf_solver, default JF_SOLVE_GRAM (jf_pass: always the Gram) */
   int32_t policy;               /* jf_policy, default JF_POLICY_SPECULATIVE                   */
   int64_t grid_w, grid_h;       /* implicit pixel grid for 2-D models when y == NULL          */
   int64_t grid_row0;            /* global row of this shard's first row (sharded images)      */

@@ -57,6 +57,7 @@ struct PassArgs {
   unsigned int* ticket; // last-block ticket (reset by the last block)
   double* out;          // combined K-vector (EPI_NONE)
   int* err;             // EPI_NONE: set to JF_ECOMM (-5) if the cross-rank combine failed
+  const double* precond; // EPI_NONE TSQR second pass: P = R1^-1, (n+1)^2 row-major upper triangular
   int32_t use_comm;     // 1: combine across ranks through the mailboxes
   int32_t fuse_solver;  // reserved (0): the solver step runs in its own kernel (jf_solver.cu)
   CommDev comm;

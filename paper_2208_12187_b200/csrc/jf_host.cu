@@ -88,9 +88,9 @@ int model_d(int model) {
 
 struct GraphKey {
   const void* jk;
-  int policy, jgrid, rgrid;
+  int policy, jgrid, rgrid, qr;
   bool operator<(const GraphKey& o) const {
-    return std::tie(jk, policy, jgrid, rgrid) < std::tie(o.jk, o.policy, o.jgrid, o.rgrid);
+    return std::tie(jk, policy, jgrid, rgrid, qr) < std::tie(o.jk, o.policy, o.jgrid, o.rgrid, o.qr);
   }
 };
 
@@ -113,6 +113,7 @@ struct Ctx {
   double* d_in = nullptr;  // staged host inputs
   size_t in_cap = 0;
   double* d_scratch = nullptr;  // small per-call scratch (status word, subproblem I/O)
+  QRState* d_qr = nullptr;      // TSQR working set
   std::map<GraphKey, cudaGraphExec_t> graphs;
 };
 
@@ -136,6 +137,7 @@ int ctx_init(Ctx& c, int dev) {
   CK(cudaMalloc(&c.d_out, sizeof(double) * KMAX));
   CK(cudaMalloc(&c.d_x, sizeof(double) * NMAX));
   CK(cudaMalloc(&c.d_scratch, sizeof(double) * SCRATCH_DOUBLES));
+  CK(cudaMalloc(&c.d_qr, sizeof(QRState)));
   // no device-wide synchronisation here: emulated ranks (jf_comm_create_local)
   // may have pass kernels spinning on their mailboxes while a peer initialises
   CK(cudaMemsetAsync(c.d_ticket, 0, sizeof(unsigned int) * 4, c.stream));
@@ -175,7 +177,7 @@ int grid_for(Ctx& c, KernelFn f, int tpb, int64_t m) {
 
 // The two pass kernels a call uses, with their launch shapes.
 struct PassPair {
-  KernelFn j = nullptr, r = nullptr;
+  KernelFn j = nullptr, r = nullptr, jp = nullptr;
   int jtpb = 256, rtpb = 256, jgrid = 1, rgrid = 1;
 };
 
@@ -183,6 +185,7 @@ PassPair select_pass(Ctx& c, const Kernels& k, bool weighted, int64_t m) {
   PassPair p;
   p.j = weighted ? k.jkw : k.jk;
   p.r = weighted ? k.rkw : k.rk;
+  p.jp = weighted ? k.jkpw : k.jkp;
   p.jtpb = k.jtpb;
   p.rtpb = k.rtpb;
   p.jgrid = grid_for(c, p.j, p.jtpb, m);
@@ -354,14 +357,15 @@ void active_mask_host(const double* x, const double* lb, const double* ub, int n
   }
 }
 
-int launch_pass(const PassPair& k, bool jac, cudaStream_t s, PassArgs* d_args, FitState* d_state) {
-  KernelFn f = jac ? k.j : k.r;
+int launch_pass(const PassPair& k, bool jac, cudaStream_t s, PassArgs* d_args, FitState* d_state,
+                bool prec = false) {
+  KernelFn f = jac ? (prec ? k.jp : k.j) : k.r;
   f<<<jac ? k.jgrid : k.rgrid, jac ? k.jtpb : k.rtpb, 0, s>>>(d_args, d_state, (cudaGraphConditionalHandle)0, 0);
   CK(cudaGetLastError());
   return 0;
 }
 
-int build_graph(Ctx& c, const PassPair& k, int policy, cudaGraphExec_t* out) {
+int build_graph(Ctx& c, const PassPair& k, int policy, bool qr, cudaGraphExec_t* out) {
   cudaGraph_t g;
   CK(cudaGraphCreate(&g, 0));
   cudaGraphConditionalHandle h;
@@ -424,6 +428,12 @@ int build_graph(Ctx& c, const PassPair& k, int policy, cudaGraphExec_t* out) {
     kp.blockDim = dim3(k.rtpb);
     if (int e = add(kp, false)) return e;
     if (int e = add(sp, true)) return e;
+  }
+  if (qr) {  // TSQR: the preconditioned second pass runs when the phase is PH_QR2
+    kp.func = (void*)k.jp;
+    kp.gridDim = dim3(k.jgrid);
+    kp.blockDim = dim3(k.jtpb);
+    if (int e = add(kp, false)) return e;
   }
   kp.func = (void*)k.j;
   kp.gridDim = dim3(k.jgrid);
@@ -609,7 +619,8 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
   } else {
     for (int j = 0; j < n; ++j) XS[j] = 1.0;
   }
-  if (o.x_scale_mode < 0 || o.x_scale_mode > 2 || o.policy < 0 || o.policy > 1) return fail(JF_EINVAL);
+  if (o.x_scale_mode < 0 || o.x_scale_mode > 2 || o.policy < 0 || o.policy > 1 || o.solver < 0 || o.solver > 2)
+    return fail(JF_EINVAL);
   if (bounded) strictly_feasible_host(X0, L, U, n, 1e-10);
 
   Ctx* c;
@@ -654,6 +665,12 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
     h.x[j] = j < n ? X0[j] : 0.0;
     h.x_eval[j] = h.x[j];
   }
+  // TSQR or AUTO (decided on the device after the first pass) need the
+  // preconditioned-pass node in the graph
+  const bool qr = (o.solver == JF_SOLVE_TSQR || o.solver == JF_SOLVE_AUTO);
+  h.qr_mode = (o.solver == JF_SOLVE_TSQR) ? 1 : (o.solver == JF_SOLVE_AUTO ? 2 : 0);
+  h.qr = c->d_qr;
+  h.prec = c->d_qr->prec;
   h.phase = PH_INIT_J;
   h.status = STATUS_NONE;
   h.cont = 1;
@@ -677,7 +694,7 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
   const int n64_est = 10 + 8 * n + (n + 1) * (n + 2) / 2;
   double small_budget = 1.0e6;
   if (const char* e = getenv("JF_SMALL_WORK")) small_budget = atof(e);
-  const bool small = !o.comm && o.policy == JF_POLICY_SPECULATIVE && kk.small &&
+  const bool small = !o.comm && !qr && o.policy == JF_POLICY_SPECULATIVE && kk.small &&
                      (double)m * n64_est <= small_budget;
   if (small) {
     SmallFitFn f = sg.wsig ? kk.smallw : kk.small;
@@ -686,11 +703,11 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
     CK(cudaMemcpyAsync(&h, c->d_state, sizeof(h), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
   } else if (o.use_graph) {
-    GraphKey key{(const void*)k.j, o.policy, k.jgrid, k.rgrid};
+    GraphKey key{(const void*)k.j, o.policy, k.jgrid, k.rgrid, qr ? 1 : 0};
     auto it = c->graphs.find(key);
     cudaGraphExec_t ge;
     if (it == c->graphs.end()) {
-      r = build_graph(*c, k, o.policy, &ge);
+      r = build_graph(*c, k, o.policy, qr, &ge);
       if (r) return fail(r);
       c->graphs[key] = ge;
     } else {
@@ -703,7 +720,7 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
     const int cap = 4 * h.max_nfev + 8;
     for (int iter = 0; iter < cap; ++iter) {
       const bool jac = (o.policy == JF_POLICY_CONSERVATIVE) ? (h.phase != PH_TRIAL_R) : true;
-      r = launch_pass(k, jac, s, c->d_args, c->d_state);
+      r = launch_pass(k, jac, s, c->d_args, c->d_state, h.phase == PH_QR2);
       if (r) return fail(r);
       if (launch_solver(c->d_state, c->d_out, s)) return fail(JF_ECUDA);
       CK(cudaMemcpyAsync(&h, c->d_state, sizeof(h), cudaMemcpyDeviceToHost, s));

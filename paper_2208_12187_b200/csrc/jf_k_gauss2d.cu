@@ -12,6 +12,8 @@ static Kernels make() {
   k.rk = pass_kernel<ModelGauss2DRot, false, C, false>;
   k.jkw = pass_kernel<ModelGauss2DRot, true, C, true>;
   k.rkw = pass_kernel<ModelGauss2DRot, false, C, true>;
+  k.jkp = pass_kernel<ModelGauss2DRot, true, C, false, PassCfg<ModelGauss2DRot, true>::P, PassCfg<ModelGauss2DRot, true>::TPB, PassCfg<ModelGauss2DRot, true>::MINB, true>;
+  k.jkpw = pass_kernel<ModelGauss2DRot, true, C, true, PassCfg<ModelGauss2DRot, true>::P, PassCfg<ModelGauss2DRot, true>::TPB, PassCfg<ModelGauss2DRot, true>::MINB, true>;
   k.jtpb = PassCfg<ModelGauss2DRot, true>::TPB;
   k.jsplit = PassCfg<ModelGauss2DRot, true>::SPLIT;
   k.small = fit_small_kernel<ModelGauss2DRot, C, false>;

@@ -10,6 +10,8 @@ static Kernels make() {
   k.rk = pass_kernel<ModelGauss2DRotX2, false, C, false>;
   k.jkw = pass_kernel<ModelGauss2DRotX2, true, C, true>;
   k.rkw = pass_kernel<ModelGauss2DRotX2, false, C, true>;
+  k.jkp = pass_kernel<ModelGauss2DRotX2, true, C, false, PassCfg<ModelGauss2DRotX2, true>::P, PassCfg<ModelGauss2DRotX2, true>::TPB, PassCfg<ModelGauss2DRotX2, true>::MINB, true>;
+  k.jkpw = pass_kernel<ModelGauss2DRotX2, true, C, true, PassCfg<ModelGauss2DRotX2, true>::P, PassCfg<ModelGauss2DRotX2, true>::TPB, PassCfg<ModelGauss2DRotX2, true>::MINB, true>;
   k.jtpb = PassCfg<ModelGauss2DRotX2, true>::TPB;
   k.jsplit = PassCfg<ModelGauss2DRotX2, true>::SPLIT;
   k.small = fit_small_kernel<ModelGauss2DRotX2, C, false>;

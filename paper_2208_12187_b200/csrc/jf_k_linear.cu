@@ -10,6 +10,8 @@ static Kernels make() {
   k.rk = pass_kernel<ModelLinear, false, C, false>;
   k.jkw = pass_kernel<ModelLinear, true, C, true>;
   k.rkw = pass_kernel<ModelLinear, false, C, true>;
+  k.jkp = pass_kernel<ModelLinear, true, C, false, PassCfg<ModelLinear, true>::P, PassCfg<ModelLinear, true>::TPB, PassCfg<ModelLinear, true>::MINB, true>;
+  k.jkpw = pass_kernel<ModelLinear, true, C, true, PassCfg<ModelLinear, true>::P, PassCfg<ModelLinear, true>::TPB, PassCfg<ModelLinear, true>::MINB, true>;
   k.jtpb = PassCfg<ModelLinear, true>::TPB;
   k.jsplit = PassCfg<ModelLinear, true>::SPLIT;
   k.small = fit_small_kernel<ModelLinear, C, false>;

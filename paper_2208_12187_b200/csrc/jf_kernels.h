@@ -13,6 +13,8 @@ struct Kernels {
   KernelFn rk = nullptr;   // residual-only pass
   KernelFn jkw = nullptr;  // weighted variants (App. C)
   KernelFn rkw = nullptr;
+  KernelFn jkp = nullptr;   // J-pass with the TSQR preconditioner (CholeskyQR2 second pass)
+  KernelFn jkpw = nullptr;
   int jtpb = 256, rtpb = 256;  // threads per block of the J / r kernels
   bool jsplit = false;         // J grid split in two halves (even grid >= 2)
   SmallFitFn small = nullptr;  // whole-fit single-block kernel (small m), unweighted / weighted

@@ -62,9 +62,10 @@ struct Part {
 // parameter whose partial is identically 1 (the offset); unweighted, its
 // diagonal slot is the point count, kept as an integer (cnt).  The non-finite
 // count is kept by the part that starts at row 0.
-template <class Model, bool JAC, int RL, int RH, class H>
+template <class Model, bool JAC, int RL, int RH, bool PREC = false, class H>
 __device__ __forceinline__ void accumulate(double (&acc)[Part<Model, JAC, RL, RH>::K], int& bad, int& cnt,
-                                           const H& h, double z, double wsig, bool weighted) {
+                                           const H& h, double z, double wsig, bool weighted,
+                                           const double* __restrict__ prec = nullptr) {
   constexpr int N = Model::N;
   if constexpr (JAC) {
     constexpr int CC = Model::CONST_COL;
@@ -80,12 +81,27 @@ __device__ __forceinline__ void accumulate(double (&acc)[Part<Model, JAC, RL, RH
     }
     if constexpr (RL == 0) bad += isfinite(w[N]) ? 0 : 1;
     ++cnt;
+    if constexpr (PREC) {
+      // TSQR (CholeskyQR2) second pass: the row of W P, P = R1^-1 upper
+      // triangular ((n+1) x (n+1), shared memory), so the accumulated Gram is
+      // P^T (W^T W) P and its Cholesky factor R2 gives R = R2 R1
+      double u[N + 1];
+#pragma unroll
+      for (int k = 0; k <= N; ++k) {
+        double t = 0.0;
+#pragma unroll
+        for (int j = 0; j <= k; ++j) t = fma(w[j], prec[j * (N + 1) + k], t);
+        u[k] = t;
+      }
+#pragma unroll
+      for (int k = 0; k <= N; ++k) w[k] = u[k];
+    }
     int s = 0;
 #pragma unroll
     for (int j = RL; j < RH; ++j) {
 #pragma unroll
       for (int k = j; k <= N; ++k) {
-        if (j == CC && k == CC) {
+        if (j == CC && k == CC && !PREC) {
           if (weighted) acc[s] = fma(w[j], w[k], acc[s]);
         } else {
           acc[s] = fma(w[j], w[k], acc[s]);
@@ -254,10 +270,10 @@ struct PointIter {
 // start).  Relative error grows by a few ulp per step (<= ~4e-15 at L = 8).
 // A lane whose chunk start is outside a safe exponent range (|q| > 600 or a
 // step factor beyond e^300) evaluates exp directly for that chunk.
-template <class Model, bool JAC, bool WGT, int L, int TPB, int RL, int RH>
+template <class Model, bool JAC, bool WGT, int L, int TPB, int RL, int RH, bool PREC>
 __device__ __forceinline__ void grid_recur_loop(const PassArgs& a, const auto& pre,
                                                 double (&acc)[Part<Model, JAC, RL, RH>::K], int& bad, int& cnt,
-                                                int blk, int nblk) {
+                                                int blk, int nblk, const double* prec) {
   constexpr int NE = Model::NEXP;
   constexpr int CW = 32 * L;
   constexpr double D = 32.0;
@@ -326,7 +342,7 @@ __device__ __forceinline__ void grid_recur_loop(const PassArgs& a, const auto& p
       for (int k = 0; k < L; ++k) {
         const double X = X0 + 32.0 * k;
         const auto h = Model::template point_e<JAC>(pre, X, Y, E);
-        accumulate<Model, JAC, RL, RH>(acc, bad, cnt, h, zc[k], WGT ? wc[k] : 1.0, WGT);
+        accumulate<Model, JAC, RL, RH, PREC>(acc, bad, cnt, h, zc[k], WGT ? wc[k] : 1.0, WGT, prec);
 #pragma unroll
         for (int g = 0; g < NE; ++g) {
           E[g] *= R[g];
@@ -340,7 +356,7 @@ __device__ __forceinline__ void grid_recur_loop(const PassArgs& a, const auto& p
         if (col0 + 32 * k < W) {
           const double X = X0 + 32.0 * k;
           const auto h = Model::template point<JAC>(pre, X, Y);
-          accumulate<Model, JAC, RL, RH>(acc, bad, cnt, h, zc[k], WGT ? wc[k] : 1.0, WGT);
+          accumulate<Model, JAC, RL, RH, PREC>(acc, bad, cnt, h, zc[k], WGT ? wc[k] : 1.0, WGT, prec);
         }
       }
     }
@@ -362,9 +378,10 @@ struct PassCfg {
 // One part [RL, RH) of the triangle over all points, by blocks [blk of nblk]:
 // the per-thread loop (grid recurrence or generic prefetching loop) and the
 // block partial into a.partials[blockIdx.x].
-template <class Model, bool JAC, int COORD, bool WGT, int P, int TPB, int RL, int RH, class Pre>
+template <class Model, bool JAC, int COORD, bool WGT, int P, int TPB, int RL, int RH, bool PREC, class Pre>
 __device__ __forceinline__ void run_part(const PassArgs& a, const Pre& pre, int blk, int nblk,
-                                         double (*red)[PassShape<Model, JAC>::KT + 1], double* part_out) {
+                                         double (*red)[PassShape<Model, JAC>::KT + 1], double* part_out,
+                                         const double* prec) {
   constexpr int KP = Part<Model, JAC, RL, RH>::K;
   double acc[KP];
 #pragma unroll
@@ -401,7 +418,7 @@ __device__ __forceinline__ void run_part(const PassArgs& a, const Pre& pre, int 
     }
   };
   if constexpr (COORD == COORD_GRID && Model::NEXP > 0) {
-    grid_recur_loop<Model, JAC, WGT, PassCfg<Model, JAC>::L, TPB, RL, RH>(a, pre, acc, bad, cnt, blk, nblk);
+    grid_recur_loop<Model, JAC, WGT, PassCfg<Model, JAC>::L, TPB, RL, RH, PREC>(a, pre, acc, bad, cnt, blk, nblk, prec);
   } else {
   auto coords = [&](double& X, double& Y) {
     if constexpr (COORD == COORD_GRID) {
@@ -414,10 +431,10 @@ __device__ __forceinline__ void run_part(const PassArgs& a, const Pre& pre, int 
   auto eval = [&](double X, double Y, double zz, double ww) {
     if constexpr (TWO) {
       const auto h = Model::template point<JAC>(pre, X, Y);
-      accumulate<Model, JAC, RL, RH>(acc, bad, cnt, h, zz, ww, weighted);
+      accumulate<Model, JAC, RL, RH, PREC>(acc, bad, cnt, h, zz, ww, weighted, prec);
     } else {
       const auto h = Model::template point<JAC>(pre, X);
-      accumulate<Model, JAC, RL, RH>(acc, bad, cnt, h, zz, ww, weighted);
+      accumulate<Model, JAC, RL, RH, PREC>(acc, bad, cnt, h, zz, ww, weighted, prec);
     }
   };
   // main loop: full groups of P points, straight-line (no per-point predicate)
@@ -459,7 +476,7 @@ __device__ __forceinline__ void run_part(const PassArgs& a, const Pre& pre, int 
   }
   if constexpr (JAC) {
     constexpr int CC = Model::CONST_COL;
-    if constexpr (CC >= RL && CC < RH) {
+    if constexpr (CC >= RL && CC < RH && !PREC) {
       if (!weighted) acc[tri_slot(Model::N, CC, CC) - tri_slot(Model::N, RL, RL)] = (double)cnt;
     }
   }
@@ -469,7 +486,7 @@ __device__ __forceinline__ void run_part(const PassArgs& a, const Pre& pre, int 
 
 // The pass kernel.  epilogue == EPI_FIT: one pass of a fit (st is the state).
 template <class Model, bool JAC, int COORD, bool WGT, int P = PassCfg<Model, JAC>::P,
-          int TPB = PassCfg<Model, JAC>::TPB, int MINB = PassCfg<Model, JAC>::MINB>
+          int TPB = PassCfg<Model, JAC>::TPB, int MINB = PassCfg<Model, JAC>::MINB, bool PREC = false>
 __global__ void __launch_bounds__(TPB, MINB)
     pass_kernel(const PassArgs* __restrict__ pa, FitState* __restrict__ st, cudaGraphConditionalHandle cond,
                 int use_cond) {
@@ -492,7 +509,8 @@ __global__ void __launch_bounds__(TPB, MINB)
       if (k < 64) st->tl[k] = t;
     }
     const int ph = st->phase;
-    const bool want = JAC ? (ph == PH_INIT_J || ph == PH_TRIAL_J || ph == PH_ACCEPT_J) : (ph == PH_TRIAL_R);
+    const bool want = JAC ? (PREC ? (ph == PH_QR2) : (ph == PH_INIT_J || ph == PH_TRIAL_J || ph == PH_ACCEPT_J))
+                          : (ph == PH_TRIAL_R);
     if (!want) return;
   }
   const double* xs = (a.epilogue == EPI_FIT) ? st->x_eval : a.x;
@@ -500,6 +518,16 @@ __global__ void __launch_bounds__(TPB, MINB)
 #pragma unroll
   for (int j = 0; j < Model::N; ++j) xv[j] = xs[j];
   const auto pre = Model::template prologue<JAC>(xv);
+
+  // TSQR second pass: the preconditioner P = R1^-1 into shared memory
+  __shared__ double prec_s[PREC ? (Model::N + 1) * (Model::N + 1) : 1];
+  const double* prec = nullptr;
+  if constexpr (PREC) {
+    const double* src = (a.epilogue == EPI_FIT) ? st->prec : a.precond;
+    for (int k = threadIdx.x; k < (Model::N + 1) * (Model::N + 1); k += TPB) prec_s[k] = src[k];
+    __syncthreads();
+    prec = prec_s;
+  }
 
   __shared__ double red[TPB / 32][KT + 1];
   __shared__ double vec[KMAX];
@@ -510,12 +538,12 @@ __global__ void __launch_bounds__(TPB, MINB)
     // split triangle: rows [0, 4) by the first half of the grid, [4, n+1) by the second
     const int half = gridDim.x / 2;
     if ((int)blockIdx.x < half) {
-      run_part<Model, JAC, COORD, WGT, P, TPB, 0, 4>(a, pre, blockIdx.x, half, red, a.partials);
+      run_part<Model, JAC, COORD, WGT, P, TPB, 0, 4, PREC>(a, pre, blockIdx.x, half, red, a.partials, prec);
     } else {
-      run_part<Model, JAC, COORD, WGT, P, TPB, 4, NP1>(a, pre, blockIdx.x - half, gridDim.x - half, red, a.partials);
+      run_part<Model, JAC, COORD, WGT, P, TPB, 4, NP1, PREC>(a, pre, blockIdx.x - half, gridDim.x - half, red, a.partials, prec);
     }
   } else {
-    run_part<Model, JAC, COORD, WGT, P, TPB, 0, (JAC ? NP1 : 1)>(a, pre, blockIdx.x, gridDim.x, red, a.partials);
+    run_part<Model, JAC, COORD, WGT, P, TPB, 0, (JAC ? NP1 : 1), PREC>(a, pre, blockIdx.x, gridDim.x, red, a.partials, prec);
   }
   __threadfence();
   __syncthreads();
@@ -594,7 +622,7 @@ __global__ void __launch_bounds__(256, 1) fit_small_kernel(const PassArgs* __res
 #pragma unroll
     for (int j = 0; j < Model::N; ++j) xv[j] = st.x_eval[j];
     const auto pre = Model::template prologue<true>(xv);
-    run_part<Model, true, COORD, WGT, P, TPB, 0, NP1>(a, pre, 0, 1, red, kvec);
+    run_part<Model, true, COORD, WGT, P, TPB, 0, NP1, false>(a, pre, 0, 1, red, kvec, nullptr);
     __syncthreads();
     if (threadIdx.x < 32) solver_step<Model::N>(&st, S, kvec, true);
   }

@@ -44,6 +44,9 @@ struct SolverSmem {
   double w1[NMAX], w2[NMAX], w3[NMAX], w4[NMAX], w5[NMAX];
   double cinv[NMAX];
   double kvs[KMAX];  // the pass's K-vector (shared-memory copy)
+  double Q[2 * NMAX][MS];  // TSQR: [R_hat; diag(sqrt(diag_h))] (rows x n), SVD input
+  double caug[2 * NMAX];   // TSQR: [c; 0]
+  double sufq[NMAX];       // TSQR: suf = a_k . [c; 0] from the one-sided Jacobi
   int need_eig, need_trial, fast;
 };
 
@@ -243,6 +246,157 @@ static __device__ __noinline__ int warp_eig(SolverSmem& S, int n, int warm) {
   }
   __syncwarp();
   return sweeps;
+}
+
+// One-sided (Hestenes) Jacobi SVD of the rows x n matrix in S.Q (rows <= 32),
+// the whole warp: lane j owns column j (padded to an even N2 with zero
+// columns); a round of the circle schedule orthogonalises N2/2 disjoint column
+// pairs (p, q) at once by the rotation that zeroes a_p . a_q (both lanes
+// compute it from alpha = |a_p|^2, beta = |a_q|^2, gamma = a_p . a_q after
+// exchanging columns by shuffle).  At convergence the columns are
+// a_j = s_j u_j: S.lam = s^2 (descending), S.V, S.sufq = a_j . [c; 0]
+// (= s_j u_j^T [c; 0] = suf, App. B's S^T U^T r for the TSQR mode).
+template <int N2>
+__device__ __forceinline__ int svd_regs(SolverSmem& S, int n, int rows, int lane) {
+  constexpr int R = 2 * NMAX;
+  double a[R], v[N2];
+#pragma unroll
+  for (int i = 0; i < R; ++i) a[i] = (lane < n && i < rows) ? S.Q[i][lane] : 0.0;
+#pragma unroll
+  for (int i = 0; i < N2; ++i) v[i] = (i == lane) ? 1.0 : 0.0;
+  int sweeps = 0;
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    ++sweeps;
+    bool any = false;
+#pragma unroll
+    for (int r = 0; r < N2 - 1; ++r) {
+      int pj;
+      if (lane == N2 - 1) pj = r;
+      else if (lane == r) pj = N2 - 1;
+      else pj = ((2 * r - lane) % (N2 - 1) + (N2 - 1)) % (N2 - 1);
+      const bool act = lane < N2;
+      if (!act) pj = lane;
+      double pc[R];
+      double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        pc[i] = __shfl_sync(FULL, a[i], pj);
+        al = fma(a[i], a[i], al);
+        be = fma(pc[i], pc[i], be);
+        ga = fma(a[i], pc[i], ga);
+      }
+      const bool lo = lane < pj;
+      const double app = lo ? al : be, aqq = lo ? be : al;
+      double c = 1.0, sn = 0.0;
+      bool rot = false;
+      if (act && fabs(ga) > 2.220446049250313e-16 * sqrt(app * aqq) && ga != 0.0) {
+        // zeta = (aqq - app) / (2 gamma); t = sgn(zeta) / (|zeta| + sqrt(1 + zeta^2))
+        const double zeta = (aqq - app) / (2.0 * ga);
+        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+        c = rsqrt(fma(t, t, 1.0));
+        sn = c * t;
+        rot = true;
+      }
+      // a_p' = c a_p - s a_q, a_q' = s a_p + c a_q  ->  own' = c own + e partner
+      const double e = lo ? -sn : sn;
+      if (!__any_sync(FULL, rot)) continue;
+      any = true;
+#pragma unroll
+      for (int i = 0; i < R; ++i) a[i] = fma(c, a[i], e * pc[i]);
+#pragma unroll
+      for (int i = 0; i < N2; ++i) {
+        const double pv = __shfl_sync(FULL, v[i], pj);
+        v[i] = fma(c, v[i], e * pv);
+      }
+    }
+    if (!any) break;
+  }
+  // singular values, suf = a_j . c_aug, sort descending
+  double s2 = 0.0, sf = 0.0;
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    s2 = fma(a[i], a[i], s2);
+    sf = fma(a[i], S.caug[i], sf);
+  }
+  if (lane >= n) {
+    s2 = 0.0;
+    sf = 0.0;
+  }
+  int rank = 0;
+  for (int k = 0; k < n; ++k) {
+    const double sk = __shfl_sync(FULL, s2, k);
+    if (lane < n && (sk > s2 || (sk == s2 && k < lane))) ++rank;
+  }
+  __syncwarp();
+  if (lane < n) {
+    S.lam[rank] = s2;
+    S.sufq[rank] = sf;
+#pragma unroll
+    for (int i = 0; i < N2; ++i)
+      if (i < n) S.V[i][rank] = v[i];
+  }
+  __syncwarp();
+  return sweeps;
+}
+
+static __device__ __noinline__ int warp_svd(SolverSmem& S, int n, int rows) {
+  const int lane = threadIdx.x & 31;
+  const int N2 = (n + 1) & ~1;
+  switch (N2) {
+    case 2: return svd_regs<2>(S, n, rows, lane);
+    case 4: return svd_regs<4>(S, n, rows, lane);
+    case 6: return svd_regs<6>(S, n, rows, lane);
+    case 8: return svd_regs<8>(S, n, rows, lane);
+    case 10: return svd_regs<10>(S, n, rows, lane);
+    case 12: return svd_regs<12>(S, n, rows, lane);
+    case 14: return svd_regs<14>(S, n, rows, lane);
+    default: return svd_regs<16>(S, n, rows, lane);
+  }
+}
+
+// ---------------------------------------------- TSQR: CholeskyQR2 factors
+// W = [J | r] (m x (n+1)).  Pass 1 gives G1 = W^T W; R1 = chol(G1) (upper),
+// P = R1^-1 is applied to every row in pass 2, whose Gram G2 = P^T G1 P ~ I
+// gives R2 = chol(G2) and R = R2 R1 with the accuracy of a Householder TSQR
+// for cond(W) < ~1e8 (one Gram pass alone loses cond(W)^2).  R = [[R_J, c],
+// [0, rho]]: g = R_J^T c, J^T J = R_J^T R_J, 2 cost = |c|^2 + rho^2.
+// Lane 0; matrices row-major with stride n+1.
+
+// upper Cholesky of the Gram packed in a K-vector; false if not SPD
+template <int n>
+__device__ __forceinline__ bool chol_kv(const double* kv, double* R) {
+  constexpr int N1 = n + 1;
+  for (int i = 0; i < N1; ++i)
+    for (int j = 0; j < N1; ++j) R[i * N1 + j] = (j >= i) ? kv[tri_slot(n, i, j)] : 0.0;
+  for (int k = 0; k < N1; ++k) {
+    double d = R[k * N1 + k];
+    for (int j = 0; j < k; ++j) d = fma(-R[j * N1 + k], R[j * N1 + k], d);
+    if (!(d > 0.0)) return false;
+    const double rk = sqrt(d);
+    const double inv = 1.0 / rk;
+    R[k * N1 + k] = rk;
+    for (int i = k + 1; i < N1; ++i) {
+      double t = R[k * N1 + i];
+      for (int j = 0; j < k; ++j) t = fma(-R[j * N1 + k], R[j * N1 + i], t);
+      R[k * N1 + i] = t * inv;
+    }
+  }
+  return true;
+}
+
+// P = R^-1 for upper-triangular R
+template <int n>
+__device__ __forceinline__ void tri_inv(const double* R, double* P) {
+  constexpr int N1 = n + 1;
+  for (int i = 0; i < N1 * N1; ++i) P[i] = 0.0;
+  for (int j = 0; j < N1; ++j) {
+    P[j * N1 + j] = 1.0 / R[j * N1 + j];
+    for (int i = j - 1; i >= 0; --i) {
+      double t = 0.0;
+      for (int k = i + 1; k <= j; ++k) t = fma(R[i * N1 + k], P[k * N1 + j], t);
+      P[i * N1 + j] = -t / R[i * N1 + i];
+    }
+  }
 }
 
 // --------------------------------------------------- Alg. 2 + App. B (scalar)
@@ -593,7 +747,9 @@ __device__ __noinline__ void st_trial_begin(FitState* st, SolverSmem& S) {
   S.need_trial = 1;
   S.fast = 0;
   S.need_eig = 0;
-  if (!st->have_eig) {
+  if (!st->have_eig && st->qr_mode) {
+    S.need_eig = 1;  // TSQR: the SVD of R_hat, no Cholesky shortcut
+  } else if (!st->have_eig) {
     const long long c0 = clock64();
     S.fast = gn_fastpath<n>(S, st->m_global, st->gh, st->Delta, S.w3);
     st->prof[1] += clock64() - c0;
@@ -616,10 +772,10 @@ __device__ __noinline__ void st_trial_finish(FitState* st, SolverSmem& S) {
         st->lam[j] = S.lam[j];
         for (int i = 0; i < n; ++i) st->V[i * NMAX + j] = S.V[i][j];
       }
-      for (int j = 0; j < n; ++j) {  // S^T U^T r = V^T g_hat (c.1b)
+      for (int j = 0; j < n; ++j) {  // S^T U^T r = V^T g_hat (c.1b); TSQR: a_j . [c; 0]
         double t = 0.0;
         for (int i = 0; i < n; ++i) t = fma(S.V[i][j], st->gh[i], t);
-        st->suf[j] = t;
+        st->suf[j] = st->qr_mode ? S.sufq[j] : t;
       }
       st->have_eig = 1;
       st->have_V = 1;
@@ -702,22 +858,104 @@ __device__ __noinline__ void st_outer_top(FitState* st, SolverSmem& S) {
   st_trial_begin<n>(st, S);
 }
 
+// TSQR: start the preconditioned second pass at the current x from the
+// first pass's Gram (kv).  Returns false if G1 is not numerically SPD
+// (cond(W) beyond ~1e8): the fit then continues in Gram mode.
+template <int n>
+__device__ __forceinline__ bool st_qr_begin(FitState* st, SolverSmem& S, const double* kv, int after) {
+  constexpr int N1 = n + 1;
+  double* R1 = &S.T[0][0];
+  double* P = &S.M2[0][0];
+  if (!chol_kv<n>(kv, R1)) {
+    st->qr_mode = 0;
+    return false;
+  }
+  tri_inv<n>(R1, P);
+  for (int i = 0; i < N1 * N1; ++i) {
+    st->qr->R1[i] = R1[i];
+    st->qr->prec[i] = P[i];
+  }
+  st->qr_after = after;
+  st->phase = PH_QR2;
+  return true;
+}
+
+// TSQR: after the preconditioned pass, R = chol(G2) R1 and (g, G) from R.
+template <int n>
+__device__ __forceinline__ void st_qr_finish(FitState* st, SolverSmem& S, const double* kv) {
+  constexpr int N1 = n + 1;
+  double* R2 = &S.T[0][0];
+  double* R = &S.M2[0][0];
+  const double* R1 = st->qr->R1;
+  if (!chol_kv<n>(kv, R2)) {  // G2 ~ I in exact arithmetic; keep R1 if rounding broke it
+    for (int i = 0; i < N1 * N1; ++i) R2[i] = (i % (N1 + 1) == 0) ? 1.0 : 0.0;
+  }
+  for (int i = 0; i < N1; ++i)
+    for (int j = 0; j < N1; ++j) {
+      double t = 0.0;
+      for (int k = i; k <= j; ++k) t = fma(R2[i * N1 + k], R1[k * N1 + j], t);
+      R[i * N1 + j] = (j >= i) ? t : 0.0;
+    }
+  for (int i = 0; i < N1 * N1; ++i) st->qr->R[i] = R[i];
+  for (int j = 0; j < n; ++j) {  // g = R_J^T c, G = R_J^T R_J
+    double t = 0.0;
+    for (int k = 0; k <= j; ++k) t = fma(R[k * N1 + j], R[k * N1 + n], t);
+    st->g[j] = t;
+    for (int l = j; l < n; ++l) {
+      double u = 0.0;
+      for (int k = 0; k <= j; ++k) u = fma(R[k * N1 + j], R[k * N1 + l], u);
+      st->G[j * NMAX + l] = u;
+      st->G[l * NMAX + j] = u;
+    }
+  }
+}
+
+// AUTO solver choice (jf.h jf_solver): an upper bound on cond(J D^-1)^2 for
+// the column-scaled Gram B = D^-1 G D^-1 (D = column norms): lambda_max <=
+// trace(B) = n and lambda_min >= 1/||L^-1||_F^2 (B = L L^T); +inf if B is not
+// numerically SPD.
+template <int n>
+__device__ __forceinline__ double kappa2_estimate(FitState* st, SolverSmem& S) {
+  double dinv[NMAX];
+  for (int j = 0; j < n; ++j) {
+    const double gjj = st->G[j * NMAX + j];
+    dinv[j] = gjj > 0.0 ? rsqrt(gjj) : 1.0;
+  }
+  double(*L)[MS] = S.T;
+  double tr = 0.0;
+  for (int i = 0; i < n; ++i) {
+    for (int j = 0; j <= i; ++j) L[i][j] = dinv[i] * st->G[i * NMAX + j] * dinv[j];
+    tr += L[i][i];
+  }
+  for (int k = 0; k < n; ++k) {
+    double d = L[k][k];
+    for (int j = 0; j < k; ++j) d = fma(-L[k][j], L[k][j], d);
+    if (!(d > 0.0)) return INFINITY;
+    const double r = rsqrt(d);
+    L[k][k] = d * r;
+    S.cinv[k] = r;
+    for (int i = k + 1; i < n; ++i) {
+      double t = L[i][k];
+      for (int j = 0; j < k; ++j) t = fma(-L[i][j], L[k][j], t);
+      L[i][k] = t * r;
+    }
+  }
+  double fro = 0.0;
+  double* y = S.w1;
+  for (int c = 0; c < n; ++c) {
+    for (int i = c; i < n; ++i) {
+      double t = (i == c) ? 1.0 : 0.0;
+      for (int k = c; k < i; ++k) t = fma(-L[i][k], y[k], t);
+      y[i] = t * S.cinv[i];
+      fro = fma(y[i], y[i], fro);
+    }
+  }
+  return tr * fro;
+}
+
 // Initialisation after the J-pass at x0 (Alg. 1 l.137-138; R3, R4, R18).
 template <int n>
-__device__ __noinline__ void st_init(FitState* st, SolverSmem& S, const double* kv) {
-  if (kv[tri_count(n)] != 0.0) {  // R18: residuals at x0 must be finite
-    st->error = -3;
-    st->status = -3;
-    st->phase = PH_DONE;
-    st->cont = 0;
-    return;
-  }
-  st_take_pass<n>(st, kv);
-  st->nfev = 1;
-  st->njev = 1;
-  st->nit = 0;
-  st->alpha = 0.0;
-  st->status = STATUS_NONE;
+__device__ __noinline__ void st_init_finish(FitState* st, SolverSmem& S) {
   if (st->jacmode) {
     st_update_scale<n>(st, true);
   } else {
@@ -740,6 +978,28 @@ __device__ __noinline__ void st_init(FitState* st, SolverSmem& S, const double* 
   st_outer_top<n>(st, S);
 }
 
+template <int n>
+__device__ __noinline__ void st_init(FitState* st, SolverSmem& S, const double* kv) {
+  if (kv[tri_count(n)] != 0.0) {  // R18: residuals at x0 must be finite
+    st->error = -3;
+    st->status = -3;
+    st->phase = PH_DONE;
+    st->cont = 0;
+    return;
+  }
+  st_take_pass<n>(st, kv);
+  st->nfev = 1;
+  st->njev = 1;
+  st->nit = 0;
+  st->alpha = 0.0;
+  st->status = STATUS_NONE;
+  if (st->qr_mode == 2) {  // AUTO: TSQR iff the column-scaled Gram at x0 is ill-conditioned
+    st->qr_mode = (kappa2_estimate<n>(st, S) > 1.0e6) ? 1 : 0;
+  }
+  if (st->qr_mode && st_qr_begin<n>(st, S, kv, 0)) return;  // R from the second pass first
+  st_init_finish<n>(st, S);
+}
+
 // End of the inner (retry) loop: accept or keep x, count the iteration.  For
 // the conservative policy an accepted step first needs the J-pass at x_new.
 template <int n>
@@ -754,6 +1014,7 @@ __device__ __noinline__ void st_end_inner(FitState* st, SolverSmem& S, bool have
     st_take_pass<n>(st, st->kv);
     st->cost = st->cost_new;  // SciPy keeps the trial's cost
     st->njev = st->njev + 1;
+    if (st->qr_mode && st_qr_begin<n>(st, S, st->kv, 1)) return;  // nit counts after the QR pass
     if (st->jacmode) st_update_scale<n>(st, false);
   }
   st->nit = st->nit + 1;  // R27
@@ -830,9 +1091,19 @@ __device__ __noinline__ void fit_after_pass(FitState* st, SolverSmem& S, const d
     st_take_pass<n>(st, st->kv);  // g, G at the accepted x (cost kept: SciPy)
     st->cost = st->cost_new;
     st->njev = st->njev + 1;
+    if (st->qr_mode && st_qr_begin<n>(st, S, st->kv, 1)) return;
     if (st->jacmode) st_update_scale<n>(st, false);
     st->nit = st->nit + 1;
     st_outer_top<n>(st, S);
+  } else if (phase == PH_QR2 && jac) {
+    st_qr_finish<n>(st, S, st->kv);
+    if (st->qr_after == 0) {
+      st_init_finish<n>(st, S);
+    } else {
+      if (st->jacmode) st_update_scale<n>(st, false);
+      st->nit = st->nit + 1;
+      st_outer_top<n>(st, S);
+    }
   }
 }
 
@@ -847,12 +1118,23 @@ __device__ __noinline__ void fit_after_pass(FitState* st, SolverSmem& S, const d
 template <int n>
 __device__ __noinline__ void st_pcov(FitState* st, SolverSmem& S) {
   const int lane = threadIdx.x & 31;
-  for (int e = lane; e < n * n; e += 32) {
-    const int i = e / n, j = e % n;
-    S.A[i][j] = st->G[i * NMAX + j];
+  if (st->qr_mode) {  // TSQR: singular values of J from R_J (one-sided Jacobi), not squared
+    constexpr int N1 = n + 1;
+    for (int e = lane; e < 2 * NMAX * n; e += 32) {
+      const int i = e / n, j = e % n;
+      S.Q[i][j] = (i < n) ? st->qr->R[i * N1 + j] : 0.0;
+    }
+    for (int i = lane; i < 2 * NMAX; i += 32) S.caug[i] = 0.0;
+    __syncwarp();
+    warp_svd(S, n, n);
+  } else {
+    for (int e = lane; e < n * n; e += 32) {
+      const int i = e / n, j = e % n;
+      S.A[i][j] = st->G[i * NMAX + j];
+    }
+    __syncwarp();
+    warp_eig(S, n, 0);
   }
-  __syncwarp();
-  warp_eig(S, n, 0);
   if (lane == 0) {
     const int64_t m = st->m_global;
     const double smax = sqrt(fmax(S.lam[0], 0.0));
@@ -879,7 +1161,24 @@ __device__ __forceinline__ void solver_step_n(FitState* st, SolverSmem& S, const
   const long long c0 = clock64();
   if (lane == 0) fit_after_pass<n>(st, S, kv, jac);
   __syncwarp();
-  if (S.need_trial && S.need_eig) {
+  if (S.need_trial && S.need_eig && st->qr_mode) {
+    // TSQR: SVD of [R_J diag(d); diag(sqrt(diag_h))] and [c; 0] (App. B on R)
+    constexpr int N1 = n + 1;
+    const double* R = st->qr->R;
+    const int rows = st->bounded ? 2 * n : n;
+    for (int e = lane; e < 2 * NMAX * n; e += 32) {
+      const int i = e / n, j = e % n;
+      double q = 0.0;
+      if (i < n) q = R[i * N1 + j] * st->d[j];
+      else if (i < rows) q = (i - n == j) ? sqrt(st->diag_h[j]) : 0.0;
+      S.Q[i][j] = q;
+    }
+    for (int i = lane; i < 2 * NMAX; i += 32) S.caug[i] = (i < n) ? R[i * N1 + n] : 0.0;
+    __syncwarp();
+    const long long c1 = clock64();
+    warp_svd(S, n, rows);
+    if (lane == 0) st->prof[0] += clock64() - c1;
+  } else if (S.need_trial && S.need_eig) {
     const int warm = st->have_V;
     for (int e = lane; e < n * n; e += 32) {
       const int i = e / n, j = e % n;

@@ -12,7 +12,16 @@ enum Phase : int32_t {
   PH_TRIAL_J = 1,   // speculative policy: J-pass at a trial point
   PH_TRIAL_R = 2,   // conservative policy: residual pass at a trial point
   PH_ACCEPT_J = 3,  // conservative policy: J-pass at the accepted point
-  PH_DONE = 4
+  PH_DONE = 4,
+  PH_QR2 = 5        // TSQR (CholeskyQR2): preconditioned J-pass at the current x
+};
+
+// TSQR working set (device, one per fit context): CholeskyQR2 factors of
+// W = [J | r], (n+1) x (n+1) row-major upper triangular.
+struct QRState {
+  double prec[(NMAX + 1) * (NMAX + 1)];  // P = R1^-1 (read by the preconditioned pass)
+  double R1[(NMAX + 1) * (NMAX + 1)];    // chol(W^T W)
+  double R[(NMAX + 1) * (NMAX + 1)];     // R = R2 R1
 };
 
 constexpr int TRACE_FIELDS = 12;
@@ -47,7 +56,10 @@ struct FitState {
   double step[NMAX], step_h[NMAX];
   double kv[KMAX];  // K-vector of the last pass
   double pcov[NMAX * NMAX];  // parameter covariance at the final x (curve_fit's pcov)
-  int32_t pcov_done, pad7;
+  int32_t pcov_done, qr_mode;  // qr_mode: TSQR (CholeskyQR2 + SVD of R) instead of the Gram eigensolver
+  int32_t qr_after, pad8;      // what follows the PH_QR2 pass: 0 initialisation, 1 an accepted step
+  QRState* qr;                 // device TSQR working set
+  double* prec;                // = qr->prec (read by the preconditioned pass kernel)
 };
 
 }  // namespace jf

@@ -157,3 +157,60 @@ def test_full_size_fit_matches_oracle_golden(key):
     ref = dict(gold)
     ref["x"] = np.array(gold["x"])
     check_fit(res, ref, res.trace, gold["trace"])
+
+
+TSQR_FITS = [
+    ("C2 m=100000", lambda: dg.make_gauss1d(100_000)),
+    ("C3 W=256", lambda: dg.make_gauss2d(256)),
+    ("C4b W=256", lambda: dg.make_gauss2d_bounded(256, "b")),
+    ("C4c W=256", lambda: dg.make_gauss2d_bounded(256, "c")),
+    ("C5 W=128", lambda: dg.make_gauss2d_x2(128)),
+]
+
+
+@pytest.mark.parametrize("name,make", TSQR_FITS, ids=[f[0] for f in TSQR_FITS])
+@pytest.mark.parametrize("policy", ["speculative", "conservative"])
+def test_tsqr_fit_matches_oracle(name, make, policy):
+    """TSQR mode (R factor of [J | r] by CholeskyQR2, SVD of
+    the scaled R by one-sided Jacobi): same trajectory as the oracle's SVD of J."""
+    pr = make()
+    tr = []
+    ref = otrf.fit(pr.model, pr.coords(), pr.z, pr.p0, pr.lb, pr.ub, trace=tr)
+    res = jf.curve_fit(pr.model, pr.z, p0=pr.p0, lb=pr.lb, ub=pr.ub, trace_cap=256, solver="tsqr",
+                       policy=policy, **_kw(pr))
+    check_fit(res, ref, res.trace, tr)
+
+
+def _ill_conditioned(sig):
+    m = 20000
+    t = np.arange(m) / m
+    truth = np.array([1.0, 0.5, sig, 0.2])
+    z = dg.render("gauss1d", t, truth) + 0.01 * np.random.default_rng(7).standard_normal(m)
+    return t, z, truth * np.array([1.1, 0.95, 1.1, 0.9])
+
+
+@pytest.mark.parametrize("sig", [1.0, 1.5])
+def test_tsqr_ill_conditioned_matches_oracle(sig):
+    """kappa(J D^-1) ~ 5e3 / 3e4 (wide Gaussian ~ offset): the TSQR path keeps
+    the oracle's trajectory (reading R28: the Gram path's eigenvalues resolve
+    s_min only to ~1e-8 s_max)."""
+    t, z, p0 = _ill_conditioned(sig)
+    tr = []
+    ref = otrf.fit("gauss1d", t, z, p0, trace=tr)
+    res = jf.curve_fit("gauss1d", z, y=t, p0=p0, solver="tsqr", trace_cap=256)
+    check_fit(res, ref, res.trace, tr)
+
+
+def test_auto_solver_picks_tsqr_only_when_ill_conditioned():
+    """AUTO: the ill-conditioned case follows the oracle like TSQR; the
+    well-conditioned case runs the Gram path (one pass per trial)."""
+    t, z, p0 = _ill_conditioned(1.5)
+    ref = otrf.fit("gauss1d", t, z, p0)
+    res = jf.curve_fit("gauss1d", z, y=t, p0=p0, solver="auto")
+    check_fit(res, ref)
+    pr = dg.make_gauss2d(256)
+    ref = otrf.fit(pr.model, pr.coords(), pr.z, pr.p0)
+    res_auto = jf.curve_fit(pr.model, pr.z, p0=pr.p0, grid=pr.grid, solver="auto")
+    res_gram = jf.curve_fit(pr.model, pr.z, p0=pr.p0, grid=pr.grid, solver="gram")
+    check_fit(res_auto, ref)
+    assert np.array_equal(res_auto.x, res_gram.x)
