@@ -59,7 +59,7 @@ struct PassArgs {
   int* err;             // EPI_NONE: set to JF_ECOMM (-5) if the cross-rank combine failed
   const double* precond; // EPI_NONE TSQR second pass: P = R1^-1, (n+1)^2 row-major upper triangular
   int32_t use_comm;     // 1: combine across ranks through the mailboxes
-  int32_t fuse_solver;  // reserved (0): the solver step runs in its own kernel (jf_solver.cu)
+  int32_t no_chain;     // debug (JF_DEBUG_NOCHAIN): return the Gram in the alt coordinates (a, 2b, c2)
   CommDev comm;
 };
 

@@ -510,6 +510,7 @@ static int pass_common(int32_t model, const double* y, const double* z, int64_t 
   PassArgs a;
   fill_args(a, sg, m, o);
   a.epilogue = EPI_NONE;
+  a.no_chain = getenv("JF_DEBUG_NOCHAIN") ? 1 : 0;
   if (x_on_device) {
     a.x = x;
   } else {
@@ -678,7 +679,7 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
   PassArgs a;
   fill_args(a, sg, m, o);
   a.epilogue = EPI_FIT;
-  a.fuse_solver = 0;
+  a.no_chain = 0;
   a.partials = c->d_partials;
   a.ticket = c->d_ticket;
   a.out = c->d_out;

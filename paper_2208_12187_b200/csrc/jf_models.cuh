@@ -31,6 +31,10 @@ __device__ __forceinline__ auto param(double v) {
 struct ModelLinear {
   static constexpr int N = 2, D = 1, CONST_COL = 1;
   static constexpr int NEXP = 0;
+  static constexpr int NT = 0;
+  template <class P>
+  __device__ __forceinline__ static const double* tblock(const P&, int) { return nullptr; }
+  __host__ __device__ static constexpr int tbase(int) { return 0; }
   struct Pre {
     double x0, x1;
   };
@@ -46,6 +50,10 @@ struct ModelLinear {
 struct ModelExpDecay {
   static constexpr int N = 3, D = 1, CONST_COL = 2;
   static constexpr int NEXP = 0;
+  static constexpr int NT = 0;
+  template <class P>
+  __device__ __forceinline__ static const double* tblock(const P&, int) { return nullptr; }
+  __host__ __device__ static constexpr int tbase(int) { return 0; }
   struct Pre {
     double a, b, c;
   };
@@ -70,6 +78,10 @@ struct PreGauss1D {
 struct ModelGauss1D {
   static constexpr int N = 4, D = 1, CONST_COL = 3;
   static constexpr int NEXP = 0;
+  static constexpr int NT = 0;
+  template <class P>
+  __device__ __forceinline__ static const double* tblock(const P&, int) { return nullptr; }
+  __host__ __device__ static constexpr int tbase(int) { return 0; }
   template <bool JAC>
   __device__ __forceinline__ static auto prologue(const double* x) {
     const auto s = param<JAC, N, 2>(x[2]);
@@ -90,60 +102,80 @@ struct ModelGauss1D {
 //   a  = cos^2/(2 sx^2) + sin^2/(2 sy^2)
 //   b  = sin(2 th) (1/(4 sy^2) - 1/(4 sx^2)) = sin cos (1/(2 sy^2) - 1/(2 sx^2))
 //   c2 = sin^2/(2 sx^2) + cos^2/(2 sy^2)
-template <class TA, class TB, class TC>
+// Two-stage forward mode (chain rule): per point, the dual numbers carry
+// the partials w.r.t. the quadratic-form coefficients (a, 2b, c2) in place of
+// (sx, sy, th) — simple monomials -dx^2, -dx dy, -dy^2 times A E — and the
+// 3x3 block T = d(a, 2b, c2)/d(sx, sy, th), computed once per pass by dual
+// numbers in the prologue, maps the reduced W^T W back to the paper's
+// parameters: W_x = W_alt T, so W_x^T W_x = T^T (W_alt^T W_alt) T
+// (jf_pass.cuh apply_chain_kvec).  Exact chain rule; fewer fp64 operations
+// and registers per point than carrying (sx, sy, th) through every point.
 struct PreGauss2D {
-  TA a;
-  TB b2;  // 2 b
-  TC c;
-  double A, x0, y0;
+  double A, x0, y0, a, b2, c;  // b2 = 2b
+  double T[9];                 // T[3r + s] = d coef_r / d param_s
 };
 
 // One rotated Gaussian component whose parameters start at index B of x.
 template <int N, int B>
 struct Gauss2DComponent {
+  static constexpr int TBASE = B + 3;  // columns (a, 2b, c2) <-> (sx, sy, th)
   template <bool JAC>
-  __device__ __forceinline__ static auto prologue(const double* x) {
-    const auto sx = param<JAC, N, B + 3>(x[B + 3]);
-    const auto sy = param<JAC, N, B + 4>(x[B + 4]);
-    const auto th = param<JAC, N, B + 5>(x[B + 5]);
+  __device__ __forceinline__ static PreGauss2D prologue(const double* x) {
+    const auto sx = seed<3, 0>(x[B + 3]);
+    const auto sy = seed<3, 1>(x[B + 4]);
+    const auto th = seed<3, 2>(x[B + 5]);
     const auto C = dcos(th);
     const auto S = dsin(th);
     const auto ix = 0.5 / (sx * sx);  // 1/(2 sx^2)
     const auto iy = 0.5 / (sy * sy);  // 1/(2 sy^2)
     const auto CC = C * C;
     const auto SS = S * S;
-    auto a = CC * ix + SS * iy;
-    auto b2 = 2.0 * ((S * C) * (iy - ix));
-    auto c = SS * ix + CC * iy;
-    return PreGauss2D<decltype(a), decltype(b2), decltype(c)>{a, b2, c, x[B + 0], x[B + 1], x[B + 2]};
+    const auto a = CC * ix + SS * iy;
+    const auto b2 = 2.0 * ((S * C) * (iy - ix));
+    const auto c = SS * ix + CC * iy;
+    PreGauss2D p;
+    p.A = x[B + 0];
+    p.x0 = x[B + 1];
+    p.y0 = x[B + 2];
+    p.a = a.v;
+    p.b2 = b2.v;
+    p.c = c.v;
+    static_for<3>([&](auto J) {
+      constexpr int s = decltype(J)::value;
+      p.T[0 + s] = a.template partial<s>();
+      p.T[3 + s] = b2.template partial<s>();
+      p.T[6 + s] = c.template partial<s>();
+    });
+    return p;
   }
-  // A * exp(-q), q = dx (a dx + 2b dy) + c2 dy^2
-  template <bool JAC, class P>
-  __device__ __forceinline__ static auto point(const P& p, double X, double Y) {
+  // A * exp(-q), q = dx (a dx + 2b dy) + c2 dy^2; seeds B+3..B+5 = (a, 2b, c2)
+  template <bool JAC>
+  __device__ __forceinline__ static auto qform(const PreGauss2D& p, double X, double Y) {
     const auto dx = X - param<JAC, N, B + 1>(p.x0);
     const auto dy = Y - param<JAC, N, B + 2>(p.y0);
-    const auto q = dx * (p.a * dx + p.b2 * dy) + p.c * (dy * dy);
-    return param<JAC, N, B + 0>(p.A) * dexp(-q);
+    const auto a = param<JAC, N, B + 3>(p.a);
+    const auto b2 = param<JAC, N, B + 4>(p.b2);
+    const auto c = param<JAC, N, B + 5>(p.c);
+    return dx * (a * dx + b2 * dy) + c * (dy * dy);
+  }
+  template <bool JAC>
+  __device__ __forceinline__ static auto point(const PreGauss2D& p, double X, double Y) {
+    return param<JAC, N, B + 0>(p.A) * dexp(-qform<JAC>(p, X, Y));
   }
   // The same with E = exp(-q(X, Y)) supplied by the caller (row recurrence).
-  template <bool JAC, class P>
-  __device__ __forceinline__ static auto point_e(const P& p, double X, double Y, double E) {
-    const auto dx = X - param<JAC, N, B + 1>(p.x0);
-    const auto dy = Y - param<JAC, N, B + 2>(p.y0);
-    const auto q = dx * (p.a * dx + p.b2 * dy) + p.c * (dy * dy);
-    return param<JAC, N, B + 0>(p.A) * dexp_given(-q, E);
+  template <bool JAC>
+  __device__ __forceinline__ static auto point_e(const PreGauss2D& p, double X, double Y, double E) {
+    return param<JAC, N, B + 0>(p.A) * dexp_given(-qform<JAC>(p, X, Y), E);
   }
-  // Plain-double quantities of the row recurrence: q(X, Y) and the
-  // coefficients a, 2b and the centre.
-  template <class P>
-  __device__ __forceinline__ static double qval(const P& p, double X, double Y) {
+  // Plain-double quantities of the row recurrence.
+  __device__ __forceinline__ static double qval(const PreGauss2D& p, double X, double Y) {
     const double dx = X - p.x0, dy = Y - p.y0;
-    return dx * (value(p.a) * dx + value(p.b2) * dy) + value(p.c) * (dy * dy);
+    return dx * (p.a * dx + p.b2 * dy) + p.c * (dy * dy);
   }
-  template <class P>
-  __device__ __forceinline__ static void rec_coeffs(const P& p, double& a, double& b2, double& x0, double& y0) {
-    a = value(p.a);
-    b2 = value(p.b2);
+  __device__ __forceinline__ static void rec_coeffs(const PreGauss2D& p, double& a, double& b2, double& x0,
+                                                    double& y0) {
+    a = p.a;
+    b2 = p.b2;
     x0 = p.x0;
     y0 = p.y0;
   }
@@ -152,73 +184,73 @@ struct Gauss2DComponent {
 struct ModelGauss2DRot {
   static constexpr int N = 7, D = 2, CONST_COL = 6;
   static constexpr int NEXP = 1;  // exp factors with a quadratic argument (row recurrence)
+  static constexpr int NT = 1;    // chain-rule blocks (see PreGauss2D)
   using G = Gauss2DComponent<N, 0>;
-  template <class P>
   struct Pre {
-    P g;
+    PreGauss2D g;
     double off;
   };
   template <bool JAC>
-  __device__ __forceinline__ static auto prologue(const double* x) {
-    auto g = G::template prologue<JAC>(x);
-    return Pre<decltype(g)>{g, x[6]};
+  __device__ __forceinline__ static Pre prologue(const double* x) {
+    return Pre{G::template prologue<JAC>(x), x[6]};
   }
-  template <bool JAC, class P>
-  __device__ __forceinline__ static auto point(const P& p, double X, double Y) {
+  template <bool JAC>
+  __device__ __forceinline__ static auto point(const Pre& p, double X, double Y) {
     return G::template point<JAC>(p.g, X, Y) + param<JAC, N, 6>(p.off);
   }
-  template <bool JAC, class P>
-  __device__ __forceinline__ static auto point_e(const P& p, double X, double Y, const double (&E)[NEXP]) {
+  template <bool JAC>
+  __device__ __forceinline__ static auto point_e(const Pre& p, double X, double Y, const double (&E)[NEXP]) {
     return G::template point_e<JAC>(p.g, X, Y, E[0]) + param<JAC, N, 6>(p.off);
   }
-  template <int g, class P>
-  __device__ __forceinline__ static double qval(const P& p, double X, double Y) {
+  template <int g>
+  __device__ __forceinline__ static double qval(const Pre& p, double X, double Y) {
     return G::qval(p.g, X, Y);
   }
-  template <int g, class P>
-  __device__ __forceinline__ static void rec_coeffs(const P& p, double& a, double& b2, double& x0, double& y0) {
+  template <int g>
+  __device__ __forceinline__ static void rec_coeffs(const Pre& p, double& a, double& b2, double& x0, double& y0) {
     G::rec_coeffs(p.g, a, b2, x0, y0);
   }
+  __device__ __forceinline__ static const double* tblock(const Pre& p, int) { return p.g.T; }
+  __host__ __device__ static constexpr int tbase(int) { return G::TBASE; }
 };
 
 // ---------------------------------------------------- GAUSS2D_ROT_X2 (n=13)
 struct ModelGauss2DRotX2 {
   static constexpr int N = 13, D = 2, CONST_COL = 12;
   static constexpr int NEXP = 2;
+  static constexpr int NT = 2;
   using G1 = Gauss2DComponent<N, 0>;
   using G2 = Gauss2DComponent<N, 6>;
-  template <class P1, class P2>
   struct Pre {
-    P1 g1;
-    P2 g2;
+    PreGauss2D g1, g2;
     double off;
   };
   template <bool JAC>
-  __device__ __forceinline__ static auto prologue(const double* x) {
-    auto g1 = G1::template prologue<JAC>(x);
-    auto g2 = G2::template prologue<JAC>(x);
-    return Pre<decltype(g1), decltype(g2)>{g1, g2, x[12]};
+  __device__ __forceinline__ static Pre prologue(const double* x) {
+    return Pre{G1::template prologue<JAC>(x), G2::template prologue<JAC>(x), x[12]};
   }
-  template <bool JAC, class P>
-  __device__ __forceinline__ static auto point(const P& p, double X, double Y) {
+  template <bool JAC>
+  __device__ __forceinline__ static auto point(const Pre& p, double X, double Y) {
     return (G1::template point<JAC>(p.g1, X, Y) + G2::template point<JAC>(p.g2, X, Y)) +
            param<JAC, N, 12>(p.off);
   }
-  template <bool JAC, class P>
-  __device__ __forceinline__ static auto point_e(const P& p, double X, double Y, const double (&E)[NEXP]) {
+  template <bool JAC>
+  __device__ __forceinline__ static auto point_e(const Pre& p, double X, double Y, const double (&E)[NEXP]) {
     return (G1::template point_e<JAC>(p.g1, X, Y, E[0]) + G2::template point_e<JAC>(p.g2, X, Y, E[1])) +
            param<JAC, N, 12>(p.off);
   }
-  template <int g, class P>
-  __device__ __forceinline__ static double qval(const P& p, double X, double Y) {
+  template <int g>
+  __device__ __forceinline__ static double qval(const Pre& p, double X, double Y) {
     if constexpr (g == 0) return G1::qval(p.g1, X, Y);
     else return G2::qval(p.g2, X, Y);
   }
-  template <int g, class P>
-  __device__ __forceinline__ static void rec_coeffs(const P& p, double& a, double& b2, double& x0, double& y0) {
+  template <int g>
+  __device__ __forceinline__ static void rec_coeffs(const Pre& p, double& a, double& b2, double& x0, double& y0) {
     if constexpr (g == 0) G1::rec_coeffs(p.g1, a, b2, x0, y0);
     else G2::rec_coeffs(p.g2, a, b2, x0, y0);
   }
+  __device__ __forceinline__ static const double* tblock(const Pre& p, int g) { return g == 0 ? p.g1.T : p.g2.T; }
+  __host__ __device__ static constexpr int tbase(int g) { return g == 0 ? G1::TBASE : G2::TBASE; }
 };
 
 }  // namespace jf

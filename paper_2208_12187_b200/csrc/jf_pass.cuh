@@ -84,7 +84,18 @@ __device__ __forceinline__ void accumulate(double (&acc)[Part<Model, JAC, RL, RH
     if constexpr (PREC) {
       // TSQR (CholeskyQR2) second pass: the row of W P, P = R1^-1 upper
       // triangular ((n+1) x (n+1), shared memory), so the accumulated Gram is
-      // P^T (W^T W) P and its Cholesky factor R2 gives R = R2 R1
+      // P^T (W^T W) P and its Cholesky factor R2 gives R = R2 R1.  The row is
+      // first mapped to the paper's parameters by the chain-rule blocks T
+      // (jf_models.cuh PreGauss2D), stored after P.
+#pragma unroll
+      for (int g = 0; g < Model::NT; ++g) {
+        constexpr int N1 = N + 1;
+        const int b = Model::tbase(g);
+        const double* T = prec + N1 * N1 + 9 * g;
+        const double u0 = w[b], u1 = w[b + 1], u2 = w[b + 2];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) w[b + q] = fma(u0, T[q], fma(u1, T[3 + q], u2 * T[6 + q]));
+      }
       double u[N + 1];
 #pragma unroll
       for (int k = 0; k <= N; ++k) {
@@ -157,6 +168,51 @@ __device__ __forceinline__ void block_partial_part(double (&acc)[Part<Model, JAC
     for (int w = 0; w < NW; ++w) s += red[w][k];
     part[(size_t)blockIdx.x * (KT + 1) + k] = s;
   }
+}
+
+// Map the reduced W_alt^T W_alt (columns (a, 2b, c2) of each Gaussian) to the
+// paper's parameters: T^T M T with the 3x3 chain-rule blocks of the model
+// (jf_models.cuh PreGauss2D).  Once per pass on the K-vector, one slot per
+// thread:  M'[j][k] = sum_{r in S(j), r' in S(k)} T(r, j) T(r', k) M[r][r'],
+// S(j) = {j} for a column outside every block, else the block's 3 columns.
+template <class Model>
+__device__ __forceinline__ int chain_block(int j) {
+#pragma unroll
+  for (int g = 0; g < Model::NT; ++g)
+    if (j >= Model::tbase(g) && j < Model::tbase(g) + 3) return g;
+  return -1;
+}
+template <class Model, int TPB, class Pre>
+__device__ __forceinline__ void apply_chain_kvec(const Pre& pre, double* vec, double* tmp /* KT doubles */) {
+  constexpr int N = Model::N, N1 = N + 1, KT = tri_count(N);
+  for (int t = threadIdx.x; t < KT; t += TPB) {
+    int j = 0, rem = t;
+    while (rem >= N1 - j) {
+      rem -= N1 - j;
+      ++j;
+    }
+    const int k = j + rem;
+    const int gj = chain_block<Model>(j), gk = chain_block<Model>(k);
+    const int nj = gj < 0 ? 1 : 3, nk = gk < 0 ? 1 : 3;
+    const int bj = gj < 0 ? j : Model::tbase(gj), bk = gk < 0 ? k : Model::tbase(gk);
+    const double* Tj = gj < 0 ? nullptr : Model::tblock(pre, gj);
+    const double* Tk = gk < 0 ? nullptr : Model::tblock(pre, gk);
+    double s = 0.0;
+    for (int r = 0; r < nj; ++r) {
+      const double cj = gj < 0 ? 1.0 : Tj[3 * r + (j - bj)];
+      double u = 0.0;
+      for (int q = 0; q < nk; ++q) {
+        const double ck = gk < 0 ? 1.0 : Tk[3 * q + (k - bk)];
+        const int x = bj + r, y = bk + q;
+        u = fma(ck, vec[x <= y ? tri_slot(N, x, y) : tri_slot(N, y, x)], u);
+      }
+      s = fma(cj, u, s);
+    }
+    tmp[t] = s;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < KT; t += TPB) vec[t] = tmp[t];
+  __syncthreads();
 }
 
 // Last-block deterministic sum over the grid's partials; result in out[0..KS).
@@ -520,11 +576,16 @@ __global__ void __launch_bounds__(TPB, MINB)
   const auto pre = Model::template prologue<JAC>(xv);
 
   // TSQR second pass: the preconditioner P = R1^-1 into shared memory
-  __shared__ double prec_s[PREC ? (Model::N + 1) * (Model::N + 1) : 1];
+  __shared__ double prec_s[PREC ? (Model::N + 1) * (Model::N + 1) + 9 * Model::NT + 1 : 1];
   const double* prec = nullptr;
   if constexpr (PREC) {
+    constexpr int N1 = Model::N + 1;
     const double* src = (a.epilogue == EPI_FIT) ? st->prec : a.precond;
-    for (int k = threadIdx.x; k < (Model::N + 1) * (Model::N + 1); k += TPB) prec_s[k] = src[k];
+    for (int k = threadIdx.x; k < N1 * N1; k += TPB) prec_s[k] = src[k];
+    if (threadIdx.x == 0) {
+      for (int g = 0; g < Model::NT; ++g)
+        for (int q = 0; q < 9; ++q) prec_s[N1 * N1 + 9 * g + q] = Model::tblock(pre, g)[q];
+    }
     __syncthreads();
     prec = prec_s;
   }
@@ -553,6 +614,9 @@ __global__ void __launch_bounds__(TPB, MINB)
   __threadfence();
   grid_combine<KS, TPB>(a.partials, gridDim.x, vec, scratch);
   if (threadIdx.x == 0) *a.ticket = 0u;  // ready for the next launch
+  if constexpr (JAC && Model::NT > 0 && !PREC) {
+    if (!a.no_chain) apply_chain_kvec<Model, TPB>(pre, vec, scratch);
+  }
 
   if (a.use_comm) {
     const unsigned long long epoch = (a.epilogue == EPI_FIT) ? (st->comm_epoch + 1) : (a.comm.epoch + 1);
@@ -624,6 +688,10 @@ __global__ void __launch_bounds__(256, 1) fit_small_kernel(const PassArgs* __res
     const auto pre = Model::template prologue<true>(xv);
     run_part<Model, true, COORD, WGT, P, TPB, 0, NP1, false>(a, pre, 0, 1, red, kvec, nullptr);
     __syncthreads();
+    if constexpr (Model::NT > 0) {
+      __shared__ double ctmp[KT];
+      apply_chain_kvec<Model, TPB>(pre, kvec, ctmp);
+    }
     if (threadIdx.x < 32) solver_step<Model::N>(&st, S, kvec, true);
   }
   __syncthreads();

@@ -147,3 +147,37 @@ def test_full_size_C5_pass_matches_oracle_on_row_band():
     X, Y = dg.grid_coords(W, r1 - r0, r0)
     ref = orp.jpass(pr.model, (X, Y), z, pr.p0)
     check_pass(jf.jpass(pr.model, torch.as_tensor(z).cuda(), pr.p0, grid=(W, r1 - r0, r0)), ref)
+
+
+def _alt_coefs(sx, sy, th):
+    """(a, 2b, c2) of the rotated Gaussian's quadratic form."""
+    C, S = math.cos(th), math.sin(th)
+    return (C * C / (2 * sx * sx) + S * S / (2 * sy * sy),
+            2 * S * C * (1 / (2 * sy * sy) - 1 / (2 * sx * sx)),
+            S * S / (2 * sx * sx) + C * C / (2 * sy * sy))
+
+
+@pytest.mark.parametrize("name,make", [c for c in CASES if c[0].startswith("gauss2d")],
+                         ids=[c[0] for c in CASES if c[0].startswith("gauss2d")])
+def test_jpass_first_stage_alt_coordinates(name, make, monkeypatch):
+    """Stage one of the two-stage chain rule (jf_models.cuh PreGauss2D) alone:
+    with the map T^T M T switched off (JF_DEBUG_NOCHAIN), the pass returns
+    the Gram of [J_alt | r] whose shape columns are d h / d(a, 2b, c2) =
+    -A E (dx^2, dx dy, dy^2) — written out here from the quadratic form, so a
+    wrong stage-two map cannot hide behind a compensating stage-one error."""
+    pr = make()
+    X, Y = pr.coords()
+    x = pr.p0
+    cols = []
+    for B in range(0, pr.n - 1, 6):
+        A, x0, y0 = x[B:B + 3]
+        a, b2, c2 = _alt_coefs(*x[B + 3:B + 6])
+        dx, dy = X - x0, Y - y0
+        E = np.exp(-(a * dx * dx + b2 * dx * dy + c2 * dy * dy))
+        AE = A * E
+        cols += [E, AE * (2 * a * dx + b2 * dy), AE * (b2 * dx + 2 * c2 * dy), -AE * dx * dx, -AE * dx * dy, -AE * dy * dy]
+    Ja = np.stack(cols + [np.ones_like(X)], 1)
+    r = dg.render(pr.model, (X, Y), x) - pr.z
+    ref = (0.5 * float(r @ r), Ja.T @ r, Ja.T @ Ja, 0)
+    monkeypatch.setenv("JF_DEBUG_NOCHAIN", "1")
+    check_pass(jf.jpass(pr.model, pr.z, x, grid=pr.grid), ref, tol=1e-9)
