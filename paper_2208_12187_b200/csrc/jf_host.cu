@@ -178,7 +178,7 @@ int grid_for(Ctx& c, KernelFn f, int tpb, int64_t m) {
 // The two pass kernels a call uses, with their launch shapes.
 struct PassPair {
   KernelFn j = nullptr, r = nullptr, jp = nullptr;
-  int jtpb = 256, rtpb = 256, jgrid = 1, rgrid = 1;
+  int jtpb = 256, rtpb = 256, jptpb = 256, jgrid = 1, rgrid = 1, jpgrid = 1;
 };
 
 PassPair select_pass(Ctx& c, const Kernels& k, bool weighted, int64_t m) {
@@ -188,8 +188,13 @@ PassPair select_pass(Ctx& c, const Kernels& k, bool weighted, int64_t m) {
   p.jp = weighted ? k.jkpw : k.jkp;
   p.jtpb = k.jtpb;
   p.rtpb = k.rtpb;
+  p.jptpb = k.jptpb;
   p.jgrid = grid_for(c, p.j, p.jtpb, m);
-  if (k.jsplit) p.jgrid = p.jgrid < 2 ? 2 : p.jgrid + (p.jgrid & 1);  // two equal halves
+  p.jpgrid = p.jp ? grid_for(c, p.jp, p.jptpb, m) : 1;
+  if (k.jsplit) {  // two equal halves
+    p.jgrid = p.jgrid < 2 ? 2 : p.jgrid + (p.jgrid & 1);
+    p.jpgrid = p.jpgrid < 2 ? 2 : p.jpgrid + (p.jpgrid & 1);
+  }
   p.rgrid = grid_for(c, p.r, p.rtpb, m);
   return p;
 }
@@ -360,7 +365,9 @@ void active_mask_host(const double* x, const double* lb, const double* ub, int n
 int launch_pass(const PassPair& k, bool jac, cudaStream_t s, PassArgs* d_args, FitState* d_state,
                 bool prec = false) {
   KernelFn f = jac ? (prec ? k.jp : k.j) : k.r;
-  f<<<jac ? k.jgrid : k.rgrid, jac ? k.jtpb : k.rtpb, 0, s>>>(d_args, d_state, (cudaGraphConditionalHandle)0, 0);
+  const int grid = jac ? (prec ? k.jpgrid : k.jgrid) : k.rgrid;
+  const int tpb = jac ? (prec ? k.jptpb : k.jtpb) : k.rtpb;
+  f<<<grid, tpb, 0, s>>>(d_args, d_state, (cudaGraphConditionalHandle)0, 0);
   CK(cudaGetLastError());
   return 0;
 }
@@ -397,11 +404,15 @@ int build_graph(Ctx& c, const PassPair& k, int policy, bool qr, cudaGraphExec_t*
   // solver nodes depend programmatically on the pass before them (PDL): the
   // solver kernel is scheduled while the pass drains and waits in
   // griddepcontrol.wait for its results, hiding the launch latency
+  // Every kernel after the first depends programmatically on the one before
+  // (PDL): it is scheduled while its predecessor runs and waits in
+  // griddepcontrol.wait for the predecessor's completion and memory.
   cudaGraphNode_t prev = nullptr;
   bool prev_is_pass = false;
   auto add = [&](const cudaKernelNodeParams& p, bool is_solver) -> int {
     cudaGraphNode_t nd;
-    if (prev && is_solver && prev_is_pass) {
+    (void)prev_is_pass;
+    if (prev) {
       cudaGraphNodeParams np = {};
       np.type = cudaGraphNodeTypeKernel;
       np.kernel.func = p.func;
@@ -422,24 +433,31 @@ int build_graph(Ctx& c, const PassPair& k, int policy, bool qr, cudaGraphExec_t*
     return 0;
   };
   kp.kernelParams = pargs;
-  if (policy == JF_POLICY_CONSERVATIVE) {
-    kp.func = (void*)k.r;
-    kp.gridDim = dim3(k.rgrid);
-    kp.blockDim = dim3(k.rtpb);
-    if (int e = add(kp, false)) return e;
-    if (int e = add(sp, true)) return e;
-  }
-  if (qr) {  // TSQR: the preconditioned second pass runs when the phase is PH_QR2
-    kp.func = (void*)k.jp;
+  // U copies of the iteration per trip of the WHILE loop: the conditional
+  // node's per-trip overhead is paid once per U iterations; copies after the
+  // fit ended find nothing to do (phase DONE) and return at once.
+  int unroll = 2;
+  if (const char* e = getenv("JF_GRAPH_UNROLL")) unroll = atoi(e) < 1 ? 1 : atoi(e);
+  for (int u = 0; u < unroll; ++u) {
+    if (policy == JF_POLICY_CONSERVATIVE) {
+      kp.func = (void*)k.r;
+      kp.gridDim = dim3(k.rgrid);
+      kp.blockDim = dim3(k.rtpb);
+      if (int e = add(kp, false)) return e;
+      if (int e = add(sp, true)) return e;
+    }
+    if (qr) {  // TSQR: the preconditioned second pass runs when the phase is PH_QR2
+      kp.func = (void*)k.jp;
+      kp.gridDim = dim3(k.jpgrid);
+      kp.blockDim = dim3(k.jptpb);
+      if (int e = add(kp, false)) return e;
+    }
+    kp.func = (void*)k.j;
     kp.gridDim = dim3(k.jgrid);
     kp.blockDim = dim3(k.jtpb);
     if (int e = add(kp, false)) return e;
+    if (int e = add(sp, true)) return e;
   }
-  kp.func = (void*)k.j;
-  kp.gridDim = dim3(k.jgrid);
-  kp.blockDim = dim3(k.jtpb);
-  if (int e = add(kp, false)) return e;
-  if (int e = add(sp, true)) return e;
   CK(cudaGraphInstantiate(out, g, 0));
   cudaGraphDestroy(g);
   return 0;

@@ -13,6 +13,7 @@ static Kernels make() {
   k.jkp = pass_kernel<ModelExpDecay, true, C, false, PassCfg<ModelExpDecay, true>::P, PassCfg<ModelExpDecay, true>::TPB, PassCfg<ModelExpDecay, true>::MINB, true>;
   k.jkpw = pass_kernel<ModelExpDecay, true, C, true, PassCfg<ModelExpDecay, true>::P, PassCfg<ModelExpDecay, true>::TPB, PassCfg<ModelExpDecay, true>::MINB, true>;
   k.jtpb = PassCfg<ModelExpDecay, true>::TPB;
+  k.jptpb = PassCfg<ModelExpDecay, true>::TPB;
   k.jsplit = PassCfg<ModelExpDecay, true>::SPLIT;
   k.small = fit_small_kernel<ModelExpDecay, C, false>;
   k.smallw = fit_small_kernel<ModelExpDecay, C, true>;

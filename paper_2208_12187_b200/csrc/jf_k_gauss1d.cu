@@ -13,6 +13,7 @@ static Kernels make() {
   k.jkp = pass_kernel<ModelGauss1D, true, C, false, PassCfg<ModelGauss1D, true>::P, PassCfg<ModelGauss1D, true>::TPB, PassCfg<ModelGauss1D, true>::MINB, true>;
   k.jkpw = pass_kernel<ModelGauss1D, true, C, true, PassCfg<ModelGauss1D, true>::P, PassCfg<ModelGauss1D, true>::TPB, PassCfg<ModelGauss1D, true>::MINB, true>;
   k.jtpb = PassCfg<ModelGauss1D, true>::TPB;
+  k.jptpb = PassCfg<ModelGauss1D, true>::TPB;
   k.jsplit = PassCfg<ModelGauss1D, true>::SPLIT;
   k.small = fit_small_kernel<ModelGauss1D, C, false>;
   k.smallw = fit_small_kernel<ModelGauss1D, C, true>;

@@ -2,7 +2,7 @@
 #include <cstdlib>
 
 #include "jf_kernels.h"
-#include "jf_pass.cuh"
+#include "jf_moment.cuh"
 
 namespace jf {
 template <int C>
@@ -15,6 +15,7 @@ static Kernels make() {
   k.jkp = pass_kernel<ModelGauss2DRot, true, C, false, PassCfg<ModelGauss2DRot, true>::P, PassCfg<ModelGauss2DRot, true>::TPB, PassCfg<ModelGauss2DRot, true>::MINB, true>;
   k.jkpw = pass_kernel<ModelGauss2DRot, true, C, true, PassCfg<ModelGauss2DRot, true>::P, PassCfg<ModelGauss2DRot, true>::TPB, PassCfg<ModelGauss2DRot, true>::MINB, true>;
   k.jtpb = PassCfg<ModelGauss2DRot, true>::TPB;
+  k.jptpb = PassCfg<ModelGauss2DRot, true>::TPB;
   k.jsplit = PassCfg<ModelGauss2DRot, true>::SPLIT;
   k.small = fit_small_kernel<ModelGauss2DRot, C, false>;
   k.smallw = fit_small_kernel<ModelGauss2DRot, C, true>;
@@ -25,11 +26,17 @@ Kernels kernels_gauss2d(int coord) {
   Kernels k = coord == COORD_EXPLICIT ? make<COORD_EXPLICIT>() : make<COORD_GRID>();
   // development aid: alternative launch shapes of the grid J-pass (JF_JVARIANT=1..3)
   if (coord == COORD_GRID) {
+    // unweighted implicit grid: the moment-form J-pass (jf_moment.cuh)
+    k.jk = moment_pass_kernel<16, 128, 3>;
+    k.jtpb = 128;
     if (const char* v = getenv("JF_JVARIANT")) {
       const int var = atoi(v);
-      if (var == 1) { k.jk = pass_kernel<ModelGauss2DRot, true, COORD_GRID, false, 4, 256, 1>; k.jtpb = 256; }
-      if (var == 2) { k.jk = pass_kernel<ModelGauss2DRot, true, COORD_GRID, false, 3, 256, 1>; k.jtpb = 256; }
-      if (var == 3) { k.jk = pass_kernel<ModelGauss2DRot, true, COORD_GRID, false, 1, 256, 2>; k.jtpb = 256; }
+      if (var == 9) { k.jk = pass_kernel<ModelGauss2DRot, true, COORD_GRID, false>; k.jtpb = 256; }  // dual-number kernel
+      if (var == 11) { k.jk = moment_pass_kernel<8, 128, 3>; }
+      if (var == 12) { k.jk = moment_pass_kernel<8, 128, 4>; }
+      if (var == 13) { k.jk = moment_pass_kernel<16, 128, 4>; }
+      if (var == 14) { k.jk = moment_pass_kernel<8, 128, 5>; }
+      if (var == 15) { k.jk = moment_pass_kernel<4, 128, 4>; }
     }
   }
   return k;

@@ -13,6 +13,7 @@ static Kernels make() {
   k.jkp = pass_kernel<ModelGauss2DRotX2, true, C, false, PassCfg<ModelGauss2DRotX2, true>::P, PassCfg<ModelGauss2DRotX2, true>::TPB, PassCfg<ModelGauss2DRotX2, true>::MINB, true>;
   k.jkpw = pass_kernel<ModelGauss2DRotX2, true, C, true, PassCfg<ModelGauss2DRotX2, true>::P, PassCfg<ModelGauss2DRotX2, true>::TPB, PassCfg<ModelGauss2DRotX2, true>::MINB, true>;
   k.jtpb = PassCfg<ModelGauss2DRotX2, true>::TPB;
+  k.jptpb = PassCfg<ModelGauss2DRotX2, true>::TPB;
   k.jsplit = PassCfg<ModelGauss2DRotX2, true>::SPLIT;
   k.small = fit_small_kernel<ModelGauss2DRotX2, C, false>;
   k.smallw = fit_small_kernel<ModelGauss2DRotX2, C, true>;

@@ -13,6 +13,7 @@ static Kernels make() {
   k.jkp = pass_kernel<ModelLinear, true, C, false, PassCfg<ModelLinear, true>::P, PassCfg<ModelLinear, true>::TPB, PassCfg<ModelLinear, true>::MINB, true>;
   k.jkpw = pass_kernel<ModelLinear, true, C, true, PassCfg<ModelLinear, true>::P, PassCfg<ModelLinear, true>::TPB, PassCfg<ModelLinear, true>::MINB, true>;
   k.jtpb = PassCfg<ModelLinear, true>::TPB;
+  k.jptpb = PassCfg<ModelLinear, true>::TPB;
   k.jsplit = PassCfg<ModelLinear, true>::SPLIT;
   k.small = fit_small_kernel<ModelLinear, C, false>;
   k.smallw = fit_small_kernel<ModelLinear, C, true>;

@@ -1,0 +1,327 @@
+// jf_moment.cuh — moment-form J-pass for the rotated 2D Gaussian (n = 7) on
+// an implicit pixel grid, unweighted.
+//
+// Same output as pass_kernel<ModelGauss2DRot, JAC=true, COORD_GRID> — the
+// upper triangle of [J | r]^T [J | r] (Eqs. 2, 4, 5: cost, J^T r, J^T J) —
+// computed with fewer fp64 operations per point by using the model's
+// structure.  In the alt coordinates (a, 2b, c2) of jf_models.cuh PreGauss2D
+// every Jacobian column of the Gaussian is u = exp(-q) times a polynomial of
+// degree <= 2 in (dx, dy):
+//   J_A = u,  J_x0 = A u (2a dx + 2b dy),  J_y0 = A u (2b dx + 2 c2 dy),
+//   J_a = -A u dx^2,  J_2b = -A u dx dy,  J_c2 = -A u dy^2,  J_off = 1,
+// so every entry of the triangle is a fixed linear combination of the moments
+//   M2[p][q] = sum u^2 dx^p dy^q  (p + q <= 4),   M1[p][q] = sum u dx^p dy^q,
+//   MR[p][q] = sum u r dx^p dy^q  (p + q <= 2),   sum r,  sum r^2,  m.
+// Exact algebra (the same sums, regrouped); the map moments -> triangle runs
+// once per pass in the last block, then the chain-rule blocks T map the alt
+// columns to (sx, sy, th) as for the dual-number kernel.
+//
+// Per point: u from the row recurrence (2 DMUL), r = A u + off - z (2), the
+// moment updates along the row (dx powers; 8 + 4 + 5), sum r and sum r^2 (2),
+// dx (1): 25 fp64 operations against ~60 for the rank-1 update of the
+// 36-slot triangle.  The dy powers are folded in once per image row a lane
+// visits: each warp walks a contiguous range of warp-chunks (32 L pixels of
+// one row), so a row's chunks are consecutive.
+#pragma once
+
+#include "jf_pass.cuh"
+
+#ifndef JF_TAIL_STAMPS
+#define JF_TAIL_STAMPS 0
+#endif
+
+namespace jf {
+
+// Moment vector layout: M2 (15) | M1 (6) | MR (6) | sum r | sum r^2 | bad
+struct MomLayout {
+  static constexpr int N2 = 15, N1 = 6;
+  static constexpr int O2 = 0, O1 = 15, OR = 21, OSR = 27, OSRR = 28, NV = 29, KS = 30;
+};
+// index of dx^p dy^q among the monomials of degree <= D (q-major)
+__host__ __device__ constexpr int mono(int D, int p, int q) { return (D + 1) * q - q * (q - 1) / 2 + p; }
+
+// The moment vector -> the K-vector of [J_alt | r] (slot (j, k), j <= k <= 7).
+// Thread t < KT computes slot t.  Column j of the Gaussian block is
+// J_j = f_j u psi_j (f_0 = 1, f_j = A else) with psi_j = sum of at most two
+// monomials c dx^p dy^q, from the formulas above.
+struct Poly2 {
+  double c[2];
+  int p[2], q[2];
+};
+__device__ __forceinline__ Poly2 psi(const PreGauss2D& g, int j) {
+  switch (j) {
+    case 0: return {{1.0, 0.0}, {0, 0}, {0, 0}};
+    case 1: return {{2.0 * g.a, g.b2}, {1, 0}, {0, 1}};
+    case 2: return {{g.b2, 2.0 * g.c}, {1, 0}, {0, 1}};
+    case 3: return {{-1.0, 0.0}, {2, 0}, {0, 0}};
+    case 4: return {{-1.0, 0.0}, {1, 0}, {1, 0}};
+    default: return {{-1.0, 0.0}, {0, 0}, {2, 0}};
+  }
+}
+__device__ __forceinline__ void moments_to_kvec(const PreGauss2D& g, double m_pts, const double* mom, double* vec) {
+  constexpr int N = 7, KT = tri_count(N);
+  for (int t = threadIdx.x; t < KT; t += blockDim.x) {
+    int j = 0, rem = t;
+    while (rem >= N + 1 - j) {
+      rem -= N + 1 - j;
+      ++j;
+    }
+    const int k = j + rem;
+    double v;
+    if (k <= 5) {
+      const Poly2 a = psi(g, j), b = psi(g, k);
+      v = 0.0;
+#pragma unroll
+      for (int s = 0; s < 2; ++s)
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+          v = fma(a.c[s] * b.c[u], mom[MomLayout::O2 + mono(4, a.p[s] + b.p[u], a.q[s] + b.q[u])], v);
+      v *= (j == 0 ? 1.0 : g.A) * g.A;  // k >= 1 here unless j = k = 0
+      if (k == 0) v = mom[MomLayout::O2 + mono(4, 0, 0)];
+    } else if (j <= 5) {  // k = 6 (offset column) or k = 7 (residual)
+      const int base = (k == 6) ? MomLayout::O1 : MomLayout::OR;
+      const Poly2 a = psi(g, j);
+      v = 0.0;
+#pragma unroll
+      for (int s = 0; s < 2; ++s) v = fma(a.c[s], mom[base + mono(2, a.p[s], a.q[s])], v);
+      v *= (j == 0 ? 1.0 : g.A);
+    } else if (j == 6) {
+      v = (k == 6) ? m_pts : mom[MomLayout::OSR];
+    } else {
+      v = mom[MomLayout::OSRR];
+    }
+    vec[t] = v;
+  }
+}
+
+// Last block: combine the grid's moment vectors, map them to the K-vector
+// (alt coordinates), apply the chain rule, hand over (pass_tail).  Out of
+// line so the prologue's 3x3 blocks never occupy the main loop's registers.
+template <int TPB>
+__device__ __noinline__ void moment_finish(const PassArgs& a, FitState* __restrict__ st, const double* xs,
+                                           double* mom, double* vec, double* scratch,
+                                           cudaGraphConditionalHandle cond, int use_cond) {
+  using Model = ModelGauss2DRot;
+  constexpr int N = Model::N, KT = tri_count(N), KS = KT + 1;
+  auto stamp = [&]() {
+    if (JF_TAIL_STAMPS && threadIdx.x == 0 && a.epilogue == EPI_FIT) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      const int k = atomicAdd(&st->tl_n, 1);
+      if (k < 64) st->tl[k] = t;
+    }
+  };
+  stamp();
+  grid_combine<MomLayout::KS, TPB>(a.partials, gridDim.x, mom, scratch);
+  if (threadIdx.x == 0) *a.ticket = 0u;  // ready for the next launch
+  stamp();
+  double xv[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) xv[j] = xs[j];
+  const auto pre = Model::template prologue<true>(xv);
+  stamp();
+  moments_to_kvec(pre.g, (double)a.m, mom, vec);
+  if (threadIdx.x == 0) vec[KT] = mom[MomLayout::NV];  // non-finite count
+  __syncthreads();
+  stamp();
+  if (!a.no_chain) apply_chain_kvec<Model, TPB>(pre, vec, scratch);
+  stamp();
+  pass_tail<KS, TPB, true>(a, st, vec, cond, use_cond);
+}
+
+template <int L, int TPB, int MINB>
+__global__ void __launch_bounds__(TPB, MINB)
+    moment_pass_kernel(const PassArgs* __restrict__ pa, FitState* __restrict__ st, cudaGraphConditionalHandle cond,
+                       int use_cond) {
+  using Model = ModelGauss2DRot;
+  constexpr int N = Model::N, KT = tri_count(N), KS = KT + 1;
+  constexpr int NV = MomLayout::NV;
+  constexpr int CW = 32 * L;
+  constexpr double D = 32.0;
+  const PassArgs& a = *pa;
+  if (!pass_begin<true, false>(a, st)) return;
+  const double* xs = (a.epilogue == EPI_FIT) ? st->x_eval : a.x;
+  double A, off, ga, gb2, gc, x0, y0;
+  {
+    double xv[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) xv[j] = xs[j];
+    const auto pre = Model::template prologue<false>(xv);
+    A = pre.g.A, off = pre.off, ga = pre.g.a, gb2 = pre.g.b2, gc = pre.g.c, x0 = pre.g.x0, y0 = pre.g.y0;
+  }
+
+  // per-thread moments with dy folded in: shared memory, one column per
+  // thread (updated once per image row a lane visits; keeps the registers for
+  // the per-point work and more resident warps)
+  __shared__ double smom[MomLayout::OSR][TPB];
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int i = 0; i < MomLayout::OSR; ++i) smom[i][tid] = 0.0;
+  double sr = 0.0, srr = 0.0;
+  double P[5], Q[3], R[3];
+#pragma unroll
+  for (int i = 0; i < 5; ++i) P[i] = 0.0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) Q[i] = R[i] = 0.0;
+  int bad = 0;
+
+  auto fold = [&](double dy) {  // row moments x dy^q into the thread's moments
+    double dq[5];
+    dq[0] = 1.0;
+    dq[1] = dy;
+    dq[2] = dy * dy;
+    dq[3] = dq[2] * dy;
+    dq[4] = dq[2] * dq[2];
+#pragma unroll
+    for (int q = 0; q <= 4; ++q)
+#pragma unroll
+      for (int p = 0; p + q <= 4; ++p) {
+        double& m2 = smom[MomLayout::O2 + mono(4, p, q)][tid];
+        m2 = fma(P[p], dq[q], m2);
+      }
+#pragma unroll
+    for (int q = 0; q <= 2; ++q)
+#pragma unroll
+      for (int p = 0; p + q <= 2; ++p) {
+        double& m1 = smom[MomLayout::O1 + mono(2, p, q)][tid];
+        m1 = fma(Q[p], dq[q], m1);
+        double& mr = smom[MomLayout::OR + mono(2, p, q)][tid];
+        mr = fma(R[p], dq[q], mr);
+      }
+#pragma unroll
+    for (int i = 0; i < 5; ++i) P[i] = 0.0;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) Q[i] = R[i] = 0.0;
+  };
+  // one point: u = exp(-q), dx, data z
+  auto point = [&](double u, double dx, double z) {
+    const double r = fma(A, u, off) - z;  // Eq. 1: r = h - z
+    bad += isfinite(r) ? 0 : 1;
+    const double u2 = u * u;
+    P[0] += u2;
+    P[1] = fma(u2, dx, P[1]);
+    const double t1 = u2 * dx;
+    P[2] = fma(t1, dx, P[2]);
+    const double t2 = t1 * dx;
+    P[3] = fma(t2, dx, P[3]);
+    const double t3 = t2 * dx;
+    P[4] = fma(t3, dx, P[4]);
+    Q[0] += u;
+    Q[1] = fma(u, dx, Q[1]);
+    const double v1 = u * dx;
+    Q[2] = fma(v1, dx, Q[2]);
+    const double ur = u * r;
+    R[0] += ur;
+    R[1] = fma(ur, dx, R[1]);
+    const double w1 = ur * dx;
+    R[2] = fma(w1, dx, R[2]);
+    sr += r;
+    srr = fma(r, r, srr);
+  };
+
+  const int lane = threadIdx.x & 31;
+  const int W = (int)a.W;
+  const int64_t H = a.m / a.W;
+  const int cpr = (W + CW - 1) / CW;
+  const int64_t nch = H * (int64_t)cpr;
+  const int64_t nwt = (int64_t)gridDim.x * (TPB / 32);
+  const int64_t gw = (int64_t)blockIdx.x * (TPB / 32) + (threadIdx.x >> 5);
+  const int64_t c_begin = gw * nch / nwt, c_end = (gw + 1) * nch / nwt;
+  const double rho = exp(-2.0 * ga * D * D);
+  const double* __restrict__ z = a.z;
+  double zn[L];
+  // chunk ch = row * cpr + cc; row and cc are advanced incrementally (no
+  // 64-bit division in the loop)
+  int64_t lrow = c_begin / cpr;  // position of the next chunk to load
+  int lcc = (int)(c_begin - lrow * cpr);
+  auto load = [&]() {
+    const int col = lcc * CW + lane;
+    const double* zp = z + lrow * a.W + col;
+#pragma unroll
+    for (int k = 0; k < L; ++k) zn[k] = (col + 32 * k < W) ? __ldcs(zp + 32 * k) : 0.0;
+    if (++lcc == cpr) {
+      lcc = 0;
+      ++lrow;
+    }
+  };
+  if (c_begin < c_end) load();
+  int64_t cur_row = c_begin / cpr;
+  int cc = (int)(c_begin - cur_row * cpr) - 1;  // chunk column of the current chunk (advanced below)
+  int64_t row = cur_row;
+  for (int64_t ch = c_begin; ch < c_end; ++ch) {
+    double zc[L];
+#pragma unroll
+    for (int k = 0; k < L; ++k) zc[k] = zn[k];
+    if (ch + 1 < c_end) load();  // prefetch the next chunk
+    if (++cc == cpr) {
+      cc = 0;
+      ++row;
+    }
+    if (row != cur_row) {  // warp-uniform
+      fold((double)(cur_row + a.row0) - y0);
+      cur_row = row;
+    }
+    const int c0 = cc * CW;
+    const double dy = (double)(row + a.row0) - y0;
+    const double dx0 = (double)(c0 + lane) - x0;
+    const double q0 = dx0 * (ga * dx0 + gb2 * dy) + gc * (dy * dy);
+    const double argR = D * (2.0 * ga * dx0 + gb2 * dy) + ga * D * D;
+    const bool ok = fabs(q0) < 600.0 && fabs(argR) < 300.0 && 2.0 * ga * D * D * L < 300.0;
+    const bool full = c0 + CW <= W;  // warp-uniform
+    if (full && __all_sync(FULL, ok)) {
+      double E = exp(-q0), Rr = exp(-argR), dx = dx0;
+#pragma unroll
+      for (int k = 0; k < L; ++k) {
+        point(E, dx, zc[k]);
+        E *= Rr;
+        Rr *= rho;
+        dx += D;
+      }
+    } else {
+      // ragged row end or unsafe exponent range: direct evaluation
+#pragma unroll
+      for (int k = 0; k < L; ++k) {
+        if (c0 + lane + 32 * k < W) {
+          const double dx = dx0 + 32.0 * k;
+          point(exp(-(dx * (ga * dx + gb2 * dy) + gc * (dy * dy))), dx, zc[k]);
+        }
+      }
+    }
+  }
+  if (c_begin < c_end) fold((double)(cur_row + a.row0) - y0);
+
+  // block partial of the moment vector
+  __shared__ double red[TPB / 32][MomLayout::KS];
+  __shared__ double vec[KMAX];
+  __shared__ double scratch[combine_scratch(TPB)];
+  __shared__ double mom[MomLayout::KS];
+  __shared__ unsigned int is_last;
+  {
+    const int warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      double s = i < MomLayout::OSR ? smom[i][tid] : (i == MomLayout::OSR ? sr : srr);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+      if (lane == 0) red[warp][i] = s;
+    }
+    const int b = __reduce_add_sync(FULL, bad);
+    if (lane == 0) red[warp][NV] = (double)b;
+    __syncthreads();
+    for (int k = threadIdx.x; k < MomLayout::KS; k += TPB) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < TPB / 32; ++w) s += red[w][k];
+      a.partials[(size_t)blockIdx.x * MomLayout::KS + k] = s;
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) is_last = (atomicAdd(a.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  moment_finish<TPB>(a, st, xs, mom, vec, scratch, cond, use_cond);
+}
+
+}  // namespace jf

@@ -215,26 +215,69 @@ __device__ __forceinline__ void apply_chain_kvec(const Pre& pre, double* vec, do
   __syncthreads();
 }
 
+__host__ __device__ constexpr int combine_scratch(int tpb) { return (tpb / 32) * 40 > tpb ? (tpb / 32) * 40 : tpb; }
+
 // Last-block deterministic sum over the grid's partials; result in out[0..KS).
+// Small K-vectors (KS <= 40): thread t sums the whole rows of blocks
+// t, t + TPB, ... (every load independent: one L2 round trip), then a fixed
+// shuffle + shared-memory tree over the threads.  Larger ones: thread
+// (k, seg) sums column k over blocks seg, seg + NSEG, ... in batches of 16
+// loads.  Either way a fixed order, so the result is bitwise reproducible.
 template <int KS, int TPB>
 __device__ __forceinline__ void grid_combine(const double* __restrict__ part, int nblk, double* out,
-                                             double* scratch /* TPB doubles */) {
-  constexpr int NSEG = (TPB / KS) > 0 ? (TPB / KS) : 1;
+                                             double* scratch /* combine_scratch(TPB) doubles */) {
   const int t = threadIdx.x;
-  if (t < NSEG * KS) {
-    const int k = t % KS, seg = t / KS;
-    double s = 0.0;
-    for (int b = seg; b < nblk; b += NSEG) s += __ldcg(part + (size_t)b * KS + k);
-    scratch[seg * KS + k] = s;
-  }
-  __syncthreads();
-  for (int k = t; k < KS; k += TPB) {
-    double s = 0.0;
+  if constexpr (KS <= 40) {
+    constexpr int NW = TPB / 32;
+    double acc[KS];
 #pragma unroll
-    for (int seg = 0; seg < NSEG; ++seg) s += scratch[seg * KS + k];
-    out[k] = s;
+    for (int k = 0; k < KS; ++k) acc[k] = 0.0;
+    for (int b = t; b < nblk; b += TPB) {
+      const double* row = part + (size_t)b * KS;
+#pragma unroll
+      for (int k = 0; k < KS; ++k) acc[k] += __ldcg(row + k);
+    }
+    const int lane = t & 31, warp = t >> 5;
+#pragma unroll
+    for (int k = 0; k < KS; ++k) {
+      double v = acc[k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+      if (lane == 0) scratch[warp * KS + k] = v;
+    }
+    __syncthreads();
+    if (t < KS) {
+      double v = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) v += scratch[w * KS + t];
+      out[t] = v;
+    }
+    __syncthreads();
+  } else {
+    constexpr int NSEG = (TPB / KS) > 0 ? (TPB / KS) : 1;
+    if (t < NSEG * KS) {
+      const int k = t % KS, seg = t / KS;
+      double s = 0.0;
+      int b = seg;
+      for (; b + 15 * NSEG < nblk; b += 16 * NSEG) {
+        double v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = __ldcg(part + (size_t)(b + i * NSEG) * KS + k);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) s += v[i];
+      }
+      for (; b < nblk; b += NSEG) s += __ldcg(part + (size_t)b * KS + k);
+      scratch[seg * KS + k] = s;
+    }
+    __syncthreads();
+    for (int k = t; k < KS; k += TPB) {
+      double s = 0.0;
+#pragma unroll
+      for (int seg = 0; seg < NSEG; ++seg) s += scratch[seg * KS + k];
+      out[k] = s;
+    }
+    __syncthreads();
   }
-  __syncthreads();
 }
 
 // Cross-rank combine through the NVLink mailboxes (see jf_comm.cu).
@@ -540,84 +583,35 @@ __device__ __forceinline__ void run_part(const PassArgs& a, const Pre& pre, int 
 
 }
 
-// The pass kernel.  epilogue == EPI_FIT: one pass of a fit (st is the state).
-template <class Model, bool JAC, int COORD, bool WGT, int P = PassCfg<Model, JAC>::P,
-          int TPB = PassCfg<Model, JAC>::TPB, int MINB = PassCfg<Model, JAC>::MINB, bool PREC = false>
-__global__ void __launch_bounds__(TPB, MINB)
-    pass_kernel(const PassArgs* __restrict__ pa, FitState* __restrict__ st, cudaGraphConditionalHandle cond,
-                int use_cond) {
-  (void)cond;
-  (void)use_cond;
-  using Sh = PassShape<Model, JAC>;
-  constexpr int KT = Sh::KT, KS = Sh::KS;
-  const PassArgs& a = *pa;
-
-  // Phase predication inside a fit: run only when this pass type is wanted.
-  if (a.epilogue == EPI_FIT) {
-    // the solver kernel after this pass may be scheduled now (PDL); it waits
-    // for this grid's completion in griddepcontrol.wait
-    asm volatile("griddepcontrol.launch_dependents;");
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      atomicAdd(&st->kernels, 1);
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      const int k = atomicAdd(&st->tl_n, 1);
-      if (k < 64) st->tl[k] = t;
-    }
-    const int ph = st->phase;
-    const bool want = JAC ? (PREC ? (ph == PH_QR2) : (ph == PH_INIT_J || ph == PH_TRIAL_J || ph == PH_ACCEPT_J))
-                          : (ph == PH_TRIAL_R);
-    if (!want) return;
+// Common start of every pass kernel: inside a fit, count the launch, stamp
+// the timeline, let the dependent solver kernel launch early (PDL; it waits
+// for this grid in griddepcontrol.wait) and run only when the fit's phase
+// wants this pass type.
+template <bool JAC, bool PREC>
+__device__ __forceinline__ bool pass_begin(const PassArgs& a, FitState* __restrict__ st) {
+  if (a.epilogue != EPI_FIT) return true;
+  // PDL: the solver kernel before this pass in the graph has finished and its
+  // state is visible (a no-op without a programmatic dependency)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    atomicAdd(&st->kernels, 1);
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const int k = atomicAdd(&st->tl_n, 1);
+    if (k < 64) st->tl[k] = t;
   }
-  const double* xs = (a.epilogue == EPI_FIT) ? st->x_eval : a.x;
-  double xv[Model::N];
-#pragma unroll
-  for (int j = 0; j < Model::N; ++j) xv[j] = xs[j];
-  const auto pre = Model::template prologue<JAC>(xv);
+  const int ph = st->phase;
+  return JAC ? (PREC ? (ph == PH_QR2) : (ph == PH_INIT_J || ph == PH_TRIAL_J || ph == PH_ACCEPT_J))
+             : (ph == PH_TRIAL_R);
+}
 
-  // TSQR second pass: the preconditioner P = R1^-1 into shared memory
-  __shared__ double prec_s[PREC ? (Model::N + 1) * (Model::N + 1) + 9 * Model::NT + 1 : 1];
-  const double* prec = nullptr;
-  if constexpr (PREC) {
-    constexpr int N1 = Model::N + 1;
-    const double* src = (a.epilogue == EPI_FIT) ? st->prec : a.precond;
-    for (int k = threadIdx.x; k < N1 * N1; k += TPB) prec_s[k] = src[k];
-    if (threadIdx.x == 0) {
-      for (int g = 0; g < Model::NT; ++g)
-        for (int q = 0; q < 9; ++q) prec_s[N1 * N1 + 9 * g + q] = Model::tblock(pre, g)[q];
-    }
-    __syncthreads();
-    prec = prec_s;
-  }
-
-  __shared__ double red[TPB / 32][KT + 1];
-  __shared__ double vec[KMAX];
-  __shared__ double scratch[TPB];
-  __shared__ unsigned int is_last;
-  constexpr int NP1 = Model::N + 1;
-  if constexpr (JAC && Model::N > 7) {
-    // split triangle: rows [0, 4) by the first half of the grid, [4, n+1) by the second
-    const int half = gridDim.x / 2;
-    if ((int)blockIdx.x < half) {
-      run_part<Model, JAC, COORD, WGT, P, TPB, 0, 4, PREC>(a, pre, blockIdx.x, half, red, a.partials, prec);
-    } else {
-      run_part<Model, JAC, COORD, WGT, P, TPB, 4, NP1, PREC>(a, pre, blockIdx.x - half, gridDim.x - half, red, a.partials, prec);
-    }
-  } else {
-    run_part<Model, JAC, COORD, WGT, P, TPB, 0, (JAC ? NP1 : 1), PREC>(a, pre, blockIdx.x, gridDim.x, red, a.partials, prec);
-  }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) is_last = (atomicAdd(a.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
-  __syncthreads();
-  if (!is_last) return;
-  __threadfence();
-  grid_combine<KS, TPB>(a.partials, gridDim.x, vec, scratch);
-  if (threadIdx.x == 0) *a.ticket = 0u;  // ready for the next launch
-  if constexpr (JAC && Model::NT > 0 && !PREC) {
-    if (!a.no_chain) apply_chain_kvec<Model, TPB>(pre, vec, scratch);
-  }
-
+// Common end of every pass kernel's last block: the cross-rank combine
+// (multi-GPU), then either the K-vector to a.out (plain pass) or the hand-off
+// to the solver kernel (fit).  vec: the block's combined K-vector (smem).
+template <int KS, int TPB, bool JAC>
+__device__ __forceinline__ void pass_tail(const PassArgs& a, FitState* __restrict__ st, double* vec,
+                                          cudaGraphConditionalHandle cond, int use_cond) {
   if (a.use_comm) {
     const unsigned long long epoch = (a.epilogue == EPI_FIT) ? (st->comm_epoch + 1) : (a.comm.epoch + 1);
     const bool ok = comm_combine<KS, TPB>(a.comm, epoch, vec);
@@ -651,6 +645,71 @@ __global__ void __launch_bounds__(TPB, MINB)
     const int k = atomicAdd(&st->tl_n, 1);
     if (k < 64) st->tl[k] = t;
   }
+}
+
+// The pass kernel.  epilogue == EPI_FIT: one pass of a fit (st is the state).
+template <class Model, bool JAC, int COORD, bool WGT, int P = PassCfg<Model, JAC>::P,
+          int TPB = PassCfg<Model, JAC>::TPB, int MINB = PassCfg<Model, JAC>::MINB, bool PREC = false>
+__global__ void __launch_bounds__(TPB, MINB)
+    pass_kernel(const PassArgs* __restrict__ pa, FitState* __restrict__ st, cudaGraphConditionalHandle cond,
+                int use_cond) {
+  (void)cond;
+  (void)use_cond;
+  using Sh = PassShape<Model, JAC>;
+  constexpr int KT = Sh::KT, KS = Sh::KS;
+  const PassArgs& a = *pa;
+
+  if (!pass_begin<JAC, PREC>(a, st)) return;
+  const double* xs = (a.epilogue == EPI_FIT) ? st->x_eval : a.x;
+  double xv[Model::N];
+#pragma unroll
+  for (int j = 0; j < Model::N; ++j) xv[j] = xs[j];
+  const auto pre = Model::template prologue<JAC>(xv);
+
+  // TSQR second pass: the preconditioner P = R1^-1 into shared memory
+  __shared__ double prec_s[PREC ? (Model::N + 1) * (Model::N + 1) + 9 * Model::NT + 1 : 1];
+  const double* prec = nullptr;
+  if constexpr (PREC) {
+    constexpr int N1 = Model::N + 1;
+    const double* src = (a.epilogue == EPI_FIT) ? st->prec : a.precond;
+    for (int k = threadIdx.x; k < N1 * N1; k += TPB) prec_s[k] = src[k];
+    if (threadIdx.x == 0) {
+      for (int g = 0; g < Model::NT; ++g)
+        for (int q = 0; q < 9; ++q) prec_s[N1 * N1 + 9 * g + q] = Model::tblock(pre, g)[q];
+    }
+    __syncthreads();
+    prec = prec_s;
+  }
+
+  __shared__ double red[TPB / 32][KT + 1];
+  __shared__ double vec[KMAX];
+  __shared__ double scratch[combine_scratch(TPB)];
+  __shared__ unsigned int is_last;
+  constexpr int NP1 = Model::N + 1;
+  if constexpr (JAC && Model::N > 7) {
+    // split triangle: rows [0, 4) by the first half of the grid, [4, n+1) by the second
+    const int half = gridDim.x / 2;
+    if ((int)blockIdx.x < half) {
+      run_part<Model, JAC, COORD, WGT, P, TPB, 0, 4, PREC>(a, pre, blockIdx.x, half, red, a.partials, prec);
+    } else {
+      run_part<Model, JAC, COORD, WGT, P, TPB, 4, NP1, PREC>(a, pre, blockIdx.x - half, gridDim.x - half, red, a.partials, prec);
+    }
+  } else {
+    run_part<Model, JAC, COORD, WGT, P, TPB, 0, (JAC ? NP1 : 1), PREC>(a, pre, blockIdx.x, gridDim.x, red, a.partials, prec);
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) is_last = (atomicAdd(a.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  grid_combine<KS, TPB>(a.partials, gridDim.x, vec, scratch);
+  if (threadIdx.x == 0) *a.ticket = 0u;  // ready for the next launch
+  if constexpr (JAC && Model::NT > 0 && !PREC) {
+    if (!a.no_chain) apply_chain_kvec<Model, TPB>(pre, vec, scratch);
+  }
+
+  pass_tail<KS, TPB, JAC>(a, st, vec, cond, use_cond);
 }
 
 // ---------------------------------------------------------------- small m

@@ -21,6 +21,8 @@ __global__ void __launch_bounds__(32, 1)
   (void)lane;
   // PDL: wait for the pass kernel before us (a no-op for a plain launch)
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // the next pass kernel may be scheduled now; it waits for this grid
+  asm volatile("griddepcontrol.launch_dependents;");
   if (lane == 0) atomicAdd(&st->kernels, 1);
   __syncwarp();
   if (st->pass_ready != 0) {

@@ -465,50 +465,83 @@ __device__ __noinline__ int solve_tr(SolverSmem& S, int64_t m, const double* suf
 // conservative: s_max^2 <= trace(B_hat) and s_min^2 >= 1 / ||L^-1||_F^2
 // (B_hat = L L^T), so 1/||L^-1||_F > 2 EPS m sqrt(trace) implies R6.
 // Returns 1 with p when the certified trial lies inside the trust region.
+// Register-resident Cholesky (lane 0, n compile-time so every loop unrolls
+// and every index is static): lower L of the SPD matrix in L (in place),
+// cinv = 1 / diag(L); false if a pivot is not positive.
 template <int n>
-__device__ __noinline__ int gn_fastpath(SolverSmem& S, int64_t m, const double* gh, double Delta, double* p) {
-  double(*L)[MS] = S.T;
-  double tr = 0.0;
-  for (int i = 0; i < n; ++i) {
-    tr += S.M[i][i];
-    for (int j = 0; j <= i; ++j) L[i][j] = S.M[i][j];
-  }
-  for (int k = 0; k < n; ++k) {  // left-looking Cholesky, lower triangle
+__device__ __forceinline__ bool chol_reg(double (&L)[n][n], double (&cinv)[n]) {
+#pragma unroll
+  for (int k = 0; k < n; ++k) {
     double d = L[k][k];
+#pragma unroll
     for (int j = 0; j < k; ++j) d = fma(-L[k][j], L[k][j], d);
-    if (!(d > 0.0)) return 0;
+    if (!(d > 0.0)) return false;
     const double r = rsqrt(d);
     L[k][k] = d * r;
-    S.cinv[k] = r;
+    cinv[k] = r;
+#pragma unroll
     for (int i = k + 1; i < n; ++i) {
       double t = L[i][k];
+#pragma unroll
       for (int j = 0; j < k; ++j) t = fma(-L[i][j], L[k][j], t);
       L[i][k] = t * r;
     }
   }
-  double fro = 0.0;  // ||L^-1||_F^2, column by column
-  double* y = S.w1;
+  return true;
+}
+// ||L^-1||_F^2 with Y = L^-1 (lower) returned
+template <int n>
+__device__ __forceinline__ double inv_fro2(const double (&L)[n][n], const double (&cinv)[n], double (&Y)[n][n]) {
+  double fro = 0.0;
+#pragma unroll
   for (int c = 0; c < n; ++c) {
+#pragma unroll
     for (int i = c; i < n; ++i) {
       double t = (i == c) ? 1.0 : 0.0;
-      for (int k = c; k < i; ++k) t = fma(-L[i][k], y[k], t);
-      y[i] = t * S.cinv[i];
-      fro = fma(y[i], y[i], fro);
+#pragma unroll
+      for (int k = c; k < i; ++k) t = fma(-L[i][k], Y[k][c], t);
+      Y[i][c] = t * cinv[i];
+      fro = fma(Y[i][c], Y[i][c], fro);
     }
   }
-  if (!(m >= n && rsqrt(fro) > 2.0 * DBL_EPSILON * (double)m * sqrt(tr))) return 0;
-  double* w = S.w2;  // L w = -g_hat
+  return fro;
+}
+
+template <int n>
+__device__ __noinline__ int gn_fastpath(SolverSmem& S, int64_t m, const double* gh, double Delta, double* p) {
+  double L[n][n], Y[n][n], cinv[n];
+  double tr = 0.0;
+#pragma unroll
   for (int i = 0; i < n; ++i) {
-    double t = -gh[i];
-    for (int k = 0; k < i; ++k) t = fma(-L[i][k], w[k], t);
-    w[i] = t * S.cinv[i];
+#pragma unroll
+    for (int j = 0; j <= i; ++j) L[i][j] = S.M[i][j];
+    tr += L[i][i];
   }
+  if (!chol_reg<n>(L, cinv)) return 0;
+  const double fro = inv_fro2<n>(L, cinv, Y);
+  if (!(m >= n && rsqrt(fro) > 2.0 * DBL_EPSILON * (double)m * sqrt(tr))) return 0;
+  double w[n], pr[n];
+#pragma unroll
+  for (int i = 0; i < n; ++i) {  // L w = -g_hat
+    double t = -gh[i];
+#pragma unroll
+    for (int k = 0; k < i; ++k) t = fma(-L[i][k], w[k], t);
+    w[i] = t * cinv[i];
+  }
+#pragma unroll
   for (int i = n - 1; i >= 0; --i) {  // L^T p = w
     double t = w[i];
-    for (int k = i + 1; k < n; ++k) t = fma(-L[k][i], p[k], t);
-    p[i] = t * S.cinv[i];
+#pragma unroll
+    for (int k = i + 1; k < n; ++k) t = fma(-L[k][i], pr[k], t);
+    pr[i] = t * cinv[i];
   }
-  return vnorm<n>(p) <= Delta ? 1 : 0;
+  double pn = 0.0;
+#pragma unroll
+  for (int i = 0; i < n; ++i) {
+    p[i] = pr[i];
+    pn = fma(pr[i], pr[i], pn);
+  }
+  return sqrt(pn) <= Delta ? 1 : 0;
 }
 
 // --------------------------------------------------- Coleman-Li helpers (R19)
@@ -916,41 +949,21 @@ __device__ __forceinline__ void st_qr_finish(FitState* st, SolverSmem& S, const 
 // numerically SPD.
 template <int n>
 __device__ __forceinline__ double kappa2_estimate(FitState* st, SolverSmem& S) {
-  double dinv[NMAX];
+  double dinv[n], L[n][n], Y[n][n], cinv[n];
+#pragma unroll
   for (int j = 0; j < n; ++j) {
     const double gjj = st->G[j * NMAX + j];
     dinv[j] = gjj > 0.0 ? rsqrt(gjj) : 1.0;
   }
-  double(*L)[MS] = S.T;
   double tr = 0.0;
+#pragma unroll
   for (int i = 0; i < n; ++i) {
+#pragma unroll
     for (int j = 0; j <= i; ++j) L[i][j] = dinv[i] * st->G[i * NMAX + j] * dinv[j];
     tr += L[i][i];
   }
-  for (int k = 0; k < n; ++k) {
-    double d = L[k][k];
-    for (int j = 0; j < k; ++j) d = fma(-L[k][j], L[k][j], d);
-    if (!(d > 0.0)) return INFINITY;
-    const double r = rsqrt(d);
-    L[k][k] = d * r;
-    S.cinv[k] = r;
-    for (int i = k + 1; i < n; ++i) {
-      double t = L[i][k];
-      for (int j = 0; j < k; ++j) t = fma(-L[i][j], L[k][j], t);
-      L[i][k] = t * r;
-    }
-  }
-  double fro = 0.0;
-  double* y = S.w1;
-  for (int c = 0; c < n; ++c) {
-    for (int i = c; i < n; ++i) {
-      double t = (i == c) ? 1.0 : 0.0;
-      for (int k = c; k < i; ++k) t = fma(-L[i][k], y[k], t);
-      y[i] = t * S.cinv[i];
-      fro = fma(y[i], y[i], fro);
-    }
-  }
-  return tr * fro;
+  if (!chol_reg<n>(L, cinv)) return INFINITY;
+  return tr * inv_fro2<n>(L, cinv, Y);
 }
 
 // Initialisation after the J-pass at x0 (Alg. 1 l.137-138; R3, R4, R18).
@@ -1107,14 +1120,6 @@ __device__ __noinline__ void fit_after_pass(FitState* st, SolverSmem& S, const d
   }
 }
 
-// Whole warp: one solver step after a pass (state machine on lane 0, the
-// eigensolver on all lanes when a trial needs it).
-// Whole warp, once at the end of a fit: the parameter covariance curve_fit
-// returns with the parameters: the Moore-Penrose
-// inverse of J^T J at the final x, discarding singular values of J below
-// EPS * max(m, n) * s_max, scaled by 2 cost / (m - n) (m > n; else +inf).
-// J^T J = V diag(s^2) V^T is the final pass's Gram (the same eigensolver as
-// the trust-region subproblem).
 // Fast path of the covariance (lane 0): when the Cholesky certificate of
 // gn_fastpath shows no singular value of J falls below the cut-off
 // (1/||L^-1||_F > 2 EPS max(m, n) sqrt(trace G) => s_min > EPS max(m, n) s_max),
@@ -1122,41 +1127,24 @@ __device__ __noinline__ void fit_after_pass(FitState* st, SolverSmem& S, const d
 // place of an eigendecomposition.  Returns false when not certified.
 template <int n>
 __device__ __noinline__ bool pcov_chol(FitState* st, SolverSmem& S, double s_sq) {
-  double(*L)[MS] = S.T;
-  double(*Y)[MS] = S.A;  // Y = L^-1 (lower)
   const int64_t m = st->m_global;
+  double L[n][n], Y[n][n], cinv[n];
   double tr = 0.0;
+#pragma unroll
   for (int i = 0; i < n; ++i) {
     tr += st->G[i * NMAX + i];
+#pragma unroll
     for (int j = 0; j <= i; ++j) L[i][j] = st->G[i * NMAX + j];
   }
-  for (int k = 0; k < n; ++k) {
-    double d = L[k][k];
-    for (int j = 0; j < k; ++j) d = fma(-L[k][j], L[k][j], d);
-    if (!(d > 0.0)) return false;
-    const double r = rsqrt(d);
-    L[k][k] = d * r;
-    S.cinv[k] = r;
-    for (int i = k + 1; i < n; ++i) {
-      double t = L[i][k];
-      for (int j = 0; j < k; ++j) t = fma(-L[i][j], L[k][j], t);
-      L[i][k] = t * r;
-    }
-  }
-  double fro = 0.0;
-  for (int c = 0; c < n; ++c) {
-    for (int i = 0; i < c; ++i) Y[i][c] = 0.0;
-    for (int i = c; i < n; ++i) {
-      double t = (i == c) ? 1.0 : 0.0;
-      for (int k = c; k < i; ++k) t = fma(-L[i][k], Y[k][c], t);
-      Y[i][c] = t * S.cinv[i];
-      fro = fma(Y[i][c], Y[i][c], fro);
-    }
-  }
+  if (!chol_reg<n>(L, cinv)) return false;
+  const double fro = inv_fro2<n>(L, cinv, Y);
   if (!(m >= n && rsqrt(fro) > 2.0 * DBL_EPSILON * (double)(m > n ? m : n) * sqrt(tr))) return false;
+#pragma unroll
   for (int i = 0; i < n; ++i) {
+#pragma unroll
     for (int j = i; j < n; ++j) {
       double t = 0.0;
+#pragma unroll
       for (int k = j; k < n; ++k) t = fma(Y[k][i], Y[k][j], t);
       st->pcov[i * NMAX + j] = st->pcov[j * NMAX + i] = t * s_sq;
     }

@@ -27,7 +27,7 @@ def _kw(pr):
     return dict(y=pr.t)
 
 
-def check_fit(res, ref, trace=None, ref_trace=None):
+def check_fit(res, ref, trace=None, ref_trace=None, trace_rtol=1e-9):
     assert (res.status, res.nfev, res.njev, res.nit) == (ref["status"], ref["nfev"], ref["njev"], ref["nit"])
     x = ref["x"]
     assert np.all(np.abs(res.x - x) <= 1e-6 * np.maximum(np.abs(x), 1e-3 * np.max(np.abs(x))))
@@ -42,7 +42,8 @@ def check_fit(res, ref, trace=None, ref_trace=None):
         assert np.array_equal(trace[:, [0, 1, 2, 11]], tr[:, [0, 1, 2, 11]])
         for col in (5, 6):
             a, b = trace[:, col], tr[:, col]
-            assert np.all(np.abs(a - b) <= 1e-9 * np.maximum(np.abs(b), 1e-300))
+            rel = np.abs(a - b) / np.maximum(np.abs(b), 1e-300)
+            assert np.all(rel <= trace_rtol), (col, float(rel.max()))
 
 
 FITS = [
@@ -193,12 +194,15 @@ def _ill_conditioned(sig):
 def test_tsqr_ill_conditioned_matches_oracle(sig):
     """kappa(J D^-1) ~ 5e3 / 3e4 (wide Gaussian ~ offset): the TSQR path keeps
     the oracle's trajectory (reading R28: the Gram path's eigenvalues resolve
-    s_min only to ~1e-8 s_max)."""
+    s_min only to ~1e-8 s_max).  R from CholeskyQR2 carries a relative error
+    ~ EPS kappa (~1e-11 here) against the oracle's Householder SVD, and the
+    Moré alpha (the root of ||p(alpha)|| = Delta, dominated by s_min) inherits
+    it amplified by s_max / s_min: Delta and alpha to 1e-7 (reading R28)."""
     t, z, p0 = _ill_conditioned(sig)
     tr = []
     ref = otrf.fit("gauss1d", t, z, p0, trace=tr)
     res = jf.curve_fit("gauss1d", z, y=t, p0=p0, solver="tsqr", trace_cap=256)
-    check_fit(res, ref, res.trace, tr)
+    check_fit(res, ref, res.trace, tr, trace_rtol=1e-7)
 
 
 def test_auto_solver_picks_tsqr_only_when_ill_conditioned():
