@@ -121,6 +121,7 @@ struct Ctx {
 // of a jf_comm_create_local emulation, so emulated ranks run concurrently.
 Ctx g_ctx[64 + 64 * 8];
 constexpr int SCRATCH_DOUBLES = 1024;
+constexpr int TICKETS = 128;  // grid_reduce: [0] groups, [1 + g] blocks of group g (<= 127 groups)
 
 int ctx_init(Ctx& c, int dev) {
   if (c.ready) return 0;
@@ -132,15 +133,16 @@ int ctx_init(Ctx& c, int dev) {
   CK(cudaMalloc(&c.d_state, sizeof(FitState)));
   CK(cudaMallocHost(&c.h_state, sizeof(FitState)));
   c.partial_blocks = c.nsm * 4;
-  CK(cudaMalloc(&c.d_partials, sizeof(double) * (size_t)c.partial_blocks * KMAX));
-  CK(cudaMalloc(&c.d_ticket, sizeof(unsigned int) * 4));
+  // block rows + group rows of the two-level grid reduction (jf_pass.cuh grid_reduce)
+  CK(cudaMalloc(&c.d_partials, sizeof(double) * (size_t)(c.partial_blocks + c.partial_blocks / 16 + 1) * KMAX));
+  CK(cudaMalloc(&c.d_ticket, sizeof(unsigned int) * TICKETS));
   CK(cudaMalloc(&c.d_out, sizeof(double) * KMAX));
   CK(cudaMalloc(&c.d_x, sizeof(double) * NMAX));
   CK(cudaMalloc(&c.d_scratch, sizeof(double) * SCRATCH_DOUBLES));
   CK(cudaMalloc(&c.d_qr, sizeof(QRState)));
   // no device-wide synchronisation here: emulated ranks (jf_comm_create_local)
   // may have pass kernels spinning on their mailboxes while a peer initialises
-  CK(cudaMemsetAsync(c.d_ticket, 0, sizeof(unsigned int) * 4, c.stream));
+  CK(cudaMemsetAsync(c.d_ticket, 0, sizeof(unsigned int) * TICKETS, c.stream));
   CK(cudaMemsetAsync(c.d_scratch, 0, sizeof(double) * SCRATCH_DOUBLES, c.stream));
   CK(cudaStreamSynchronize(c.stream));
   c.ready = true;

@@ -37,6 +37,10 @@ Kernels kernels_gauss2d(int coord) {
       if (var == 13) { k.jk = moment_pass_kernel<16, 128, 4>; }
       if (var == 14) { k.jk = moment_pass_kernel<8, 128, 5>; }
       if (var == 15) { k.jk = moment_pass_kernel<4, 128, 4>; }
+      if (var == 16) { k.jk = moment_pass_kernel<16, 128, 3, 1>; }
+      if (var == 17) { k.jk = moment_pass_kernel<16, 128, 3, 2>; }
+      if (var == 18) { k.jk = moment_pass_kernel<16, 128, 3, 8>; }
+      if (var == 19) { k.jk = moment_pass_kernel<8, 128, 3, 8>; }
     }
   }
   return k;

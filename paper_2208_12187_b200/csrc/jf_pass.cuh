@@ -215,69 +215,78 @@ __device__ __forceinline__ void apply_chain_kvec(const Pre& pre, double* vec, do
   __syncthreads();
 }
 
-__host__ __device__ constexpr int combine_scratch(int tpb) { return (tpb / 32) * 40 > tpb ? (tpb / 32) * 40 : tpb; }
+__host__ __device__ constexpr int combine_scratch(int tpb) { return tpb; }
 
-// Last-block deterministic sum over the grid's partials; result in out[0..KS).
-// Small K-vectors (KS <= 40): thread t sums the whole rows of blocks
-// t, t + TPB, ... (every load independent: one L2 round trip), then a fixed
-// shuffle + shared-memory tree over the threads.  Larger ones: thread
-// (k, seg) sums column k over blocks seg, seg + NSEG, ... in batches of 16
-// loads.  Either way a fixed order, so the result is bitwise reproducible.
+// Two-level deterministic grid reduction of the per-block partials
+// (partials[b][0..KS), written by every block before calling).  Blocks form
+// groups of GROUP consecutive indices; the last block of a group to finish
+// (atomic ticket) sums the group's rows in block order into a group row
+// (stored after the nblk block rows); the last group to finish sums the group
+// rows in group order into out[0..KS) and returns true — exactly one block of
+// the grid gets true.  Every sum has a fixed order (bitwise reproducible) and
+// at most two L2 round trips sit on the critical path after the last block
+// arrives (one for its group, one for the group rows).
+// Tickets: a.ticket[0] (groups), a.ticket[1 + g] (blocks of group g); each
+// is reset by its last user, ready for the next launch.
+constexpr int GROUP = 16;
 template <int KS, int TPB>
-__device__ __forceinline__ void grid_combine(const double* __restrict__ part, int nblk, double* out,
-                                             double* scratch /* combine_scratch(TPB) doubles */) {
+__device__ __forceinline__ bool grid_reduce(const PassArgs& a, double* out, double* scratch /* TPB doubles */) {
+  __shared__ unsigned int flag;
   const int t = threadIdx.x;
-  if constexpr (KS <= 40) {
-    constexpr int NW = TPB / 32;
-    double acc[KS];
+  const int nblk = gridDim.x;
+  const int ngrp = (nblk + GROUP - 1) / GROUP;
+  const int g = blockIdx.x / GROUP;
+  const int b0 = g * GROUP, nb = min(GROUP, nblk - b0);
+  double* grp = a.partials + (size_t)nblk * KS;
+  __threadfence();
+  __syncthreads();
+  if (t == 0) flag = (atomicAdd(a.ticket + 1 + g, 1u) == (unsigned)(nb - 1)) ? 1u : 0u;
+  __syncthreads();
+  if (!flag) return false;
+  __threadfence();
+  for (int k = t; k < KS; k += TPB) {
+    double v[GROUP];
 #pragma unroll
-    for (int k = 0; k < KS; ++k) acc[k] = 0.0;
-    for (int b = t; b < nblk; b += TPB) {
-      const double* row = part + (size_t)b * KS;
+    for (int i = 0; i < GROUP; ++i) v[i] = (i < nb) ? __ldcg(a.partials + (size_t)(b0 + i) * KS + k) : 0.0;
+    double s = 0.0;
 #pragma unroll
-      for (int k = 0; k < KS; ++k) acc[k] += __ldcg(row + k);
-    }
-    const int lane = t & 31, warp = t >> 5;
-#pragma unroll
-    for (int k = 0; k < KS; ++k) {
-      double v = acc[k];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-      if (lane == 0) scratch[warp * KS + k] = v;
-    }
-    __syncthreads();
-    if (t < KS) {
-      double v = 0.0;
-#pragma unroll
-      for (int w = 0; w < NW; ++w) v += scratch[w * KS + t];
-      out[t] = v;
-    }
-    __syncthreads();
-  } else {
-    constexpr int NSEG = (TPB / KS) > 0 ? (TPB / KS) : 1;
-    if (t < NSEG * KS) {
-      const int k = t % KS, seg = t / KS;
-      double s = 0.0;
-      int b = seg;
-      for (; b + 15 * NSEG < nblk; b += 16 * NSEG) {
-        double v[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = __ldcg(part + (size_t)(b + i * NSEG) * KS + k);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) s += v[i];
-      }
-      for (; b < nblk; b += NSEG) s += __ldcg(part + (size_t)b * KS + k);
-      scratch[seg * KS + k] = s;
-    }
-    __syncthreads();
-    for (int k = t; k < KS; k += TPB) {
-      double s = 0.0;
-#pragma unroll
-      for (int seg = 0; seg < NSEG; ++seg) s += scratch[seg * KS + k];
-      out[k] = s;
-    }
-    __syncthreads();
+    for (int i = 0; i < GROUP; ++i) s += v[i];
+    grp[(size_t)g * KS + k] = s;
   }
+  if (t == 0) a.ticket[1 + g] = 0u;
+  __threadfence();
+  __syncthreads();
+  if (t == 0) flag = (atomicAdd(a.ticket, 1u) == (unsigned)(ngrp - 1)) ? 1u : 0u;
+  __syncthreads();
+  if (!flag) return false;
+  __threadfence();
+  // group rows: NSEG segments per column, each up to 16 rows in one batch
+  constexpr int NSEG = (TPB / KS) > 0 ? (TPB / KS) : 1;
+  if (t < NSEG * KS) {
+    const int k = t % KS, seg = t / KS;
+    double s = 0.0;
+    for (int r0 = seg; r0 < ngrp; r0 += 16 * NSEG) {
+      double v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int r = r0 + i * NSEG;
+        v[i] = (r < ngrp) ? __ldcg(grp + (size_t)r * KS + k) : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) s += v[i];
+    }
+    scratch[seg * KS + k] = s;
+  }
+  if (t == 0) a.ticket[0] = 0u;
+  __syncthreads();
+  for (int k = t; k < KS; k += TPB) {
+    double s = 0.0;
+#pragma unroll
+    for (int seg = 0; seg < NSEG; ++seg) s += scratch[seg * KS + k];
+    out[k] = s;
+  }
+  __syncthreads();
+  return true;
 }
 
 // Cross-rank combine through the NVLink mailboxes (see jf_comm.cu).
@@ -684,7 +693,6 @@ __global__ void __launch_bounds__(TPB, MINB)
   __shared__ double red[TPB / 32][KT + 1];
   __shared__ double vec[KMAX];
   __shared__ double scratch[combine_scratch(TPB)];
-  __shared__ unsigned int is_last;
   constexpr int NP1 = Model::N + 1;
   if constexpr (JAC && Model::N > 7) {
     // split triangle: rows [0, 4) by the first half of the grid, [4, n+1) by the second
@@ -697,14 +705,7 @@ __global__ void __launch_bounds__(TPB, MINB)
   } else {
     run_part<Model, JAC, COORD, WGT, P, TPB, 0, (JAC ? NP1 : 1), PREC>(a, pre, blockIdx.x, gridDim.x, red, a.partials, prec);
   }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) is_last = (atomicAdd(a.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
-  __syncthreads();
-  if (!is_last) return;
-  __threadfence();
-  grid_combine<KS, TPB>(a.partials, gridDim.x, vec, scratch);
-  if (threadIdx.x == 0) *a.ticket = 0u;  // ready for the next launch
+  if (!grid_reduce<KS, TPB>(a, vec, scratch)) return;
   if constexpr (JAC && Model::NT > 0 && !PREC) {
     if (!a.no_chain) apply_chain_kvec<Model, TPB>(pre, vec, scratch);
   }
