@@ -41,13 +41,15 @@ import datagen as dg  # noqa: E402
 W_IMG = 4096
 SEED = 6
 N_PARAMS = 7
-# Algorithmic FP64 work per point of the n=7 J-pass: the analytic reference
-# (closed-form row + 36-slot triangle, libdevice exp) compiled for sm_100a
-# executes 85 FP64-pipe instructions per point (52 DFMA, 17 DADD, 16 DMUL;
-# SURVEY §8(d) d.3, re-measured by tools/alg_count.py).  Each FP64-pipe
-# instruction is one issue slot of the 64 FP64 lanes/SM; we count it as 2
-# flops (an FMA slot), so the peak below is the FMA-slot peak.
-ALG_FP64_INSTR_PER_POINT = 85
+# Algorithmic FP64 work per point of the n=7 J-pass as built: the moment
+# form (jf_moment.cuh): per point 19 fp64 operations (row
+# recurrence 2, residual 2, u^2 1, the eleven step-index moments 11 + the u r
+# product 1, sum r and sum r^2 2), per 16-point warp-chunk ~69 (shift of the
+# moments to dx 46, chunk set-up 12, exp re-seed every 4 chunks 11): 23 per
+# point.  Each fp64 operation is one issue slot of the 64 FP64 lanes/SM,
+# counted as 2 flops (an FMA slot), so the peak below is the FMA-slot peak.
+# (The dual-number rank-1 form needs 85 per point — SURVEY §8(d) d.3.)
+ALG_FP64_INSTR_PER_POINT = 23
 BYTES_PER_POINT = 8  # z only (implicit grid)
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.2: SMs x FP64 lanes x 2 x max SM clock
 
@@ -268,7 +270,7 @@ def main():
     alg_flops = 2.0 * ALG_FP64_INSTR_PER_POINT * m_local
     achieved = alg_flops / t_j / 1e12
     roofline = {
-        "bound": "alu", "kernel": "pass_kernel<ModelGauss2DRot,J,grid> (fused dual-number J-pass + fp64 Gram)",
+        "bound": "alu", "kernel": "moment_pass_kernel<16,128,3> (moment-form J-pass, n=7 implicit grid, fp64)",
         "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
         "traffic": None, "launch_us": t_j * 1e6,
         "alg_work": f"{ALG_FP64_INSTR_PER_POINT} FP64-pipe instr/point x 2 flops x {m_local} points",

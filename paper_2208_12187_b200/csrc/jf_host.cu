@@ -155,7 +155,7 @@ int ctx_init(Ctx& c, int dev) {
 std::mutex g_occ_mu;
 std::map<std::pair<int, const void*>, int> g_occ;  // (device, kernel) -> resident blocks/SM
 
-int grid_for(Ctx& c, KernelFn f, int tpb, int64_t m) {
+int grid_for(Ctx& c, KernelFn f, int tpb, int64_t m, int smem = 0) {
   int occ;
   {
     std::lock_guard<std::mutex> g(g_occ_mu);
@@ -163,7 +163,7 @@ int grid_for(Ctx& c, KernelFn f, int tpb, int64_t m) {
     auto it = g_occ.find(key);
     if (it == g_occ.end()) {
       occ = 1;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, tpb, 0) != cudaSuccess || occ < 1) occ = 1;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, tpb, smem) != cudaSuccess || occ < 1) occ = 1;
       if (occ > 4) occ = 4;
       g_occ[key] = occ;
     } else {
@@ -180,7 +180,7 @@ int grid_for(Ctx& c, KernelFn f, int tpb, int64_t m) {
 // The two pass kernels a call uses, with their launch shapes.
 struct PassPair {
   KernelFn j = nullptr, r = nullptr, jp = nullptr;
-  int jtpb = 256, rtpb = 256, jptpb = 256, jgrid = 1, rgrid = 1, jpgrid = 1;
+  int jtpb = 256, rtpb = 256, jptpb = 256, jgrid = 1, rgrid = 1, jpgrid = 1, jsmem = 0;
 };
 
 PassPair select_pass(Ctx& c, const Kernels& k, bool weighted, int64_t m) {
@@ -191,7 +191,8 @@ PassPair select_pass(Ctx& c, const Kernels& k, bool weighted, int64_t m) {
   p.jtpb = k.jtpb;
   p.rtpb = k.rtpb;
   p.jptpb = k.jptpb;
-  p.jgrid = grid_for(c, p.j, p.jtpb, m);
+  p.jsmem = weighted ? 0 : k.jsmem;
+  p.jgrid = grid_for(c, p.j, p.jtpb, m, p.jsmem);
   p.jpgrid = p.jp ? grid_for(c, p.jp, p.jptpb, m) : 1;
   if (k.jsplit) {  // two equal halves
     p.jgrid = p.jgrid < 2 ? 2 : p.jgrid + (p.jgrid & 1);
@@ -369,7 +370,8 @@ int launch_pass(const PassPair& k, bool jac, cudaStream_t s, PassArgs* d_args, F
   KernelFn f = jac ? (prec ? k.jp : k.j) : k.r;
   const int grid = jac ? (prec ? k.jpgrid : k.jgrid) : k.rgrid;
   const int tpb = jac ? (prec ? k.jptpb : k.jtpb) : k.rtpb;
-  f<<<grid, tpb, 0, s>>>(d_args, d_state, (cudaGraphConditionalHandle)0, 0);
+  const int smem = (jac && !prec) ? k.jsmem : 0;
+  f<<<grid, tpb, smem, s>>>(d_args, d_state, (cudaGraphConditionalHandle)0, 0);
   CK(cudaGetLastError());
   return 0;
 }
@@ -457,7 +459,9 @@ int build_graph(Ctx& c, const PassPair& k, int policy, bool qr, cudaGraphExec_t*
     kp.func = (void*)k.j;
     kp.gridDim = dim3(k.jgrid);
     kp.blockDim = dim3(k.jtpb);
+    kp.sharedMemBytes = k.jsmem;
     if (int e = add(kp, false)) return e;
+    kp.sharedMemBytes = 0;
     if (int e = add(sp, true)) return e;
   }
   CK(cudaGraphInstantiate(out, g, 0));

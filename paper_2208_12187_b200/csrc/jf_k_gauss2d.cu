@@ -22,25 +22,32 @@ static Kernels make() {
   k.rtpb = PassCfg<ModelGauss2DRot, false>::TPB;
   return k;
 }
+template <int L, int TPB, int MINB, int SEEDN = 4, int STAGES = 0>
+static void use_moment(Kernels& k) {
+  auto f = moment_pass_kernel<L, TPB, MINB, SEEDN, STAGES>;
+  k.jk = f;
+  k.jtpb = TPB;
+  k.jsmem = moment_zbuf_bytes(L, TPB, STAGES);
+  if (k.jsmem > 0) cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, k.jsmem);
+}
+
 Kernels kernels_gauss2d(int coord) {
   Kernels k = coord == COORD_EXPLICIT ? make<COORD_EXPLICIT>() : make<COORD_GRID>();
-  // development aid: alternative launch shapes of the grid J-pass (JF_JVARIANT=1..3)
   if (coord == COORD_GRID) {
     // unweighted implicit grid: the moment-form J-pass (jf_moment.cuh)
-    k.jk = moment_pass_kernel<16, 128, 3>;
-    k.jtpb = 128;
-    if (const char* v = getenv("JF_JVARIANT")) {
+    use_moment<16, 128, 3>(k);
+    if (const char* v = getenv("JF_JVARIANT")) {  // development aid: alternative shapes
       const int var = atoi(v);
-      if (var == 9) { k.jk = pass_kernel<ModelGauss2DRot, true, COORD_GRID, false>; k.jtpb = 256; }  // dual-number kernel
-      if (var == 11) { k.jk = moment_pass_kernel<8, 128, 3>; }
-      if (var == 12) { k.jk = moment_pass_kernel<8, 128, 4>; }
-      if (var == 13) { k.jk = moment_pass_kernel<16, 128, 4>; }
-      if (var == 14) { k.jk = moment_pass_kernel<8, 128, 5>; }
-      if (var == 15) { k.jk = moment_pass_kernel<4, 128, 4>; }
-      if (var == 16) { k.jk = moment_pass_kernel<16, 128, 3, 1>; }
-      if (var == 17) { k.jk = moment_pass_kernel<16, 128, 3, 2>; }
-      if (var == 18) { k.jk = moment_pass_kernel<16, 128, 3, 8>; }
-      if (var == 19) { k.jk = moment_pass_kernel<8, 128, 3, 8>; }
+      if (var == 9) { k.jk = pass_kernel<ModelGauss2DRot, true, COORD_GRID, false>; k.jtpb = 256; k.jsmem = 0; }  // dual numbers
+      if (var == 11) use_moment<8, 128, 3>(k);
+      if (var == 12) use_moment<8, 128, 4>(k);
+      if (var == 13) use_moment<16, 128, 3, 8>(k);
+      if (var == 20) use_moment<16, 128, 3, 4, 2>(k);
+      if (var == 21) use_moment<16, 128, 3, 4, 3>(k);
+      if (var == 22) use_moment<8, 128, 4, 4, 2>(k);
+      if (var == 23) use_moment<8, 128, 4, 4, 3>(k);
+      if (var == 24) use_moment<16, 128, 4, 4, 2>(k);
+      if (var == 25) use_moment<8, 128, 5, 4, 2>(k);
     }
   }
   return k;

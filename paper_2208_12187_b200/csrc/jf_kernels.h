@@ -17,6 +17,7 @@ struct Kernels {
   KernelFn jkpw = nullptr;
   int jtpb = 256, rtpb = 256;  // threads per block of the J / r kernels
   int jptpb = 256;             // threads per block of the preconditioned J kernel
+  int jsmem = 0;               // dynamic shared memory of the J kernel (bytes)
   bool jsplit = false;         // J grid split in two halves (even grid >= 2)
   SmallFitFn small = nullptr;  // whole-fit single-block kernel (small m), unweighted / weighted
   SmallFitFn smallw = nullptr;

@@ -32,6 +32,11 @@
 
 namespace jf {
 
+// dynamic shared memory of moment_pass_kernel (the cp.async z ring)
+__host__ __device__ constexpr int moment_zbuf_bytes(int L, int TPB, int STAGES) {
+  return STAGES >= 2 ? (TPB / 32) * STAGES * L * 32 * 8 : 0;
+}
+
 // Moment vector layout: M2 (15) | M1 (6) | MR (6) | sum r | sum r^2 | bad
 struct MomLayout {
   static constexpr int N2 = 15, N1 = 6;
@@ -126,7 +131,7 @@ __device__ __noinline__ void moment_finish(const PassArgs& a, FitState* __restri
   pass_tail<KS, TPB, true>(a, st, vec, cond, use_cond);
 }
 
-template <int L, int TPB, int MINB, int SEEDN = 4>
+template <int L, int TPB, int MINB, int SEEDN = 4, int STAGES = 0>
 __global__ void __launch_bounds__(TPB, MINB)
     moment_pass_kernel(const PassArgs* __restrict__ pa, FitState* __restrict__ st, cudaGraphConditionalHandle cond,
                        int use_cond) {
@@ -219,6 +224,7 @@ __global__ void __launch_bounds__(TPB, MINB)
   const int lane = threadIdx.x & 31;
   const int W = (int)a.W;
   const int64_t H = a.m / a.W;
+  const int64_t row0 = a.row0;  // PassArgs fields read once (the loop must not reload them)
   const int cpr = (W + CW - 1) / CW;
   const int64_t nch = H * (int64_t)cpr;
   const int64_t nwt = (int64_t)gridDim.x * (TPB / 32);
@@ -226,44 +232,85 @@ __global__ void __launch_bounds__(TPB, MINB)
   const int64_t c_begin = gw * nch / nwt, c_end = (gw + 1) * nch / nwt;
   const double rho = exp(-2.0 * ga * D * D);
   const double* __restrict__ z = a.z;
-  double zn[L];
+  // z staging.  STAGES == 0: the next chunk is prefetched into registers.
+  // STAGES >= 2: each lane streams its own points of the next STAGES - 1
+  // chunks into a per-warp shared-memory ring with cp.async (LDGSTS,
+  // evict-first in L2), freeing the registers for the arithmetic.
+  constexpr bool ASYNC = STAGES >= 2;
+  extern __shared__ __align__(16) double zbuf[];  // dynamic: moment_zbuf_bytes(L, TPB, STAGES)
+  double* wz = zbuf + (ASYNC ? (threadIdx.x >> 5) * STAGES * L * 32 : 0);
+  unsigned long long pol = 0;
+  if constexpr (ASYNC) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  double zn[ASYNC ? 1 : L];
   // chunk ch = row * cpr + cc; row and cc are advanced incrementally (no
   // 64-bit division in the loop)
   int64_t lrow = c_begin / cpr;  // position of the next chunk to load
   int lcc = (int)(c_begin - lrow * cpr);
-  auto load = [&]() {
+  auto load = [&](int stage) {
     const int col = lcc * CW + lane;
-    const double* zp = z + lrow * a.W + col;
+    const double* zp = z + lrow * (int64_t)W + col;
+    if constexpr (ASYNC) {
 #pragma unroll
-    for (int k = 0; k < L; ++k) zn[k] = (col + 32 * k < W) ? __ldcs(zp + 32 * k) : 0.0;
+      for (int k = 0; k < L; ++k) {
+        const bool v = col + 32 * k < W;
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(wz + (stage * L + k) * 32 + lane);
+        asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2, %3;" ::"r"(dst),
+                     "l"(v ? zp + 32 * k : z), "r"(v ? 8 : 0), "l"(pol)
+                     : "memory");
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < L; ++k) zn[k] = (col + 32 * k < W) ? __ldcs(zp + 32 * k) : 0.0;
+    }
     if (++lcc == cpr) {
       lcc = 0;
       ++lrow;
     }
   };
-  if (c_begin < c_end) load();
+  if constexpr (ASYNC) {
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+      if (c_begin + s < c_end) load(s);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+  } else {
+    if (c_begin < c_end) load(0);
+  }
   int64_t cur_row = c_begin / cpr;
   int cc = (int)(c_begin - cur_row * cpr) - 1;  // chunk column of the current chunk (advanced below)
   int64_t row = cur_row;
   double E = 0.0, Rr = 0.0;
   bool carried = false;
   int since_seed = 0;
+  int stage = 0;
   for (int64_t ch = c_begin; ch < c_end; ++ch) {
-    double zc[L];
+    double zc[ASYNC ? 1 : L];
+    const double* zs = wz + stage * L * 32 + lane;  // ASYNC: this chunk's points, stride 32
+    if constexpr (ASYNC) {
+      const int nxt = stage == 0 ? STAGES - 1 : stage - 1;  // the slot consumed last iteration
+      if (ch + STAGES - 1 < c_end) load(nxt);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_group %0;" ::"n"(STAGES - 1) : "memory");
+    } else {
 #pragma unroll
-    for (int k = 0; k < L; ++k) zc[k] = zn[k];
-    if (ch + 1 < c_end) load();  // prefetch the next chunk
+      for (int k = 0; k < L; ++k) zc[k] = zn[k];
+      if (ch + 1 < c_end) load(0);  // prefetch the next chunk
+    }
+    auto zat = [&](int k) -> double {
+      if constexpr (ASYNC) return zs[32 * k];
+      else return zc[k];
+    };
     if (++cc == cpr) {
       cc = 0;
       ++row;
     }
     if (row != cur_row) {  // warp-uniform
-      fold((double)(cur_row + a.row0) - y0);
+      fold((double)(cur_row + row0) - y0);
       cur_row = row;
       carried = false;
     }
     const int c0 = cc * CW;
-    const double dy = (double)(row + a.row0) - y0;
+    const double dy = (double)(row + row0) - y0;
     const double dx0 = (double)(c0 + lane) - x0;
     const double q0 = dx0 * (ga * dx0 + gb2 * dy) + gc * (dy * dy);
     const double argR = D * (2.0 * ga * dx0 + gb2 * dy) + ga * D * D;
@@ -285,7 +332,7 @@ __global__ void __launch_bounds__(TPB, MINB)
 #pragma unroll
       for (int k = 0; k < L; ++k) {
         const double u = E;
-        const double r = fma(A, u, off) - zc[k];  // Eq. 1: r = h - z
+        const double r = fma(A, u, off) - zat(k);  // Eq. 1: r = h - z
         bad += isfinite(r) ? 0 : 1;
         const double u2 = u * u;
         const double k1 = (double)k, k2 = k1 * k1, k3 = k2 * k1, k4 = k2 * k2;
@@ -330,12 +377,13 @@ __global__ void __launch_bounds__(TPB, MINB)
       for (int k = 0; k < L; ++k) {
         if (c0 + lane + 32 * k < W) {
           const double dx = dx0 + 32.0 * k;
-          point(exp(-(dx * (ga * dx + gb2 * dy) + gc * (dy * dy))), dx, zc[k]);
+          point(exp(-(dx * (ga * dx + gb2 * dy) + gc * (dy * dy))), dx, zat(k));
         }
       }
     }
+    stage = (stage + 1 == (ASYNC ? STAGES : 1)) ? 0 : stage + 1;
   }
-  if (c_begin < c_end) fold((double)(cur_row + a.row0) - y0);
+  if (c_begin < c_end) fold((double)(cur_row + row0) - y0);
 
   // block partial of the moment vector
   __shared__ double red[TPB / 32][MomLayout::KS];
