@@ -13,6 +13,7 @@ import argparse
 import concurrent.futures as cf
 import glob
 import os
+import re
 import shutil
 import subprocess
 import sys
@@ -35,9 +36,19 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found: the CUDA toolkit is required to build libjfb200.so")
 
 
-def _headers():
-    return glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) + \
-        glob.glob(os.path.join(ROOT, "include", "*.h"))
+def _deps(path: str, seen: set | None = None) -> set:
+    """Files a unit includes (quoted #include, recursively): a header edit
+    recompiles only the units that include it."""
+    seen = set() if seen is None else seen
+    with open(path) as f:
+        for line in f:
+            mt = re.match(r'\s*#\s*include\s+"([^"]+)"', line)
+            if mt:
+                dep = os.path.normpath(os.path.join(os.path.dirname(path), mt.group(1)))
+                if os.path.exists(dep) and dep not in seen:
+                    seen.add(dep)
+                    _deps(dep, seen)
+    return seen
 
 
 def _stale(src: str, obj: str, hdr_mtime: float) -> bool:
@@ -60,12 +71,12 @@ def _compile(src: str, obj: str, verbose: bool) -> str:
 def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -> str:
     os.makedirs(OBJ, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
-    hdr_mtime = max((os.path.getmtime(h) for h in _headers()), default=0.0)
     todo = []
     objs = []
     for s in srcs:
         o = os.path.join(OBJ, os.path.basename(s)[:-3] + ".o")
         objs.append(o)
+        hdr_mtime = max((os.path.getmtime(h) for h in _deps(s)), default=0.0)
         if force or _stale(s, o, hdr_mtime):
             todo.append((s, o))
     if todo:

@@ -60,6 +60,7 @@ struct PassArgs {
   const double* precond; // EPI_NONE TSQR second pass: P = R1^-1, (n+1)^2 row-major upper triangular
   int32_t use_comm;     // 1: combine across ranks through the mailboxes
   int32_t no_chain;     // debug (JF_DEBUG_NOCHAIN): return the Gram in the alt coordinates (a, 2b, c2)
+  unsigned long long* dbg; // debug (JF_DEBUG_STAMPS): per-warp [smid, t_start, t_loop_end, t_exit] (moment kernel)
   CommDev comm;
 };
 

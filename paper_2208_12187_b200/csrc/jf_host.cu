@@ -535,6 +535,12 @@ static int pass_common(int32_t model, const double* y, const double* z, int64_t 
   fill_args(a, sg, m, o);
   a.epilogue = EPI_NONE;
   a.no_chain = getenv("JF_DEBUG_NOCHAIN") ? 1 : 0;
+  const char* stamps = residual_only ? nullptr : getenv("JF_DEBUG_STAMPS");  // development aid: per-warp timeline
+  static unsigned long long* d_dbg = nullptr;
+  constexpr int DBG_N = 4 * 16384;
+  if (stamps && !d_dbg) CK(cudaMalloc(&d_dbg, sizeof(unsigned long long) * DBG_N));
+  a.dbg = stamps ? d_dbg : nullptr;
+  if (stamps) CK(cudaMemsetAsync(d_dbg, 0, sizeof(unsigned long long) * DBG_N, s));
   if (x_on_device) {
     a.x = x;
   } else {
@@ -553,6 +559,15 @@ static int pass_common(int32_t model, const double* y, const double* z, int64_t 
   CK(cudaMemcpyAsync(c->d_args, &a, sizeof(a), cudaMemcpyHostToDevice, s));
   r = launch_pass(k, !residual_only, s, c->d_args, c->d_state);
   if (r) return r;
+  if (stamps) {
+    static unsigned long long h_dbg[DBG_N];
+    CK(cudaMemcpyAsync(h_dbg, d_dbg, sizeof(h_dbg), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (FILE* f = fopen(stamps, "wb")) {
+      fwrite(h_dbg, sizeof(h_dbg), 1, f);
+      fclose(f);
+    }
+  }
   if (host_out) {
     const int KS = residual_only ? 2 : tri_count(n) + 1;
     CK(cudaMemcpyAsync(host_out, a.out, sizeof(double) * KS, cudaMemcpyDeviceToHost, s));
@@ -704,6 +719,7 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
   fill_args(a, sg, m, o);
   a.epilogue = EPI_FIT;
   a.no_chain = 0;
+  a.dbg = nullptr;
   a.partials = c->d_partials;
   a.ticket = c->d_ticket;
   a.out = c->d_out;

@@ -22,13 +22,22 @@ static Kernels make() {
   k.rtpb = PassCfg<ModelGauss2DRot, false>::TPB;
   return k;
 }
-template <int L, int TPB, int MINB, int SEEDN = 4, int STAGES = 0>
+template <int L, int TPB, int MINB, int SEEDN = 4, int STG = 0>
 static void use_moment(Kernels& k) {
-  auto f = moment_pass_kernel<L, TPB, MINB, SEEDN, STAGES>;
+  auto f = moment_pass_kernel<L, TPB, MINB, SEEDN, STG>;
   k.jk = f;
   k.jtpb = TPB;
-  k.jsmem = moment_zbuf_bytes(L, TPB, STAGES);
+  k.jsmem = moment_smem_bytes(L, TPB, STG);
   if (k.jsmem > 0) cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, k.jsmem);
+}
+
+template <int L, int TC, int NW, int SEEDN = 4>
+static void use_task(Kernels& k) {
+  auto f = moment_task_kernel<L, TC, NW, SEEDN>;
+  k.jk = f;
+  k.jtpb = NW * 32;
+  k.jsmem = moment_task_smem_bytes(NW);
+  cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, k.jsmem);
 }
 
 Kernels kernels_gauss2d(int coord) {
@@ -39,15 +48,21 @@ Kernels kernels_gauss2d(int coord) {
     if (const char* v = getenv("JF_JVARIANT")) {  // development aid: alternative shapes
       const int var = atoi(v);
       if (var == 9) { k.jk = pass_kernel<ModelGauss2DRot, true, COORD_GRID, false>; k.jtpb = 256; k.jsmem = 0; }  // dual numbers
-      if (var == 11) use_moment<8, 128, 3>(k);
-      if (var == 12) use_moment<8, 128, 4>(k);
-      if (var == 13) use_moment<16, 128, 3, 8>(k);
-      if (var == 20) use_moment<16, 128, 3, 4, 2>(k);
-      if (var == 21) use_moment<16, 128, 3, 4, 3>(k);
-      if (var == 22) use_moment<8, 128, 4, 4, 2>(k);
-      if (var == 23) use_moment<8, 128, 4, 4, 3>(k);
-      if (var == 24) use_moment<16, 128, 4, 4, 2>(k);
-      if (var == 25) use_moment<8, 128, 5, 4, 2>(k);
+      if (var == 11) use_moment<8, 128, 4>(k);
+      if (var == 30) use_task<16, 4, 12>(k);
+      if (var == 31) use_task<16, 2, 12>(k);
+      if (var == 32) use_task<16, 4, 16>(k);
+      if (var == 33) use_task<16, 8, 12>(k);
+      if (var == 34) use_task<8, 8, 16>(k);
+      if (var == 35) use_task<32, 2, 8, 2>(k);
+      if (var == 13) use_moment<32, 128, 2, 2>(k);
+      if (var == 20) use_moment<16, 128, 3, 4, 3>(k);
+      if (var == 21) use_moment<16, 128, 3, 4, 4>(k);
+      if (var == 22) use_moment<8, 128, 4, 8, 4>(k);
+      if (var == 23) use_moment<8, 128, 4, 8, 6>(k);
+      if (var == 24) use_moment<16, 256, 1, 4, 3>(k);
+      if (var == 25) use_moment<32, 128, 2, 2, 3>(k);
+      if (var == 26) use_moment<16, 128, 2, 4, 6>(k);
     }
   }
   return k;

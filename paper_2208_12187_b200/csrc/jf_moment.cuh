@@ -32,11 +32,6 @@
 
 namespace jf {
 
-// dynamic shared memory of moment_pass_kernel (the cp.async z ring)
-__host__ __device__ constexpr int moment_zbuf_bytes(int L, int TPB, int STAGES) {
-  return STAGES >= 2 ? (TPB / 32) * STAGES * L * 32 * 8 : 0;
-}
-
 // Moment vector layout: M2 (15) | M1 (6) | MR (6) | sum r | sum r^2 | bad
 struct MomLayout {
   static constexpr int N2 = 15, N1 = 6;
@@ -117,29 +112,64 @@ __device__ __noinline__ void moment_finish(const PassArgs& a, FitState* __restri
     }
   };
   stamp();
+  dbg_tail(a, 3);
   double xv[N];
 #pragma unroll
   for (int j = 0; j < N; ++j) xv[j] = xs[j];
   const auto pre = Model::template prologue<true>(xv);
   stamp();
+  dbg_tail(a, 4);
   moments_to_kvec(pre.g, (double)a.m, mom, vec);
   if (threadIdx.x == 0) vec[KT] = mom[MomLayout::NV];  // non-finite count
   __syncthreads();
   stamp();
+  dbg_tail(a, 5);
   if (!a.no_chain) apply_chain_kvec<Model, TPB>(pre, vec, scratch);
   stamp();
+  dbg_tail(a, 6);
   pass_tail<KS, TPB, true>(a, st, vec, cond, use_cond);
+  dbg_tail(a, 7);
 }
 
-template <int L, int TPB, int MINB, int SEEDN = 4, int STAGES = 0>
+// dynamic shared memory of moment_pass_kernel<.., STG> (the z ring; reused
+// for the block-partial table after the main loop)
+__host__ __device__ constexpr int moment_smem_bytes(int L, int TPB, int STG) {
+  return STG > 0 ? ((TPB / 32) * STG * 32 * L * 8 > MomLayout::KS * (TPB + 1) * 8
+                        ? (TPB / 32) * STG * 32 * L * 8
+                        : MomLayout::KS * (TPB + 1) * 8)
+                 : 0;
+}
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  const unsigned a = smem_u32(bar);
+  unsigned done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+// STG == 0: each lane prefetches its points of the next chunk into registers.
+// STG >= 2: z streams through a per-warp ring of STG chunk slots in shared
+// memory, filled by TMA bulk copies (cp.async.bulk, one 32 L x 8 B copy per
+// chunk, completion on an mbarrier per slot) issued STG - 1 chunks ahead by
+// lane 0; the row moments then live in registers and the ring doubles as the
+// block-partial table at the end.
+template <int L, int TPB, int MINB, int SEEDN = 4, int STG = 0>
 __global__ void __launch_bounds__(TPB, MINB)
     moment_pass_kernel(const PassArgs* __restrict__ pa, FitState* __restrict__ st, cudaGraphConditionalHandle cond,
                        int use_cond) {
   using Model = ModelGauss2DRot;
-  constexpr int N = Model::N, KT = tri_count(N), KS = KT + 1;
+  constexpr int N = Model::N;
   constexpr int NV = MomLayout::NV;
   constexpr int CW = 32 * L;
   constexpr double D = 32.0;
+  constexpr bool TMA = STG >= 2;
+  constexpr int NF = MomLayout::OSR;  // folded moments per thread (27)
   const PassArgs& a = *pa;
   if (!pass_begin<true, false>(a, st)) return;
   const double* xs = (a.epilogue == EPI_FIT) ? st->x_eval : a.x;
@@ -152,14 +182,32 @@ __global__ void __launch_bounds__(TPB, MINB)
     A = pre.g.A, off = pre.off, ga = pre.g.a, gb2 = pre.g.b2, gc = pre.g.c, x0 = pre.g.x0, y0 = pre.g.y0;
   }
 
-  // per-thread moments with dy folded in: shared memory, one column per
-  // thread (updated once per image row a lane visits; keeps the registers for
-  // the per-point work and more resident warps)
-  __shared__ double smom[MomLayout::KS][TPB + 1];  // + sum r, sum r^2, bad at the end; padded rows
+  // per-thread moments with dy folded in.  STG == 0: shared memory, one
+  // column per thread (updated once per image row a lane visits; keeps the
+  // registers for the z prefetch); STG >= 2: registers.
+  extern __shared__ __align__(128) double dyn[];
+  __shared__ double smom_s[TMA ? 1 : MomLayout::KS][TMA ? 1 : TPB + 1];  // + sum r, sum r^2, bad; padded rows
+  auto smom = [&](int i, int t) -> double& {
+    if constexpr (TMA) return dyn[i * (TPB + 1) + t];
+    else return smom_s[i][t];
+  };
   const int tid = threadIdx.x;
+  double Mf[TMA ? NF : 1];
 #pragma unroll
-  for (int i = 0; i < MomLayout::OSR; ++i) smom[i][tid] = 0.0;
+  for (int i = 0; i < NF; ++i) {
+    if constexpr (TMA) Mf[i] = 0.0;
+    else smom(i, tid) = 0.0;
+  }
+  auto macc = [&](int i) -> double& {
+    if constexpr (TMA) return Mf[i];
+    else return smom(i, tid);
+  };
   double sr = 0.0, srr = 0.0;
+  // The lane's running moments of the current image row, about a moving
+  // origin o (the dx of the lane's first pixel of the current chunk):
+  //   P[p] = sum u^2 t^p, Q[p] = sum u t^p, R[p] = sum u r t^p,  t = dx - o.
+  // Within a chunk t = D k (k = step index), so every t^p is a compile-time
+  // constant; moving the origin to the next chunk (o += CW) is a Taylor shift.
   double P[5], Q[3], R[3];
 #pragma unroll
   for (int i = 0; i < 5; ++i) P[i] = 0.0;
@@ -167,7 +215,24 @@ __global__ void __launch_bounds__(TPB, MINB)
   for (int i = 0; i < 3; ++i) Q[i] = R[i] = 0.0;
   int bad = 0;
 
-  auto fold = [&](double dy) {  // row moments x dy^q into the thread's moments
+  // moments about o -> about o - d:  M'_p = sum_i C(p, i) d^(p-i) M_i
+  // (Pascal scheme: for j = 1..deg, for p = deg..j: M_p += d M_(p-1))
+  auto shift = [&](double d) {
+#pragma unroll
+    for (int j = 1; j <= 4; ++j)
+#pragma unroll
+      for (int p = 4; p >= j; --p) P[p] = fma(d, P[p - 1], P[p]);
+#pragma unroll
+    for (int j = 1; j <= 2; ++j)
+#pragma unroll
+      for (int p = 2; p >= j; --p) {
+        Q[p] = fma(d, Q[p - 1], Q[p]);
+        R[p] = fma(d, R[p - 1], R[p]);
+      }
+  };
+  double org = 0.0;  // o of the running row moments
+  auto fold = [&](double dy) {  // row moments (about dx = 0) x dy^q into the thread's moments
+    shift(org);
     double dq[5];
     dq[0] = 1.0;
     dq[1] = dy;
@@ -178,16 +243,16 @@ __global__ void __launch_bounds__(TPB, MINB)
     for (int q = 0; q <= 4; ++q)
 #pragma unroll
       for (int p = 0; p + q <= 4; ++p) {
-        double& m2 = smom[MomLayout::O2 + mono(4, p, q)][tid];
+        double& m2 = macc(MomLayout::O2 + mono(4, p, q));
         m2 = fma(P[p], dq[q], m2);
       }
 #pragma unroll
     for (int q = 0; q <= 2; ++q)
 #pragma unroll
       for (int p = 0; p + q <= 2; ++p) {
-        double& m1 = smom[MomLayout::O1 + mono(2, p, q)][tid];
+        double& m1 = macc(MomLayout::O1 + mono(2, p, q));
         m1 = fma(Q[p], dq[q], m1);
-        double& mr = smom[MomLayout::OR + mono(2, p, q)][tid];
+        double& mr = macc(MomLayout::OR + mono(2, p, q));
         mr = fma(R[p], dq[q], mr);
       }
 #pragma unroll
@@ -195,28 +260,24 @@ __global__ void __launch_bounds__(TPB, MINB)
 #pragma unroll
     for (int i = 0; i < 3; ++i) Q[i] = R[i] = 0.0;
   };
-  // one point: u = exp(-q), dx, data z
-  auto point = [&](double u, double dx, double z) {
+  // one point at t = D k from the origin: u = exp(-q), data z
+  auto point = [&](double u, double t, double z) {
     const double r = fma(A, u, off) - z;  // Eq. 1: r = h - z
     bad += isfinite(r) ? 0 : 1;
     const double u2 = u * u;
+    const double t2 = t * t;
     P[0] += u2;
-    P[1] = fma(u2, dx, P[1]);
-    const double t1 = u2 * dx;
-    P[2] = fma(t1, dx, P[2]);
-    const double t2 = t1 * dx;
-    P[3] = fma(t2, dx, P[3]);
-    const double t3 = t2 * dx;
-    P[4] = fma(t3, dx, P[4]);
+    P[1] = fma(u2, t, P[1]);
+    P[2] = fma(u2, t2, P[2]);
+    P[3] = fma(u2, t2 * t, P[3]);
+    P[4] = fma(u2, t2 * t2, P[4]);
     Q[0] += u;
-    Q[1] = fma(u, dx, Q[1]);
-    const double v1 = u * dx;
-    Q[2] = fma(v1, dx, Q[2]);
+    Q[1] = fma(u, t, Q[1]);
+    Q[2] = fma(u, t2, Q[2]);
     const double ur = u * r;
     R[0] += ur;
-    R[1] = fma(ur, dx, R[1]);
-    const double w1 = ur * dx;
-    R[2] = fma(w1, dx, R[2]);
+    R[1] = fma(ur, t, R[1]);
+    R[2] = fma(ur, t2, R[2]);
     sr += r;
     srr = fma(r, r, srr);
   };
@@ -232,47 +293,78 @@ __global__ void __launch_bounds__(TPB, MINB)
   const int64_t c_begin = gw * nch / nwt, c_end = (gw + 1) * nch / nwt;
   const double rho = exp(-2.0 * ga * D * D);
   const double* __restrict__ z = a.z;
-  // z staging.  STAGES == 0: the next chunk is prefetched into registers.
-  // STAGES >= 2: each lane streams its own points of the next STAGES - 1
-  // chunks into a per-warp shared-memory ring with cp.async (LDGSTS,
-  // evict-first in L2), freeing the registers for the arithmetic.
-  constexpr bool ASYNC = STAGES >= 2;
-  extern __shared__ __align__(16) double zbuf[];  // dynamic: moment_zbuf_bytes(L, TPB, STAGES)
-  double* wz = zbuf + (ASYNC ? (threadIdx.x >> 5) * STAGES * L * 32 : 0);
+  auto dbg_stamp = [&](int slot) {  // development aid (JF_DEBUG_STAMPS)
+    if (a.dbg && lane == 0 && gw < 16384) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      a.dbg[gw * 4 + 0] = smid;
+      a.dbg[gw * 4 + slot] = t;
+    }
+  };
+  dbg_stamp(1);
+
+  // ---- z staging
+  double zn[TMA ? 1 : L];  // STG == 0: the next chunk's points
+  constexpr int NWB = TPB / 32;
+  __shared__ __align__(8) unsigned long long mbar[TMA ? NWB * STG : 1];
+  double* ring = dyn + (TMA ? (threadIdx.x >> 5) * STG * CW : 0);
+  unsigned long long* wbar = mbar + (TMA ? (threadIdx.x >> 5) * STG : 0);
+  unsigned direct = 0;  // TMA: slot s holds no copy (ragged or unaligned chunk: read from global)
+  unsigned parity = 0;  // TMA: mbarrier phase parity per slot
+  const bool z_al16 = (reinterpret_cast<uintptr_t>(z) & 15) == 0;
   unsigned long long pol = 0;
-  if constexpr (ASYNC) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  double zn[ASYNC ? 1 : L];
+  if constexpr (TMA) {
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    if (lane == 0) {
+#pragma unroll
+      for (int s = 0; s < STG; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(wbar + s)));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+  }
   // chunk ch = row * cpr + cc; row and cc are advanced incrementally (no
   // 64-bit division in the loop)
   int64_t lrow = c_begin / cpr;  // position of the next chunk to load
   int lcc = (int)(c_begin - lrow * cpr);
-  auto load = [&](int stage) {
-    const int col = lcc * CW + lane;
-    const double* zp = z + lrow * (int64_t)W + col;
-    if constexpr (ASYNC) {
-#pragma unroll
-      for (int k = 0; k < L; ++k) {
-        const bool v = col + 32 * k < W;
-        const unsigned dst = (unsigned)__cvta_generic_to_shared(wz + (stage * L + k) * 32 + lane);
-        asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2, %3;" ::"r"(dst),
-                     "l"(v ? zp + 32 * k : z), "r"(v ? 8 : 0), "l"(pol)
-                     : "memory");
+  auto load = [&](int slot) {
+    const int c0l = lcc * CW;
+    const int64_t g0 = lrow * (int64_t)W + c0l;
+    if constexpr (TMA) {
+      if (c0l + CW <= W && z_al16 && (g0 & 1) == 0) {  // warp-uniform
+        direct &= ~(1u << slot);
+        if (lane == 0) {
+          const unsigned b = smem_u32(wbar + slot);
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(CW * 8) : "memory");
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
+              "%4;" ::"r"(smem_u32(ring + slot * CW)),
+              "l"(z + g0), "r"(CW * 8), "r"(b), "l"(pol)
+              : "memory");
+        }
+      } else {
+        direct |= 1u << slot;
       }
     } else {
+      const double* zp = z + g0 + lane;
+      if (c0l + CW <= W) {  // warp-uniform
 #pragma unroll
-      for (int k = 0; k < L; ++k) zn[k] = (col + 32 * k < W) ? __ldcs(zp + 32 * k) : 0.0;
+        for (int k = 0; k < L; ++k) zn[k] = __ldcs(zp + 32 * k);
+      } else {
+#pragma unroll
+        for (int k = 0; k < L; ++k) zn[k] = (c0l + lane + 32 * k < W) ? __ldcs(zp + 32 * k) : 0.0;
+      }
     }
     if (++lcc == cpr) {
       lcc = 0;
       ++lrow;
     }
   };
-  if constexpr (ASYNC) {
+  if constexpr (TMA) {
 #pragma unroll
-    for (int s = 0; s < STAGES - 1; ++s) {
+    for (int s = 0; s < STG; ++s)
       if (c_begin + s < c_end) load(s);
-      asm volatile("cp.async.commit_group;" ::: "memory");
-    }
   } else {
     if (c_begin < c_end) load(0);
   }
@@ -282,24 +374,14 @@ __global__ void __launch_bounds__(TPB, MINB)
   double E = 0.0, Rr = 0.0;
   bool carried = false;
   int since_seed = 0;
-  int stage = 0;
+  int slot = 0;
   for (int64_t ch = c_begin; ch < c_end; ++ch) {
-    double zc[ASYNC ? 1 : L];
-    const double* zs = wz + stage * L * 32 + lane;  // ASYNC: this chunk's points, stride 32
-    if constexpr (ASYNC) {
-      const int nxt = stage == 0 ? STAGES - 1 : stage - 1;  // the slot consumed last iteration
-      if (ch + STAGES - 1 < c_end) load(nxt);
-      asm volatile("cp.async.commit_group;" ::: "memory");
-      asm volatile("cp.async.wait_group %0;" ::"n"(STAGES - 1) : "memory");
-    } else {
+    double zc[TMA ? 1 : L];
+    if constexpr (!TMA) {
 #pragma unroll
       for (int k = 0; k < L; ++k) zc[k] = zn[k];
       if (ch + 1 < c_end) load(0);  // prefetch the next chunk
     }
-    auto zat = [&](int k) -> double {
-      if constexpr (ASYNC) return zs[32 * k];
-      else return zc[k];
-    };
     if (++cc == cpr) {
       cc = 0;
       ++row;
@@ -312,78 +394,110 @@ __global__ void __launch_bounds__(TPB, MINB)
     const int c0 = cc * CW;
     const double dy = (double)(row + row0) - y0;
     const double dx0 = (double)(c0 + lane) - x0;
+    const double* zrow = z + row * (int64_t)W + c0 + lane;  // this lane's first point of the chunk (global)
+    const double* zsl = ring + slot * CW + lane;           // ... in the ring (TMA)
+    bool from_ring = false;
+    if constexpr (TMA) {
+      if (!((direct >> slot) & 1u)) {
+        mbar_wait(wbar + slot, (parity >> slot) & 1u);
+        parity ^= 1u << slot;
+        from_ring = true;
+      }
+    }
+    // origin of the running moments -> this chunk's first pixel (zero
+    // moments after a fold shift to zero)
+    shift(-(double)CW);
+    org = dx0;
     const double q0 = dx0 * (ga * dx0 + gb2 * dy) + gc * (dy * dy);
     const double argR = D * (2.0 * ga * dx0 + gb2 * dy) + ga * D * D;
     const bool ok = fabs(q0) < 600.0 && fabs(argR) < 300.0 && 2.0 * ga * D * D * L < 300.0;
     const bool full = c0 + CW <= W;  // warp-uniform
-    if (full && __all_sync(FULL, ok)) {
+    // the chunk: recurrence for u, moments in t = D k (compile-time t^p)
+    auto chunk = [&](auto zat) {
       // E, Rr continue from the previous chunk of the same row (its last
       // step lands on this chunk's first pixel); re-seeded by exp at a row
       // start, after a direct-evaluation chunk, and every SEEDN chunks so the
-      // recurrence's rounding stays below ~(16 SEEDN)^2 / 2 ulp
+      // recurrence's rounding stays below ~(L SEEDN)^2 / 2 ulp
       if (!carried || ++since_seed >= SEEDN) {  // warp-uniform
         E = exp(-q0);
         Rr = exp(-argR);
         since_seed = 0;
       }
-      // moments in the local step index k (dx = dx0 + D k): the k^p are
-      // compile-time constants, so each update is one FMA
-      double a2[5] = {0.0, 0.0, 0.0, 0.0, 0.0}, a1[3] = {0.0, 0.0, 0.0}, ar[3] = {0.0, 0.0, 0.0};
+      // the chunk's sum r^2 doubles as its non-finite test (any non-finite
+      // r makes it non-finite; the exact count is then taken below)
+      double cs = 0.0;
+      const double E_in = E, R_in = Rr;
 #pragma unroll
       for (int k = 0; k < L; ++k) {
         const double u = E;
         const double r = fma(A, u, off) - zat(k);  // Eq. 1: r = h - z
-        bad += isfinite(r) ? 0 : 1;
         const double u2 = u * u;
-        const double k1 = (double)k, k2 = k1 * k1, k3 = k2 * k1, k4 = k2 * k2;
-        a2[0] += u2;
-        a2[1] = fma(u2, k1, a2[1]);
-        a2[2] = fma(u2, k2, a2[2]);
-        a2[3] = fma(u2, k3, a2[3]);
-        a2[4] = fma(u2, k4, a2[4]);
-        a1[0] += u;
-        a1[1] = fma(u, k1, a1[1]);
-        a1[2] = fma(u, k2, a1[2]);
+        const double k1 = D * k, k2 = k1 * k1, k3 = k2 * k1, k4 = k2 * k2;
         const double ur = u * r;
-        ar[0] += ur;
-        ar[1] = fma(ur, k1, ar[1]);
-        ar[2] = fma(ur, k2, ar[2]);
+        P[0] += u2;
+        Q[0] += u;
+        R[0] += ur;
+        if (k > 0) {
+          P[1] = fma(u2, k1, P[1]);
+          P[2] = fma(u2, k2, P[2]);
+          P[3] = fma(u2, k3, P[3]);
+          P[4] = fma(u2, k4, P[4]);
+          Q[1] = fma(u, k1, Q[1]);
+          Q[2] = fma(u, k2, Q[2]);
+          R[1] = fma(ur, k1, R[1]);
+          R[2] = fma(ur, k2, R[2]);
+        }
         sr += r;
-        srr = fma(r, r, srr);
+        cs = fma(r, r, cs);
         E *= Rr;
         Rr *= rho;
       }
       carried = true;
-      // shift to dx: sum w (dx0 + D k)^p = sum_i C(p, i) dx0^(p-i) D^i sum w k^i
-      const double d1 = dx0, d2 = d1 * d1, d3 = d2 * d1, d4 = d2 * d2;
-      const double s1 = D * a2[1], s2 = (D * D) * a2[2], s3 = (D * D * D) * a2[3], s4 = (D * D * D * D) * a2[4];
-      P[0] += a2[0];
-      P[1] += fma(d1, a2[0], s1);
-      P[2] += fma(d2, a2[0], fma(2.0 * d1, s1, s2));
-      P[3] += fma(d3, a2[0], fma(3.0 * d2, s1, fma(3.0 * d1, s2, s3)));
-      P[4] += fma(d4, a2[0], fma(4.0 * d3, s1, fma(6.0 * d2, s2, fma(4.0 * d1, s3, s4))));
-      const double t1 = D * a1[1], t2 = (D * D) * a1[2];
-      Q[0] += a1[0];
-      Q[1] += fma(d1, a1[0], t1);
-      Q[2] += fma(d2, a1[0], fma(2.0 * d1, t1, t2));
-      const double v1 = D * ar[1], v2 = (D * D) * ar[2];
-      R[0] += ar[0];
-      R[1] += fma(d1, ar[0], v1);
-      R[2] += fma(d2, ar[0], fma(2.0 * d1, v1, v2));
+      srr += cs;
+      if (!isfinite(cs)) {  // rare: replay the chunk's residuals and count the non-finite ones
+        double e = E_in, rr = R_in;
+#pragma unroll
+        for (int k = 0; k < L; ++k) {
+          bad += isfinite(fma(A, e, off) - zat(k)) ? 0 : 1;
+          e *= rr;
+          rr *= rho;
+        }
+      }
+    };
+    if (full && __all_sync(FULL, ok)) {
+      if constexpr (TMA) {
+        if (from_ring) chunk([&](int k) { return zsl[32 * k]; });
+        else chunk([&](int k) { return __ldcs(zrow + 32 * k); });
+      } else {
+        chunk([&](int k) { return zc[k]; });
+      }
     } else {
       // ragged row end or unsafe exponent range: direct evaluation
       carried = false;
 #pragma unroll
       for (int k = 0; k < L; ++k) {
         if (c0 + lane + 32 * k < W) {
-          const double dx = dx0 + 32.0 * k;
-          point(exp(-(dx * (ga * dx + gb2 * dy) + gc * (dy * dy))), dx, zat(k));
+          const double dx = dx0 + D * k;
+          double zk;
+          if constexpr (TMA) zk = from_ring ? zsl[32 * k] : __ldcs(zrow + 32 * k);
+          else zk = zc[k];
+          point(exp(-(dx * (ga * dx + gb2 * dy) + gc * (dy * dy))), D * k, zk);
         }
       }
     }
-    stage = (stage + 1 == (ASYNC ? STAGES : 1)) ? 0 : stage + 1;
+    if constexpr (TMA) {
+      __syncwarp();  // every lane has read the slot: refill it STG chunks ahead
+      if (ch + STG < c_end) load(slot);
+      slot = (slot + 1 == STG) ? 0 : slot + 1;
+    }
   }
   if (c_begin < c_end) fold((double)(cur_row + row0) - y0);
+  dbg_stamp(2);
+  if constexpr (TMA) {
+    __syncthreads();  // the ring becomes the block-partial table
+#pragma unroll
+    for (int i = 0; i < NF; ++i) smom(i, tid) = Mf[i];
+  }
 
   // block partial of the moment vector
   __shared__ double red[TPB / 32][MomLayout::KS];
@@ -393,9 +507,9 @@ __global__ void __launch_bounds__(TPB, MINB)
   {
     // block partial: the threads' columns of smom summed by rows, NSEG
     // segments of 32 threads each, then the segments in order
-    smom[MomLayout::OSR][tid] = sr;
-    smom[MomLayout::OSRR][tid] = srr;
-    smom[NV][tid] = (double)bad;
+    smom(MomLayout::OSR, tid) = sr;
+    smom(MomLayout::OSRR, tid) = srr;
+    smom(NV, tid) = (double)bad;
     __syncthreads();
     constexpr int NSEG = TPB / 32;
     static_assert(NSEG * MomLayout::KS <= TPB, "one (row, segment) per thread");
@@ -403,7 +517,7 @@ __global__ void __launch_bounds__(TPB, MINB)
       const int i = tid % MomLayout::KS, seg = tid / MomLayout::KS;
       double s = 0.0;
 #pragma unroll 8
-      for (int j = 0; j < 32; ++j) s += smom[i][seg * 32 + j];
+      for (int j = 0; j < 32; ++j) s += smom(i, seg * 32 + j);
       red[seg][i] = s;
     }
     __syncthreads();
@@ -414,8 +528,390 @@ __global__ void __launch_bounds__(TPB, MINB)
       a.partials[(size_t)blockIdx.x * MomLayout::KS + k] = s;
     }
   }
+  dbg_stamp(3);
   if (!grid_reduce<MomLayout::KS, TPB>(a, mom, scratch)) return;
   moment_finish<TPB>(a, st, xs, mom, vec, scratch, cond, use_cond);
+  if (a.dbg && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.dbg[4 * 16384 - 1] = t;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Task-scheduled moment J-pass (the production kernel for the north-star
+// configuration).  One block per SM (NW warps).  The block's share of the
+// image is a fixed, contiguous range of TASKS — runs of up to TC chunks
+// (32 L pixels each) of one image row — and the warps take tasks from a
+// shared-memory counter as they become free, so the SM's warps finish
+// together however the warp scheduler shares the FP64 pipe among them
+// (with a static per-warp split, the fastest and slowest warps of an SM
+// differed 2x).  The result does not depend on which warp ran a task: every
+// task starts from zero moments and a fresh exp seed, its per-lane moments
+// are summed across the warp in lane order and written, folded with dy, to
+// the task's own slot; the block partial sums the slots in task order.
+// Single-level grid combine (one partial per SM).
+constexpr int MOMENT_MAXT = 112;  // task slots per block of moment_task_kernel
+__host__ __device__ constexpr int moment_task_smem_bytes(int NW) {
+  return (MOMENT_MAXT * MomLayout::KS + NW * 13 * 33) * 8;
+}
+template <int L, int TC, int NW, int SEEDN = 4>
+__global__ void __launch_bounds__(NW * 32, 1)
+    moment_task_kernel(const PassArgs* __restrict__ pa, FitState* __restrict__ st, cudaGraphConditionalHandle cond,
+                       int use_cond) {
+  using Model = ModelGauss2DRot;
+  using Pre = typename Model::Pre;
+  constexpr int N = Model::N, KT = tri_count(N), KS2 = KT + 1;
+  constexpr int TPB = NW * 32;
+  constexpr int KS = MomLayout::KS, NV = MomLayout::NV;
+  constexpr int CW = 32 * L;
+  constexpr int MAXT = MOMENT_MAXT;
+  constexpr double D = 32.0;
+  const PassArgs& a = *pa;
+  if (!pass_begin<true, false>(a, st)) return;
+  const double* xs = (a.epilogue == EPI_FIT) ? st->x_eval : a.x;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+
+  extern __shared__ __align__(16) double dyn_task[];  // moment_task_smem_bytes(NW)
+  double (*tslot)[KS] = reinterpret_cast<double (*)[KS]>(dyn_task);                 // [MAXT][KS] per-task vectors
+  double (*wred)[13][33] = reinterpret_cast<double (*)[13][33]>(dyn_task + MAXT * KS);  // [NW]: lane-sum transpose
+  __shared__ double red[TPB / 32 > 0 ? NW : 1][KS];
+  __shared__ double vec[KMAX];
+  __shared__ double scratch[combine_scratch(TPB)];
+  __shared__ double mom[KS];
+  __shared__ Pre pre_s;                     // chain-rule blocks for the finish (warp 0)
+  __shared__ int next_task;
+  __shared__ double binom[5][5];            // C(p, i)
+
+  double A, off, ga, gb2, gc, x0, y0;
+  {
+    double xv[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) xv[j] = xs[j];
+    const auto pre = Model::template prologue<false>(xv);
+    A = pre.g.A, off = pre.off, ga = pre.g.a, gb2 = pre.g.b2, gc = pre.g.c, x0 = pre.g.x0, y0 = pre.g.y0;
+  }
+  if (tid == 0) next_task = 0;
+  if (tid < 25) {
+    const int p = tid / 5, i = tid % 5;
+    double c = 0.0;
+    if (i <= p) {
+      c = 1.0;
+      for (int j = 0; j < i; ++j) c = c * (p - j) / (j + 1);
+    }
+    binom[p][i] = c;
+  }
+  __syncthreads();
+  // lane -> entry of the moment vector it folds at a task end: family row
+  // base in the lane-sum table, dx power p, dy power q (MomLayout order)
+  int f_base = 0, f_p = 0, f_q = 0;
+  if (lane < MomLayout::OSR) {
+    int deg, idx;
+    if (lane < MomLayout::O1) f_base = 0, deg = 4, idx = lane;
+    else if (lane < MomLayout::OR) f_base = 5, deg = 2, idx = lane - MomLayout::O1;
+    else f_base = 8, deg = 2, idx = lane - MomLayout::OR;
+    f_p = idx;
+    while (f_p > deg - f_q) {
+      f_p -= deg - f_q + 1;
+      ++f_q;
+    }
+  }
+
+  // ---- the block's tasks
+  const int W = (int)a.W;
+  const int64_t H = a.m / a.W;
+  const int64_t row0 = a.row0;
+  const int cpr = (W + CW - 1) / CW;
+  const int nblk = gridDim.x;
+  // task length: TC chunks, longer when the block would get more than MAXT tasks
+  int tcr = TC < cpr ? TC : cpr;
+  while (((H * (int64_t)((cpr + tcr - 1) / tcr)) + nblk - 1) / nblk > MAXT) ++tcr;
+  const int tpr = (cpr + tcr - 1) / tcr;  // tasks per row
+  const int64_t ntask = H * (int64_t)tpr;
+  const int64_t t_begin = (int64_t)blockIdx.x * ntask / nblk, t_end = (int64_t)(blockIdx.x + 1) * ntask / nblk;
+  const int nt = (int)(t_end - t_begin);
+
+  const double rho = exp(-2.0 * ga * D * D);
+  const double* __restrict__ z = a.z;
+  if (a.dbg && lane == 0 && blockIdx.x * NW + wid < 16384) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    a.dbg[(blockIdx.x * NW + wid) * 4 + 0] = smid;
+    a.dbg[(blockIdx.x * NW + wid) * 4 + 1] = t;
+  }
+
+  // warp 0 computes the finish's chain-rule blocks first (any block may be
+  // the last one); the task counter balances its late start
+  if (wid == 0) {
+    double xv[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) xv[j] = xs[j];
+    const auto pre = Model::template prologue<true>(xv);
+    if (lane == 0) pre_s = pre;
+  }
+
+  double P[5], Q[3], R[3], sr, srr;
+  int bad;
+  auto shift = [&](double d) {  // moments about o -> about o - d (Pascal scheme)
+#pragma unroll
+    for (int j = 1; j <= 4; ++j)
+#pragma unroll
+      for (int p = 4; p >= j; --p) P[p] = fma(d, P[p - 1], P[p]);
+#pragma unroll
+    for (int j = 1; j <= 2; ++j)
+#pragma unroll
+      for (int p = 2; p >= j; --p) {
+        Q[p] = fma(d, Q[p - 1], Q[p]);
+        R[p] = fma(d, R[p - 1], R[p]);
+      }
+  };
+  auto point = [&](double u, double t, double zv) {
+    const double r = fma(A, u, off) - zv;  // Eq. 1: r = h - z
+    bad += isfinite(r) ? 0 : 1;
+    const double u2 = u * u;
+    const double t2 = t * t;
+    P[0] += u2;
+    P[1] = fma(u2, t, P[1]);
+    P[2] = fma(u2, t2, P[2]);
+    P[3] = fma(u2, t2 * t, P[3]);
+    P[4] = fma(u2, t2 * t2, P[4]);
+    Q[0] += u;
+    Q[1] = fma(u, t, Q[1]);
+    Q[2] = fma(u, t2, Q[2]);
+    const double ur = u * r;
+    R[0] += ur;
+    R[1] = fma(ur, t, R[1]);
+    R[2] = fma(ur, t2, R[2]);
+    sr += r;
+    srr = fma(r, r, srr);
+  };
+
+  // task -> (row, first chunk column, chunks); 32-bit arithmetic relative to
+  // the block's first task
+  const int64_t row_b = t_begin / tpr;
+  const int k_b = (int)(t_begin - row_b * tpr);
+  auto task_pos = [&](int t, int64_t& row, int& cc0, int& ncc) {
+    const int g = k_b + t;
+    const int dr = g / tpr;
+    row = row_b + dr;
+    cc0 = (g - dr * tpr) * tcr;
+    ncc = min(tcr, cpr - cc0);
+  };
+  auto grab = [&]() {
+    int t = 0;
+    if (lane == 0) t = atomicAdd(&next_task, 1);
+    return __shfl_sync(FULL, t, 0);
+  };
+  double zn[L];
+  auto load = [&](int64_t row, int cc) {
+    const int c0l = cc * CW;
+    const double* zp = z + row * (int64_t)W + c0l + lane;
+    if (c0l + CW <= W) {  // warp-uniform
+#pragma unroll
+      for (int k = 0; k < L; ++k) zn[k] = __ldcs(zp + 32 * k);
+    } else {
+#pragma unroll
+      for (int k = 0; k < L; ++k) zn[k] = (c0l + lane + 32 * k < W) ? __ldcs(zp + 32 * k) : 0.0;
+    }
+  };
+
+  int task = grab();
+  int64_t trow = 0;
+  int tcc0 = 0, tncc = 0;
+  if (task < nt) {
+    task_pos(task, trow, tcc0, tncc);
+    load(trow, tcc0);
+  }
+  while (task < nt) {
+    // ---- one task: chunks tcc0 .. tcc0 + tncc - 1 of row trow
+    const int64_t row = trow;
+    const int cc0 = tcc0, ncc = tncc;
+    const int my = task;
+    const double dy = (double)(row + row0) - y0;
+    int next = nt;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) P[i] = 0.0;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) Q[i] = R[i] = 0.0;
+    sr = srr = 0.0;
+    bad = 0;
+    double E = 0.0, Rr = 0.0, org = 0.0;
+    bool carried = false;
+    int since_seed = 0;
+    for (int j = 0; j < ncc; ++j) {
+      double zc[L];
+#pragma unroll
+      for (int k = 0; k < L; ++k) zc[k] = zn[k];
+      if (j + 1 < ncc) {
+        load(row, cc0 + j + 1);  // prefetch the next chunk of this task
+      } else {
+        next = grab();  // ... or the first chunk of the next task
+        if (next < nt) {
+          task_pos(next, trow, tcc0, tncc);
+          load(trow, tcc0);
+        }
+      }
+      const int c0 = (cc0 + j) * CW;
+      const double dx0 = (double)(c0 + lane) - x0;
+      shift(-(double)CW);  // origin -> this chunk's first pixel (zero moments at j = 0)
+      org = dx0;
+      const double q0 = dx0 * (ga * dx0 + gb2 * dy) + gc * (dy * dy);
+      const double argR = D * (2.0 * ga * dx0 + gb2 * dy) + ga * D * D;
+      const bool ok = fabs(q0) < 600.0 && fabs(argR) < 300.0 && 2.0 * ga * D * D * L < 300.0;
+      const bool full = c0 + CW <= W;  // warp-uniform
+      if (full && __all_sync(FULL, ok)) {
+        if (!carried || ++since_seed >= SEEDN) {  // warp-uniform
+          E = exp(-q0);
+          Rr = exp(-argR);
+          since_seed = 0;
+        }
+        double cs = 0.0;
+        const double E_in = E, R_in = Rr;
+#pragma unroll
+        for (int k = 0; k < L; ++k) {
+          const double u = E;
+          const double r = fma(A, u, off) - zc[k];  // Eq. 1: r = h - z
+          const double u2 = u * u;
+          const double k1 = D * k, k2 = k1 * k1, k3 = k2 * k1, k4 = k2 * k2;
+          const double ur = u * r;
+          P[0] += u2;
+          Q[0] += u;
+          R[0] += ur;
+          if (k > 0) {
+            P[1] = fma(u2, k1, P[1]);
+            P[2] = fma(u2, k2, P[2]);
+            P[3] = fma(u2, k3, P[3]);
+            P[4] = fma(u2, k4, P[4]);
+            Q[1] = fma(u, k1, Q[1]);
+            Q[2] = fma(u, k2, Q[2]);
+            R[1] = fma(ur, k1, R[1]);
+            R[2] = fma(ur, k2, R[2]);
+          }
+          sr += r;
+          cs = fma(r, r, cs);
+          E *= Rr;
+          Rr *= rho;
+        }
+        carried = true;
+        srr += cs;
+        if (!isfinite(cs)) {  // rare: replay the chunk's residuals and count the non-finite ones
+          double e = E_in, rr = R_in;
+#pragma unroll
+          for (int k = 0; k < L; ++k) {
+            bad += isfinite(fma(A, e, off) - zc[k]) ? 0 : 1;
+            e *= rr;
+            rr *= rho;
+          }
+        }
+      } else {
+        // ragged row end or unsafe exponent range: direct evaluation
+        carried = false;
+#pragma unroll
+        for (int k = 0; k < L; ++k) {
+          if (c0 + lane + 32 * k < W) {
+            const double dx = dx0 + D * k;
+            point(exp(-(dx * (ga * dx + gb2 * dy) + gc * (dy * dy))), D * k, zc[k]);
+          }
+        }
+      }
+    }
+    // ---- the task's moment vector: lane moments to the common origin
+    // o* = org - lane (lane 0's), summed across the warp in lane order,
+    // then moved to dx = 0 and folded with dy^q (lane i: vector entry i)
+    shift((double)lane);
+    {
+      double (*wr)[33] = wred[wid];
+#pragma unroll
+      for (int i = 0; i < 5; ++i) wr[i][lane] = P[i];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        wr[5 + i][lane] = Q[i];
+        wr[8 + i][lane] = R[i];
+      }
+      wr[11][lane] = sr;
+      wr[12][lane] = srr;
+      const int nbad = __reduce_add_sync(FULL, bad);
+      __syncwarp();
+      if (lane < 13) {
+        double s = 0.0;
+#pragma unroll 8
+        for (int l = 0; l < 32; ++l) s += wr[lane][l];
+        wr[lane][32] = s;
+      }
+      __syncwarp();
+      const double os = org - (double)lane;  // o*: the common origin (dx of lane 0's first pixel of the last chunk)
+      const double o = __shfl_sync(FULL, os, 0);
+      if (lane < KS) {
+        double v;
+        if (lane < MomLayout::OSR) {
+          // about dx = 0: sum_i C(p, i) o^(p-i) M_i (Horner in o), times dy^q
+          double mv = 0.0;
+          for (int i = 0; i <= f_p; ++i) mv = fma(mv, o, binom[f_p][i] * wr[f_base + i][32]);
+          double dq = 1.0;
+          for (int e = 0; e < f_q; ++e) dq *= dy;
+          v = mv * dq;
+        } else if (lane == MomLayout::OSR) {
+          v = wr[11][32];
+        } else if (lane == MomLayout::OSRR) {
+          v = wr[12][32];
+        } else {
+          v = (double)nbad;
+        }
+        tslot[my][lane] = v;
+      }
+      __syncwarp();
+    }
+    task = next;
+  }
+  if (a.dbg && lane == 0 && blockIdx.x * NW + wid < 16384) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.dbg[(blockIdx.x * NW + wid) * 4 + 2] = t;
+  }
+  __syncthreads();
+
+  // ---- block partial: the task slots summed in task order
+  {
+    static_assert(NW * KS <= TPB, "one (entry, segment) per thread");
+    if (tid < NW * KS) {
+      const int i = tid % KS, seg = tid / KS;
+      double s = 0.0;
+      for (int t = seg; t < nt; t += NW) s += tslot[t][i];
+      red[seg][i] = s;
+    }
+    __syncthreads();
+    for (int k = tid; k < KS; k += TPB) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) s += red[w][k];
+      a.partials[(size_t)blockIdx.x * KS + k] = s;
+    }
+  }
+  if (a.dbg && lane == 0 && blockIdx.x * NW + wid < 16384) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.dbg[(blockIdx.x * NW + wid) * 4 + 3] = t;
+  }
+  if (!grid_reduce1<KS, TPB>(a, mom, scratch)) return;
+  // ---- last block: the moment vector -> K-vector (alt coordinates) -> chain rule -> hand-off
+  dbg_tail(a, 3);
+  if (a.dbg) {  // development aid: the finish once more (warm instruction cache) for the timeline
+    moments_to_kvec(pre_s.g, (double)a.m, mom, vec);
+    __syncthreads();
+    dbg_tail(a, 8);
+    if (!a.no_chain) apply_chain_kvec<Model, TPB>(pre_s, vec, scratch);
+    dbg_tail(a, 9);
+  }
+  moments_to_kvec(pre_s.g, (double)a.m, mom, vec);
+  if (tid == 0) vec[KT] = mom[NV];  // non-finite count
+  __syncthreads();
+  dbg_tail(a, 5);
+  if (!a.no_chain) apply_chain_kvec<Model, TPB>(pre_s, vec, scratch);
+  dbg_tail(a, 6);
+  pass_tail<KS2, TPB, true>(a, st, vec, cond, use_cond);
+  dbg_tail(a, 7);
 }
 
 }  // namespace jf

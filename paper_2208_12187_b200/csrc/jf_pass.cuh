@@ -229,6 +229,12 @@ __host__ __device__ constexpr int combine_scratch(int tpb) { return tpb; }
 // Tickets: a.ticket[0] (groups), a.ticket[1 + g] (blocks of group g); each
 // is reset by its last user, ready for the next launch.
 constexpr int GROUP = 16;
+// development aid (JF_DEBUG_STAMPS): timestamps of the last block's tail phases
+__device__ __forceinline__ void dbg_tail(const PassArgs& a, int i) {
+  if (a.dbg && threadIdx.x == 0) {
+    a.dbg[4 * 16384 - 16 + i] = clock64();  // SM cycles (all tail stamps are on the last block's SM)
+  }
+}
 template <int KS, int TPB>
 __device__ __forceinline__ bool grid_reduce(const PassArgs& a, double* out, double* scratch /* TPB doubles */) {
   __shared__ unsigned int flag;
@@ -243,6 +249,7 @@ __device__ __forceinline__ bool grid_reduce(const PassArgs& a, double* out, doub
   if (t == 0) flag = (atomicAdd(a.ticket + 1 + g, 1u) == (unsigned)(nb - 1)) ? 1u : 0u;
   __syncthreads();
   if (!flag) return false;
+  dbg_tail(a, 1);
   __threadfence();
   for (int k = t; k < KS; k += TPB) {
     double v[GROUP];
@@ -259,6 +266,7 @@ __device__ __forceinline__ bool grid_reduce(const PassArgs& a, double* out, doub
   if (t == 0) flag = (atomicAdd(a.ticket, 1u) == (unsigned)(ngrp - 1)) ? 1u : 0u;
   __syncthreads();
   if (!flag) return false;
+  dbg_tail(a, 2);
   __threadfence();
   // group rows: NSEG segments per column, each up to 16 rows in one batch
   constexpr int NSEG = (TPB / KS) > 0 ? (TPB / KS) : 1;
@@ -286,6 +294,52 @@ __device__ __forceinline__ bool grid_reduce(const PassArgs& a, double* out, doub
     out[k] = s;
   }
   __syncthreads();
+  return true;
+}
+
+// Single-level variant for small grids (one block per SM): the last block
+// sums all gridDim.x partials, NSEG interleaved segments per entry in
+// parallel, then the segments in order (fixed order: bitwise reproducible).
+template <int KS, int TPB>
+__device__ __forceinline__ bool grid_reduce1(const PassArgs& a, double* out, double* scratch /* TPB doubles */) {
+  __shared__ unsigned int flag;
+  const int t = threadIdx.x;
+  const int nblk = gridDim.x;
+  __syncthreads();
+  if (t == 0) {
+    __threadfence();  // the block's partial (written by threads < KS, ordered by the barrier)
+    flag = (atomicAdd(a.ticket, 1u) == (unsigned)(nblk - 1)) ? 1u : 0u;
+  }
+  __syncthreads();
+  if (!flag) return false;
+  dbg_tail(a, 1);
+  __threadfence();
+  constexpr int NSEG = (TPB / KS) > 0 ? (TPB / KS) : 1;
+  if (t < NSEG * KS) {
+    const int k = t % KS, seg = t / KS;
+    double s = 0.0;
+    for (int r0 = seg; r0 < nblk; r0 += 8 * NSEG) {
+      double v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int r = r0 + i * NSEG;
+        v[i] = (r < nblk) ? __ldcg(a.partials + (size_t)r * KS + k) : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) s += v[i];
+    }
+    scratch[seg * KS + k] = s;
+  }
+  if (t == 0) a.ticket[0] = 0u;
+  __syncthreads();
+  for (int k = t; k < KS; k += TPB) {
+    double s = 0.0;
+#pragma unroll
+    for (int seg = 0; seg < NSEG; ++seg) s += scratch[seg * KS + k];
+    out[k] = s;
+  }
+  __syncthreads();
+  dbg_tail(a, 2);
   return true;
 }
 
