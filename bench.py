@@ -41,15 +41,17 @@ import datagen as dg  # noqa: E402
 W_IMG = 4096
 SEED = 6
 N_PARAMS = 7
-# Algorithmic FP64 work per point of the n=7 J-pass as built: the moment
-# form (jf_moment.cuh): per point 19 fp64 operations (row
-# recurrence 2, residual 2, u^2 1, the eleven step-index moments 11 + the u r
-# product 1, sum r and sum r^2 2), per 16-point warp-chunk ~69 (shift of the
-# moments to dx 46, chunk set-up 12, exp re-seed every 4 chunks 11): 23 per
-# point.  Each fp64 operation is one issue slot of the 64 FP64 lanes/SM,
-# counted as 2 flops (an FMA slot), so the peak below is the FMA-slot peak.
-# (The dual-number rank-1 form needs 85 per point — SURVEY §8(d) d.3.)
-ALG_FP64_INSTR_PER_POINT = 23
+# Roofline of the n=7 J-pass: per point it must read z (8 B,
+# implicit grid) and, in the moment form (jf_moment.cuh), execute 19 fp64
+# operations (row recurrence 2, residual 2, u^2 1, u r 1, the eleven
+# step-index moments 11, sum r and sum r^2 2; per-chunk/per-task overheads
+# are the implementation's, not the algorithm's).  HBM: 8 B / 6467 GB/s per
+# point; FP64: 19 / (148 SMs x 64 lanes x 1.965 GHz) per point -> at 4096^2
+# 20.8 us vs 17.1 us: the pass is HBM-bound and is reported against the
+# measured HBM peak (MEASURED_PEAKS.json hbm_gbs), with the FP64-pipe
+# fraction alongside.  (The dual-number rank-1 form needs 85 fp64 per point,
+# SURVEY §8(d) d.3, and would be FP64-bound.)
+ALG_FP64_INSTR_PER_POINT = 19
 BYTES_PER_POINT = 8  # z only (implicit grid)
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.2: SMs x FP64 lanes x 2 x max SM clock
 
@@ -267,15 +269,24 @@ def main():
     e1.record(stream)
     barrier()
     t_j = e0.elapsed_time(e1) / NJ * 1e-3
-    alg_flops = 2.0 * ALG_FP64_INSTR_PER_POINT * m_local
-    achieved = alg_flops / t_j / 1e12
+    hbm_peak = 6467.1
+    try:
+        hbm_peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        pass
+    achieved = BYTES_PER_POINT * m_local / t_j / 1e9
+    fp64_achieved = 2.0 * ALG_FP64_INSTR_PER_POINT * m_local / t_j / 1e12
     roofline = {
-        "bound": "alu", "kernel": "moment_pass_kernel<16,128,3> (moment-form J-pass, n=7 implicit grid, fp64)",
-        "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
+        "bound": "hbm", "kernel": "moment_task_kernel<16,4,12> (moment-form J-pass, n=7 implicit grid, fp64)",
+        "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
         "traffic": None, "launch_us": t_j * 1e6,
-        "alg_work": f"{ALG_FP64_INSTR_PER_POINT} FP64-pipe instr/point x 2 flops x {m_local} points",
-        "peak_source": "derived: 148 SMs x 64 FP64 lanes x 2 x 1.965 GHz (DESIGN.md §6)",
-        "hbm_frac": (BYTES_PER_POINT * m_local / t_j) / 6536.7e9,
+        "alg_work": f"{BYTES_PER_POINT} B/point (z) x {m_local} points; "
+                    f"FP64 floor {ALG_FP64_INSTR_PER_POINT} instr/point x {m_local} points",
+        "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)",
+        "fp64_tflops": fp64_achieved, "fp64_peak_tflops": FP64_PEAK_TFLOPS,
+        "fp64_frac": fp64_achieved / FP64_PEAK_TFLOPS,
+        "t_floor_us": max(BYTES_PER_POINT * m_local / (hbm_peak * 1e9),
+                          ALG_FP64_INSTR_PER_POINT * m_local / (FP64_PEAK_TFLOPS * 1e12 / 2)) * 1e6,
     }
     prof_path = os.path.join(ROOT, "profiles", "traffic_jpass.json")
     if os.path.exists(prof_path):

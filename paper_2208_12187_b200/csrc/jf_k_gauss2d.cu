@@ -28,26 +28,50 @@ static void use_moment(Kernels& k) {
   k.jk = f;
   k.jtpb = TPB;
   k.jsmem = moment_smem_bytes(L, TPB, STG);
-  if (k.jsmem > 0) cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, k.jsmem);
 }
 
 template <int L, int TC, int NW, int SEEDN = 4>
 static void use_task(Kernels& k) {
-  auto f = moment_task_kernel<L, TC, NW, SEEDN>;
-  k.jk = f;
+  k.jk = moment_task_kernel<L, TC, NW, SEEDN>;
   k.jtpb = NW * 32;
   k.jsmem = moment_task_smem_bytes(NW);
-  cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, k.jsmem);
+}
+template <int L, int TC, int NW, int SEEDN = 4>
+static void attr_task() {
+  cudaFuncSetAttribute((const void*)moment_task_kernel<L, TC, NW, SEEDN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       moment_task_smem_bytes(NW));
+}
+template <int L, int TPB, int MINB, int SEEDN, int STG>
+static void attr_moment() {
+  cudaFuncSetAttribute((const void*)moment_pass_kernel<L, TPB, MINB, SEEDN, STG>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, moment_smem_bytes(L, TPB, STG));
+}
+void kernel_attrs_init() {
+  attr_task<16, 4, 12>();
+  attr_task<16, 2, 12>();
+  attr_task<16, 4, 16>();
+  attr_task<16, 8, 12>();
+  attr_task<8, 8, 16>();
+  attr_task<32, 2, 8, 2>();
+  attr_moment<16, 128, 3, 4, 3>();
+  attr_moment<16, 128, 3, 4, 4>();
+  attr_moment<8, 128, 4, 8, 4>();
+  attr_moment<8, 128, 4, 8, 6>();
+  attr_moment<16, 256, 1, 4, 3>();
+  attr_moment<32, 128, 2, 2, 3>();
+  attr_moment<16, 128, 2, 4, 6>();
 }
 
 Kernels kernels_gauss2d(int coord) {
   Kernels k = coord == COORD_EXPLICIT ? make<COORD_EXPLICIT>() : make<COORD_GRID>();
   if (coord == COORD_GRID) {
-    // unweighted implicit grid: the moment-form J-pass (jf_moment.cuh)
-    use_moment<16, 128, 3>(k);
+    // unweighted implicit grid: the moment-form J-pass (jf_moment.cuh),
+    // task-scheduled, one block of 12 warps per SM
+    use_task<16, 4, 12>(k);
     if (const char* v = getenv("JF_JVARIANT")) {  // development aid: alternative shapes
       const int var = atoi(v);
       if (var == 9) { k.jk = pass_kernel<ModelGauss2DRot, true, COORD_GRID, false>; k.jtpb = 256; k.jsmem = 0; }  // dual numbers
+      if (var == 1) use_moment<16, 128, 3>(k);  // static per-warp split (r1d)
       if (var == 11) use_moment<8, 128, 4>(k);
       if (var == 30) use_task<16, 4, 12>(k);
       if (var == 31) use_task<16, 2, 12>(k);

@@ -27,4 +27,8 @@ Kernels kernels_exp_decay(int coord);
 Kernels kernels_gauss1d(int coord);
 Kernels kernels_gauss2d(int coord);
 Kernels kernels_gauss2d_x2(int coord);
+// Per-device function attributes (opt-in dynamic shared memory), set once per
+// device when its first context is created — never during a pass, when an
+// attribute call could wait on the spinning kernels of emulated peer ranks.
+void kernel_attrs_init();
 }  // namespace jf

@@ -94,6 +94,75 @@ __device__ __forceinline__ void moments_to_kvec(const PreGauss2D& g, double m_pt
   }
 }
 
+// The alt-coordinate K-vector slot (x, y), x <= y <= 7, as <= 4 terms
+// coef * mom[idx] (idx == NV stands for the point count m), the same
+// formulas as moments_to_kvec.
+__device__ __forceinline__ int kalt_terms(const PreGauss2D& g, int x, int y, int* idx, double* c) {
+  if (y <= 5) {
+    if (y == 0) {
+      idx[0] = MomLayout::O2 + mono(4, 0, 0);
+      c[0] = 1.0;
+      return 1;
+    }
+    const Poly2 a = psi(g, x), b = psi(g, y);
+    const double f = (x == 0 ? 1.0 : g.A) * g.A;
+    int n = 0;
+    for (int s = 0; s < 2; ++s)
+      for (int u = 0; u < 2; ++u) {
+        idx[n] = MomLayout::O2 + mono(4, a.p[s] + b.p[u], a.q[s] + b.q[u]);
+        c[n++] = a.c[s] * b.c[u] * f;
+      }
+    return n;
+  }
+  if (x <= 5) {
+    const int base = (y == 6) ? MomLayout::O1 : MomLayout::OR;
+    const Poly2 a = psi(g, x);
+    const double f = (x == 0 ? 1.0 : g.A);
+    for (int s = 0; s < 2; ++s) {
+      idx[s] = base + mono(2, a.p[s], a.q[s]);
+      c[s] = a.c[s] * f;
+    }
+    return 2;
+  }
+  idx[0] = (x == 6) ? (y == 6 ? MomLayout::NV : MomLayout::OSR) : MomLayout::OSRR;
+  c[0] = 1.0;
+  return 1;
+}
+
+// The whole finish map as one matrix: K-vector slot t (paper coordinates,
+// after the chain rule) = sum_i C[t][i] mom[i], i < NV, + C[t][NV] * m.
+// Built by one warp from the pass's parameters (R33, R34): the same linear
+// algebra as moments_to_kvec followed by apply_chain_kvec, composed once.
+constexpr int FMAP_COLS = MomLayout::NV + 1;
+template <class Pre>
+__device__ __forceinline__ void build_finish_map(const Pre& pre, double (*C)[FMAP_COLS], int lane) {
+  using Model = ModelGauss2DRot;
+  constexpr int N = Model::N, N1 = N + 1, KT = tri_count(N);
+  for (int t = lane; t < KT; t += 32) {
+    for (int i = 0; i < FMAP_COLS; ++i) C[t][i] = 0.0;
+    int j = 0, rem = t;
+    while (rem >= N1 - j) {
+      rem -= N1 - j;
+      ++j;
+    }
+    const int k = j + rem;
+    const int gj = chain_block<Model>(j), gk = chain_block<Model>(k);
+    const int nj = gj < 0 ? 1 : 3, nk = gk < 0 ? 1 : 3;
+    const int bj = gj < 0 ? j : Model::tbase(gj), bk = gk < 0 ? k : Model::tbase(gk);
+    for (int r = 0; r < nj; ++r) {
+      const double cj = gj < 0 ? 1.0 : pre.g.T[3 * r + (j - bj)];
+      for (int q = 0; q < nk; ++q) {
+        const double ck = gk < 0 ? 1.0 : pre.g.T[3 * q + (k - bk)];
+        const int x = bj + r, y = bk + q;
+        int idx[4];
+        double c[4];
+        const int n = kalt_terms(pre.g, x <= y ? x : y, x <= y ? y : x, idx, c);
+        for (int u = 0; u < n; ++u) C[t][idx[u]] = fma(cj * ck, c[u], C[t][idx[u]]);
+      }
+    }
+  }
+}
+
 // Last block: combine the grid's moment vectors, map them to the K-vector
 // (alt coordinates), apply the chain rule, hand over (pass_tail).  Out of
 // line so the prologue's 3x3 blocks never occupy the main loop's registers.
@@ -579,7 +648,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
   __shared__ double vec[KMAX];
   __shared__ double scratch[combine_scratch(TPB)];
   __shared__ double mom[KS];
-  __shared__ Pre pre_s;                     // chain-rule blocks for the finish (warp 0)
+  __shared__ double fmap[KT][FMAP_COLS];    // the finish map (warp 0, at the start)
   __shared__ int next_task;
   __shared__ double binom[5][5];            // C(p, i)
 
@@ -642,14 +711,14 @@ __global__ void __launch_bounds__(NW * 32, 1)
     a.dbg[(blockIdx.x * NW + wid) * 4 + 1] = t;
   }
 
-  // warp 0 computes the finish's chain-rule blocks first (any block may be
-  // the last one); the task counter balances its late start
+  // warp 0 first builds the finish map (any block may be the last one); the
+  // task counter balances its late start
   if (wid == 0) {
     double xv[N];
 #pragma unroll
     for (int j = 0; j < N; ++j) xv[j] = xs[j];
     const auto pre = Model::template prologue<true>(xv);
-    if (lane == 0) pre_s = pre;
+    build_finish_map(pre, fmap, lane);
   }
 
   double P[5], Q[3], R[3], sr, srr;
@@ -886,7 +955,12 @@ __global__ void __launch_bounds__(NW * 32, 1)
       double s = 0.0;
 #pragma unroll
       for (int w = 0; w < NW; ++w) s += red[w][k];
-      a.partials[(size_t)blockIdx.x * KS + k] = s;
+      // keep the partial in L2 for the last block (the image streams through evict-first)
+      unsigned long long pol;
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+      asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a.partials + (size_t)blockIdx.x * KS + k), "d"(s),
+                   "l"(pol)
+                   : "memory");
     }
   }
   if (a.dbg && lane == 0 && blockIdx.x * NW + wid < 16384) {
@@ -897,18 +971,26 @@ __global__ void __launch_bounds__(NW * 32, 1)
   if (!grid_reduce1<KS, TPB>(a, mom, scratch)) return;
   // ---- last block: the moment vector -> K-vector (alt coordinates) -> chain rule -> hand-off
   dbg_tail(a, 3);
-  if (a.dbg) {  // development aid: the finish once more (warm instruction cache) for the timeline
-    moments_to_kvec(pre_s.g, (double)a.m, mom, vec);
-    __syncthreads();
-    dbg_tail(a, 8);
-    if (!a.no_chain) apply_chain_kvec<Model, TPB>(pre_s, vec, scratch);
-    dbg_tail(a, 9);
+  if (tid < KT) {
+    double v = fmap[tid][NV] * (double)a.m;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v = fma(fmap[tid][i], mom[i], v);
+    vec[tid] = a.no_chain ? 0.0 : v;
+  } else if (tid == KT) {
+    vec[KT] = mom[NV];  // non-finite count
   }
-  moments_to_kvec(pre_s.g, (double)a.m, mom, vec);
-  if (tid == 0) vec[KT] = mom[NV];  // non-finite count
   __syncthreads();
-  dbg_tail(a, 5);
-  if (!a.no_chain) apply_chain_kvec<Model, TPB>(pre_s, vec, scratch);
+  if (a.no_chain) {  // debug: the K-vector in the alt coordinates (the two-stage map)
+    Pre pre;
+    {
+      double xv[N];
+#pragma unroll
+      for (int j = 0; j < N; ++j) xv[j] = xs[j];
+      pre = Model::template prologue<true>(xv);
+    }
+    moments_to_kvec(pre.g, (double)a.m, mom, vec);
+    __syncthreads();
+  }
   dbg_tail(a, 6);
   pass_tail<KS2, TPB, true>(a, st, vec, cond, use_cond);
   dbg_tail(a, 7);

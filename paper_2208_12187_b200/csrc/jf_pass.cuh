@@ -243,6 +243,7 @@ __device__ __forceinline__ bool grid_reduce(const PassArgs& a, double* out, doub
   const int ngrp = (nblk + GROUP - 1) / GROUP;
   const int g = blockIdx.x / GROUP;
   const int b0 = g * GROUP, nb = min(GROUP, nblk - b0);
+  const double* part = a.partials;
   double* grp = a.partials + (size_t)nblk * KS;
   __threadfence();
   __syncthreads();
@@ -254,7 +255,7 @@ __device__ __forceinline__ bool grid_reduce(const PassArgs& a, double* out, doub
   for (int k = t; k < KS; k += TPB) {
     double v[GROUP];
 #pragma unroll
-    for (int i = 0; i < GROUP; ++i) v[i] = (i < nb) ? __ldcg(a.partials + (size_t)(b0 + i) * KS + k) : 0.0;
+    for (int i = 0; i < GROUP; ++i) v[i] = (i < nb) ? __ldcg(part + (size_t)(b0 + i) * KS + k) : 0.0;
     double s = 0.0;
 #pragma unroll
     for (int i = 0; i < GROUP; ++i) s += v[i];
@@ -283,6 +284,7 @@ __device__ __forceinline__ bool grid_reduce(const PassArgs& a, double* out, doub
 #pragma unroll
       for (int i = 0; i < 16; ++i) s += v[i];
     }
+    if (t == 0) dbg_tail(a, 10);
     scratch[seg * KS + k] = s;
   }
   if (t == 0) a.ticket[0] = 0u;
@@ -305,29 +307,33 @@ __device__ __forceinline__ bool grid_reduce1(const PassArgs& a, double* out, dou
   __shared__ unsigned int flag;
   const int t = threadIdx.x;
   const int nblk = gridDim.x;
+  // the block's partial (written by threads < KS) is released by thread 0
+  // after the barrier (release is cumulative); the last block acquires
   __syncthreads();
   if (t == 0) {
-    __threadfence();  // the block's partial (written by threads < KS, ordered by the barrier)
-    flag = (atomicAdd(a.ticket, 1u) == (unsigned)(nblk - 1)) ? 1u : 0u;
+    unsigned prev;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(prev) : "l"(a.ticket) : "memory");
+    flag = (prev == (unsigned)(nblk - 1)) ? 1u : 0u;
   }
   __syncthreads();
   if (!flag) return false;
   dbg_tail(a, 1);
-  __threadfence();
   constexpr int NSEG = (TPB / KS) > 0 ? (TPB / KS) : 1;
+  const double* part = a.partials;  // read once (each L2 load below would otherwise re-read the field)
   if (t < NSEG * KS) {
     const int k = t % KS, seg = t / KS;
     double s = 0.0;
-    for (int r0 = seg; r0 < nblk; r0 += 8 * NSEG) {
-      double v[8];
+    for (int r0 = seg; r0 < nblk; r0 += 16 * NSEG) {  // one batch of loads for nblk <= 16 NSEG
+      double v[16];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < 16; ++i) {
         const int r = r0 + i * NSEG;
-        v[i] = (r < nblk) ? __ldcg(a.partials + (size_t)r * KS + k) : 0.0;
+        v[i] = (r < nblk) ? __ldcg(part + (size_t)r * KS + k) : 0.0;
       }
 #pragma unroll
-      for (int i = 0; i < 8; ++i) s += v[i];
+      for (int i = 0; i < 16; ++i) s += v[i];
     }
+    if (t == 0) dbg_tail(a, 10);
     scratch[seg * KS + k] = s;
   }
   if (t == 0) a.ticket[0] = 0u;

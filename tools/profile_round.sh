@@ -14,7 +14,7 @@ mkdir -p gpurun_out
 timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-graph > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:moment_pass -s 3 -c 1 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:moment_ -s 3 -c 1 \
     -o gpurun_out/jpass_${TAG} -f python tools/quick_time.py 4096 passonly > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:^pass_kernel -s 3 -c 1 \
     -o gpurun_out/rpass_${TAG} -f python tools/quick_time.py 4096 passonly > /dev/null 2>&1

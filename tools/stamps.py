@@ -24,5 +24,5 @@ print("fastest SMs:", [(int(s), round(float(x), 2)) for s, x in zip(np.unique(sm
 tail = np.where(tail > 0, tail - tail[1], np.nan) / 1.9e3  # clock64 -> us at ~1.9 GHz, from [1]
 print("last block tail (us): [1] L1 ticket, [2] reduced, [3] finish start, [8] kvec (1st), [9] chain (1st), "
       "[4] prologue, [5] kvec, [6] chain, [7] hand-off:")
-print("   ", " ".join(f"[{i}] {tail[i]:.2f}" for i in (1, 2, 3, 8, 9, 4, 5, 6, 7) if not np.isnan(tail[i])),
+print("   ", " ".join(f"[{i}] {tail[i]:.2f}" for i in (1, 10, 2, 3, 8, 9, 4, 5, 6, 7) if not np.isnan(tail[i])),
       f"(loop end max {lo.max():.2f}, block partial max {ex.max():.2f})")
