@@ -624,7 +624,7 @@ constexpr int MOMENT_MAXT = 112;  // task slots per block of moment_task_kernel
 __host__ __device__ constexpr int moment_task_smem_bytes(int NW) {
   return (MOMENT_MAXT * MomLayout::KS + NW * 13 * 33) * 8;
 }
-template <int L, int TC, int NW, int SEEDN = 4>
+template <int L, int TC, int NW, int SEEDN = 4, int DBGZ = 0>
 __global__ void __launch_bounds__(NW * 32, 1)
     moment_task_kernel(const PassArgs* __restrict__ pa, FitState* __restrict__ st, cudaGraphConditionalHandle cond,
                        int use_cond) {
@@ -693,12 +693,18 @@ __global__ void __launch_bounds__(NW * 32, 1)
   const int cpr = (W + CW - 1) / CW;
   const int nblk = gridDim.x;
   // task length: TC chunks, longer when the block would get more than MAXT tasks
+  // (TSPLIT > 0: the block's last TSPLIT tasks are split into single-chunk
+  // tasks so the warps run out of work within about one chunk of each other;
+  // measured slower at 4096^2 — the per-task overhead outweighs the balance)
+  constexpr int TSPLIT = 0;
   int tcr = TC < cpr ? TC : cpr;
-  while (((H * (int64_t)((cpr + tcr - 1) / tcr)) + nblk - 1) / nblk > MAXT) ++tcr;
+  while (((H * (int64_t)((cpr + tcr - 1) / tcr)) + nblk - 1) / nblk + TSPLIT * (tcr - 1) > MAXT) ++tcr;
   const int tpr = (cpr + tcr - 1) / tcr;  // tasks per row
   const int64_t ntask = H * (int64_t)tpr;
   const int64_t t_begin = (int64_t)blockIdx.x * ntask / nblk, t_end = (int64_t)(blockIdx.x + 1) * ntask / nblk;
-  const int nt = (int)(t_end - t_begin);
+  const int nt_big = (int)(t_end - t_begin);
+  const int nbig = nt_big > TSPLIT ? nt_big - TSPLIT : 0;  // tasks kept whole
+  const int nt = nbig + (nt_big - nbig) * tcr;              // task slots (single-chunk tail tasks may be empty)
 
   const double rho = exp(-2.0 * ga * D * D);
   const double* __restrict__ z = a.z;
@@ -762,11 +768,20 @@ __global__ void __launch_bounds__(NW * 32, 1)
   const int64_t row_b = t_begin / tpr;
   const int k_b = (int)(t_begin - row_b * tpr);
   auto task_pos = [&](int t, int64_t& row, int& cc0, int& ncc) {
+    int sub = -1;
+    if (t >= nbig) {  // single-chunk tail task: chunk sub of whole task bt
+      sub = (t - nbig) % tcr;
+      t = nbig + (t - nbig) / tcr;
+    }
     const int g = k_b + t;
     const int dr = g / tpr;
     row = row_b + dr;
     cc0 = (g - dr * tpr) * tcr;
     ncc = min(tcr, cpr - cc0);
+    if (sub >= 0) {
+      cc0 += sub;
+      ncc = sub < ncc ? 1 : 0;
+    }
   };
   auto grab = [&]() {
     int t = 0;
@@ -776,7 +791,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
   double zn[L];
   auto load = [&](int64_t row, int cc) {
     const int c0l = cc * CW;
-    const double* zp = z + row * (int64_t)W + c0l + lane;
+    const double* zp = DBGZ ? z + lane : z + row * (int64_t)W + c0l + lane;  // DBGZ: compute-only probe (L1-resident z)
     if (c0l + CW <= W) {  // warp-uniform
 #pragma unroll
       for (int k = 0; k < L; ++k) zn[k] = __ldcs(zp + 32 * k);
@@ -886,6 +901,13 @@ __global__ void __launch_bounds__(NW * 32, 1)
         }
       }
     }
+    if (ncc == 0) {  // empty tail task: zero slot, next task
+      next = grab();
+      if (next < nt) {
+        task_pos(next, trow, tcc0, tncc);
+        load(trow, tcc0);
+      }
+    }
     // ---- the task's moment vector: lane moments to the common origin
     // o* = org - lane (lane 0's), summed across the warp in lane order,
     // then moved to dx = 0 and folded with dy^q (lane i: vector entry i)
@@ -903,11 +925,11 @@ __global__ void __launch_bounds__(NW * 32, 1)
       wr[12][lane] = srr;
       const int nbad = __reduce_add_sync(FULL, bad);
       __syncwarp();
-      if (lane < 13) {
-        double s = 0.0;
-#pragma unroll 8
-        for (int l = 0; l < 32; ++l) s += wr[lane][l];
-        wr[lane][32] = s;
+      if (lane < 13) {  // four interleaved chains, then combined (fixed order)
+        double s4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int l = 0; l < 32; ++l) s4[l & 3] += wr[lane][l];
+        wr[lane][32] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
       }
       __syncwarp();
       const double os = org - (double)lane;  // o*: the common origin (dx of lane 0's first pixel of the last chunk)
@@ -915,12 +937,21 @@ __global__ void __launch_bounds__(NW * 32, 1)
       if (lane < KS) {
         double v;
         if (lane < MomLayout::OSR) {
-          // about dx = 0: sum_i C(p, i) o^(p-i) M_i (Horner in o), times dy^q
+          // about dx = 0: sum_i C(p, i) o^(p-i) M_i, times dy^q (branch-free:
+          // binom[p][i] = 0 for i > p)
+          const double o2 = o * o, y2 = dy * dy;
+          auto pw = [](int e, double x1, double x2) {  // x^e, e <= 4
+            const double lo = (e & 1) ? x1 : 1.0;
+            return (e >= 2) ? ((e >= 4) ? x2 * x2 : x2 * lo) : lo;
+          };
           double mv = 0.0;
-          for (int i = 0; i <= f_p; ++i) mv = fma(mv, o, binom[f_p][i] * wr[f_base + i][32]);
-          double dq = 1.0;
-          for (int e = 0; e < f_q; ++e) dq *= dy;
-          v = mv * dq;
+#pragma unroll
+          for (int i = 0; i < 5; ++i) {
+            const int e = f_p - i;
+            const double c = binom[f_p][i] * pw(e < 0 ? 0 : e, o, o2);
+            mv = fma(c, wr[min(f_base + i, 12)][32], mv);
+          }
+          v = mv * pw(f_q, dy, y2);
         } else if (lane == MomLayout::OSR) {
           v = wr[11][32];
         } else if (lane == MomLayout::OSRR) {

@@ -1024,14 +1024,18 @@ __device__ __noinline__ void st_end_inner(FitState* st, SolverSmem& S, bool have
       st->phase = PH_ACCEPT_J;
       return;
     }
+    const long long c0 = clock64();
     st_take_pass<n>(st, st->kv);
     st->cost = st->cost_new;  // SciPy keeps the trial's cost
     st->njev = st->njev + 1;
     if (st->qr_mode && st_qr_begin<n>(st, S, st->kv, 1)) return;  // nit counts after the QR pass
     if (st->jacmode) st_update_scale<n>(st, false);
+    st->prof[5] += clock64() - c0;
   }
   st->nit = st->nit + 1;  // R27
+  const long long c1 = clock64();
   st_outer_top<n>(st, S);
+  st->prof[6] += clock64() - c1;
 }
 
 // After a trial pass at x_eval (speculative J-pass or conservative r-pass).
@@ -1097,17 +1101,23 @@ __device__ __noinline__ void fit_after_pass(FitState* st, SolverSmem& S, const d
   if (phase == PH_INIT_J) {
     st_init<n>(st, S, st->kv);
   } else if (phase == PH_TRIAL_J && jac) {
+    const long long c0 = clock64();
     st_after_trial<n>(st, S, st->kv, true);
+    st->prof[4] += clock64() - c0;
   } else if (phase == PH_TRIAL_R && !jac) {
     st_after_trial<n>(st, S, st->kv, false);
   } else if (phase == PH_ACCEPT_J && jac) {
+    const long long c0 = clock64();
     st_take_pass<n>(st, st->kv);  // g, G at the accepted x (cost kept: SciPy)
     st->cost = st->cost_new;
     st->njev = st->njev + 1;
     if (st->qr_mode && st_qr_begin<n>(st, S, st->kv, 1)) return;
     if (st->jacmode) st_update_scale<n>(st, false);
     st->nit = st->nit + 1;
+    const long long c1 = clock64();
+    st->prof[5] += c1 - c0;
     st_outer_top<n>(st, S);
+    st->prof[6] += clock64() - c1;
   } else if (phase == PH_QR2 && jac) {
     st_qr_finish<n>(st, S, st->kv);
     if (st->qr_after == 0) {
@@ -1246,7 +1256,11 @@ __device__ __forceinline__ void solver_step_n(FitState* st, SolverSmem& S, const
     if (lane == 0) st->prof[0] += clock64() - c1;
   }
   __syncwarp();
-  if (lane == 0 && S.need_trial) st_trial_finish<n>(st, S);
+  if (lane == 0 && S.need_trial) {
+    const long long c2 = clock64();
+    st_trial_finish<n>(st, S);
+    st->prof[7] += clock64() - c2;
+  }
   __syncwarp();
   if (!st->cont && st->error == 0 && !st->pcov_done) st_pcov<n>(st, S);
   if (lane == 0) st->prof[3] += clock64() - c0;

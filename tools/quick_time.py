@@ -25,6 +25,17 @@ for ro in (False, True):
     e1.record(); torch.cuda.synchronize()
     t = e0.elapsed_time(e1) / N
     print(f"{'r' if ro else 'J'}-pass W={W}: {t*1e3:.1f} us  {pr.m/t*1e3:.3e} pts/s")
+    try:  # the same launches captured in a CUDA graph: kernel time without the host calls
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(N):
+                jf.pass_device(pr.model, z, x, kv, grid=pr.grid, stream=s.cuda_stream, residual_only=ro)
+        g.replay(); torch.cuda.synchronize()
+        e0.record(s); g.replay(); e1.record(s); torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / N
+        print(f"{'r' if ro else 'J'}-pass W={W} (graph): {t*1e3:.1f} us  {pr.m/t*1e3:.3e} pts/s")
+    except Exception as ex:
+        print("graph timing failed:", ex)
 if len(sys.argv) > 2 and sys.argv[2] == "passonly":
     sys.exit(0)
 for mode in ("graph", "hostloop"):
