@@ -774,9 +774,18 @@ __device__ __forceinline__ void st_update_scale(FitState* st, bool first) {
 // Trial, part 1: the Gauss-Newton fast path; sets S.need_eig when Alg. 2 or
 // the exact rank test needs the eigendecomposition (computed by the warp).
 template <int n>
-__device__ __noinline__ void st_trial_begin(FitState* st, SolverSmem& S) {
-  for (int i = 0; i < n; ++i)
-    for (int j = 0; j < n; ++j) S.M[i][j] = st->Gh[i * NMAX + j];
+__device__ __noinline__ void st_trial_begin(FitState* st, SolverSmem& S, bool have_M = false) {
+  if (!have_M) {
+    double M[n][n];
+#pragma unroll
+    for (int i = 0; i < n; ++i)
+#pragma unroll
+      for (int j = 0; j < n; ++j) M[i][j] = st->Gh[i * NMAX + j];
+#pragma unroll
+    for (int i = 0; i < n; ++i)
+#pragma unroll
+      for (int j = 0; j < n; ++j) S.M[i][j] = M[i][j];
+  }
   S.need_trial = 1;
   S.fast = 0;
   S.need_eig = 0;
@@ -865,30 +874,49 @@ __device__ __noinline__ void st_outer_top(FitState* st, SolverSmem& S) {
     st->cont = 0;
     return;
   }
+  // register copies first: every load is issued before any store (the
+  // state lives in shared memory; interleaved stores would serialise them)
+  double dd[n], dh[n], gj[n], G[n][n];
+  const bool bounded = st->bounded;
+#pragma unroll
+  for (int j = 0; j < n; ++j) {
+    gj[j] = st->g[j];
+#pragma unroll
+    for (int k = 0; k < n; ++k) G[j][k] = st->G[j * NMAX + k];
+  }
+#pragma unroll
   for (int j = 0; j < n; ++j) {
     const double si = st->scale_inv[j];
-    if (st->bounded) {
+    if (bounded) {
       double vj = v[j];
       if (dv[j] != 0.0) vj *= si;
-      st->d[j] = sqrt(vj) / si;              // R19: d = v^0.5 * scale
-      st->diag_h[j] = st->g[j] * dv[j] / si;  // C = diag(g * scale) Jv
+      dd[j] = sqrt(vj) / si;          // R19: d = v^0.5 * scale
+      dh[j] = gj[j] * dv[j] / si;      // C = diag(g * scale) Jv
     } else {
-      st->d[j] = 1.0 / si;  // Eq. 8: J_hat = J D^-1
-      st->diag_h[j] = 0.0;
+      dd[j] = 1.0 / si;  // Eq. 8: J_hat = J D^-1
+      dh[j] = 0.0;
     }
-    st->gh[j] = st->d[j] * st->g[j];
   }
+#pragma unroll
+  for (int j = 0; j < n; ++j) {
+    st->d[j] = dd[j];
+    st->diag_h[j] = dh[j];
+    st->gh[j] = dd[j] * gj[j];
+  }
+#pragma unroll
   for (int i = 0; i < n; ++i) {  // B_hat = d G d (+ diag_h)
+#pragma unroll
     for (int j = 0; j < n; ++j) {
-      double b = st->d[i] * st->G[i * NMAX + j] * st->d[j];
-      if (i == j) b += st->diag_h[i];
+      double b = dd[i] * G[i][j] * dd[j];
+      if (i == j) b += dh[i];
       st->Gh[i * NMAX + j] = b;
+      S.M[i][j] = b;  // the trial's copy (st_trial_begin)
     }
   }
   st->theta = fmax(0.995, 1.0 - gnorm);
   st->actual = -1.0;
   st->have_eig = 0;
-  st_trial_begin<n>(st, S);
+  st_trial_begin<n>(st, S, true);
 }
 
 // TSQR: start the preconditioned second pass at the current x from the
