@@ -548,6 +548,10 @@ static int pass_common(int32_t model, const double* y, const double* z, int64_t 
   a.epilogue = EPI_NONE;
   a.no_chain = getenv("JF_DEBUG_NOCHAIN") ? 1 : 0;
   const char* stamps = residual_only ? nullptr : getenv("JF_DEBUG_STAMPS");  // development aid: per-warp timeline
+  if (stamps) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) stamps = nullptr;
+  }
   static unsigned long long* d_dbg = nullptr;
   constexpr int DBG_N = 4 * 16384;
   if (stamps && !d_dbg) CK(cudaMalloc(&d_dbg, sizeof(unsigned long long) * DBG_N));
@@ -569,9 +573,11 @@ static int pass_common(int32_t model, const double* y, const double* z, int64_t 
     o.comm->epoch += 1;
   }
   if (!c->h_args_valid || memcmp(&c->h_args, &a, sizeof(a)) != 0) {
-    CK(cudaMemcpyAsync(c->d_args, &a, sizeof(a), cudaMemcpyHostToDevice, s));
+    // source: the context's persistent copy (a copy captured into a CUDA
+    // graph must not read a stack buffer at replay)
     c->h_args = a;
     c->h_args_valid = true;
+    CK(cudaMemcpyAsync(c->d_args, &c->h_args, sizeof(a), cudaMemcpyHostToDevice, s));
   }
   r = launch_pass(k, !residual_only, s, c->d_args, c->d_state);
   if (r) return r;

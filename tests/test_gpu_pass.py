@@ -51,6 +51,10 @@ CASES = [
     ("gauss2d W=64", lambda: dg.make_gauss2d(64)),
     ("gauss2d W=1000x777", lambda: dg.make_gauss2d(1000, H=777)),
     ("gauss2d W=1024", lambda: dg.make_gauss2d(1024)),
+    # the moment kernel's whole-task fast path (rows of 4 x 512-pixel chunks),
+    # and rows mixing whole tasks with a shorter row-end task
+    ("gauss2d W=2048x48", lambda: dg.make_gauss2d(2048, H=48)),
+    ("gauss2d W=2600x37", lambda: dg.make_gauss2d(2600, H=37)),
     ("gauss2d_x2 W=96", lambda: dg.make_gauss2d_x2(96)),
     ("gauss2d_x2 W=700x333", lambda: dg.make_gauss2d_x2(700, H=333)),
 ]
@@ -102,6 +106,19 @@ def test_nonfinite_counts_and_weighted_pass():
     sig = np.random.default_rng(1).uniform(0.5, 2.0, pr.m)
     ref = orp.jpass(pr.model, pr.t, pr.z, pr.p0, sigma=sig)
     check_pass(jf.jpass(pr.model, pr.z, pr.p0, y=pr.t, sigma=sig), ref)
+
+
+def test_nonfinite_counts_moment_kernel():
+    """Non-finite residuals in whole-task (fast path) and row-end chunks are
+    counted exactly (per-chunk sum r^2 test + replay) in the moment J-pass."""
+    pr = dg.make_gauss2d(2600, H=23)
+    z = pr.z.copy()
+    idx = [0, 17, 2047, 2048, 2599, 2600 * 5 + 1000, 2600 * 22 + 2599]
+    z[idx[:4]] = np.nan
+    z[idx[4:]] = np.inf
+    _, _, _, bad = jf.jpass(pr.model, z, pr.p0, grid=pr.grid)
+    _, bad_r = jf.residual_pass(pr.model, z, pr.p0, grid=pr.grid)
+    assert bad == len(idx) and bad_r == len(idx)
 
 
 def test_pass_is_bitwise_deterministic():
