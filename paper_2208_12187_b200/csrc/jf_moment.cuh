@@ -1047,7 +1047,10 @@ __global__ void __launch_bounds__(NW * 32, 1)
   }
   __syncthreads();
 
-  // ---- block partial: the task slots summed in task order
+  // ---- block partial: the task slots summed in task order, then (unless
+  // debugging the alt coordinates) mapped through the finish map here, so
+  // the last block only sums the blocks' K-vectors
+  const bool mapped = !a.no_chain;
   {
     static_assert(NW * KS <= TPB, "one (entry, segment) per thread");
     if (tid < NW * KS) {
@@ -1061,10 +1064,25 @@ __global__ void __launch_bounds__(NW * 32, 1)
       double s = 0.0;
 #pragma unroll
       for (int w = 0; w < NW; ++w) s += red[w][k];
-      // keep the partial in L2 for the last block (the image streams through evict-first)
-      unsigned long long pol;
-      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-      asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a.partials + (size_t)blockIdx.x * KS + k), "d"(s),
+      mom[k] = s;
+    }
+    __syncthreads();
+    // keep the partial in L2 for the last block (the image streams through evict-first)
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    const int np = mapped ? KS2 : KS;
+    if (tid < np) {
+      double v;
+      if (!mapped) {
+        v = mom[tid];
+      } else if (tid < KT) {
+        v = 0.0;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) v = fma(fmap[tid][i], mom[i], v);
+      } else {
+        v = mom[NV];  // non-finite count
+      }
+      asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a.partials + (size_t)blockIdx.x * np + tid), "d"(v),
                    "l"(pol)
                    : "memory");
     }
@@ -1074,19 +1092,15 @@ __global__ void __launch_bounds__(NW * 32, 1)
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     a.dbg[(blockIdx.x * NW + wid) * 4 + 3] = t;
   }
-  if (!grid_reduce1<KS, TPB>(a, mom, scratch)) return;
-  // ---- last block: the moment vector -> K-vector (alt coordinates) -> chain rule -> hand-off
-  dbg_tail(a, 3);
-  if (tid < KT) {
-    double v = fmap[tid][NV] * (double)a.m;
-#pragma unroll
-    for (int i = 0; i < NV; ++i) v = fma(fmap[tid][i], mom[i], v);
-    vec[tid] = a.no_chain ? 0.0 : v;
-  } else if (tid == KT) {
-    vec[KT] = mom[NV];  // non-finite count
-  }
-  __syncthreads();
-  if (a.no_chain) {  // debug: the K-vector in the alt coordinates (the two-stage map)
+  if (mapped) {
+    if (!grid_reduce1<KS2, TPB>(a, vec, scratch)) return;
+    // ---- last block: + the point-count term of the map, hand-off
+    dbg_tail(a, 3);
+    if (tid < KT) vec[tid] = fma(fmap[tid][NV], (double)a.m, vec[tid]);
+    __syncthreads();
+  } else {
+    // debug: the K-vector in the alt coordinates (the two-stage map)
+    if (!grid_reduce1<KS, TPB>(a, mom, scratch)) return;
     Pre pre;
     {
       double xv[N];
@@ -1095,6 +1109,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
       pre = Model::template prologue<true>(xv);
     }
     moments_to_kvec(pre.g, (double)a.m, mom, vec);
+    if (tid == 0) vec[KT] = mom[NV];
     __syncthreads();
   }
   dbg_tail(a, 6);
