@@ -717,9 +717,12 @@ __global__ void __launch_bounds__(NW * 32, 1)
     a.dbg[(blockIdx.x * NW + wid) * 4 + 1] = t;
   }
 
-  // warp 0 first builds the finish map (any block may be the last one); the
-  // task counter balances its late start
-  if (wid == 0) {
+  // one warp builds the finish map (any block may be the last one): warp 0
+  // before its first task when the block has at least NW tasks (the task
+  // counter balances its late start); otherwise the last warp, which then
+  // takes no task, so the map is built while the other warps run the tasks
+  const int map_warp = (nt < NW) ? NW - 1 : 0;
+  if (wid == map_warp) {
     double xv[N];
 #pragma unroll
     for (int j = 0; j < N; ++j) xv[j] = xs[j];
@@ -801,7 +804,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
     }
   };
 
-  int task = grab();
+  int task = (nt < NW && wid == map_warp) ? nt : grab();
   int64_t trow = 0;
   int tcc0 = 0, tncc = 0;
   if (task < nt) {
