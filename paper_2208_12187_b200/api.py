@@ -151,14 +151,17 @@ def curve_fit(model, z, y=None, *, grid=None, p0=None, lb=None, ub=None, sigma=N
                           C.byref(opts), C.byref(res))
     if rc < 0:
         raise JFError(rc, "jf_curve_fit")
+    # numpy views of the ctypes arrays, copied (no per-element Python lists)
+    def arr(field_, k):
+        return np.frombuffer(field_, dtype=np.float64, count=k).copy()
     out = FitResult(
-        x=np.array(res.x[:n]), cost=res.cost, optimality=res.optimality, grad=np.array(res.grad[:n]),
-        gram=np.array(res.gram[: n * n]).reshape(n, n), pcov=np.array(res.pcov[: n * n]).reshape(n, n),
+        x=arr(res.x, n), cost=res.cost, optimality=res.optimality, grad=arr(res.grad, n),
+        gram=arr(res.gram, n * n).reshape(n, n), pcov=arr(res.pcov, n * n).reshape(n, n),
         status=res.status, nfev=res.nfev, njev=res.njev,
-        nit=res.nit, active_mask=np.array(res.active_mask[:n], dtype=np.int64),
+        nit=res.nit, active_mask=np.frombuffer(res.active_mask, dtype=np.int8, count=n).astype(np.int64),
         kernel_launches=res.kernel_launches, t_upload_s=res.t_upload_s, t_solve_s=res.t_solve_s,
-        t_epilogue_s=res.t_epilogue_s, epilogue_cycles=tuple(res.epilogue_cycles),
-        timeline_ns=tuple(res.timeline_ns[:res.timeline_len]))
+        t_epilogue_s=res.t_epilogue_s, epilogue_cycles=tuple(arr(res.epilogue_cycles, 8)),
+        timeline_ns=tuple(arr(res.timeline_ns, res.timeline_len)))
     if tr is not None:
         out.trace = tr[: res.trace_len].copy()
     return out
