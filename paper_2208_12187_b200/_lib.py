@@ -77,8 +77,8 @@ def load() -> C.CDLL:
     for f in ("jf_model_nparams", "jf_model_ydim", "jf_model_kslots"):
         getattr(lib, f).argtypes = [C.c_int32]
         getattr(lib, f).restype = C.c_int32
-    lib.jf_curve_fit.argtypes = [C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, dp, C.c_int32, dp, dp,
-                                 C.POINTER(jf_opts), C.POINTER(jf_result)]
+    lib.jf_curve_fit.argtypes = [C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.c_void_p,
+                                 C.c_void_p, C.POINTER(jf_opts), C.POINTER(jf_result)]
     lib.jf_curve_fit.restype = C.c_int32
     lib.jf_pass.argtypes = [C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, dp, C.c_int32,
                             C.POINTER(jf_opts), dp, dp, dp, ip]

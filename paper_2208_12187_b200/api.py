@@ -125,8 +125,8 @@ class FitResult:
     t_upload_s: float
     t_solve_s: float
     t_epilogue_s: float
-    epilogue_cycles: tuple = ()
-    timeline_ns: tuple = ()
+    epilogue_cycles: np.ndarray = field(default_factory=lambda: np.zeros(8))
+    timeline_ns: np.ndarray = field(default_factory=lambda: np.zeros(0))
     trace: np.ndarray = field(default_factory=lambda: np.zeros((0, L.JF_TRACE_FIELDS)))
 
 
@@ -147,7 +147,8 @@ def curve_fit(model, z, y=None, *, grid=None, p0=None, lb=None, ub=None, sigma=N
     lba = None if lb is None else _as_host(lb)
     uba = None if ub is None else _as_host(ub)
     res = L.jf_result()
-    rc = lib.jf_curve_fit(mid, data.yp, data.zp, data.m, _dptr(p0a), n, _dptr(lba), _dptr(uba),
+    rc = lib.jf_curve_fit(mid, data.yp, data.zp, data.m, None if p0a is None else p0a.ctypes.data, n,
+                          None if lba is None else lba.ctypes.data, None if uba is None else uba.ctypes.data,
                           C.byref(opts), C.byref(res))
     if rc < 0:
         raise JFError(rc, "jf_curve_fit")
@@ -160,8 +161,8 @@ def curve_fit(model, z, y=None, *, grid=None, p0=None, lb=None, ub=None, sigma=N
         status=res.status, nfev=res.nfev, njev=res.njev,
         nit=res.nit, active_mask=np.frombuffer(res.active_mask, dtype=np.int8, count=n).astype(np.int64),
         kernel_launches=res.kernel_launches, t_upload_s=res.t_upload_s, t_solve_s=res.t_solve_s,
-        t_epilogue_s=res.t_epilogue_s, epilogue_cycles=tuple(arr(res.epilogue_cycles, 8)),
-        timeline_ns=tuple(arr(res.timeline_ns, res.timeline_len)))
+        t_epilogue_s=res.t_epilogue_s, epilogue_cycles=arr(res.epilogue_cycles, 8),
+        timeline_ns=arr(res.timeline_ns, res.timeline_len))
     if tr is not None:
         out.trace = tr[: res.trace_len].copy()
     return out
