@@ -137,6 +137,7 @@ int ctx_init(Ctx& c, int dev) {
     std::lock_guard<std::mutex> g(attr_mu);
     if (!attr_done[dev]) {
       kernel_attrs_init();
+      kernel_attrs_init_x2();
       attr_done[dev] = true;
     }
   }
@@ -199,14 +200,17 @@ PassPair select_pass(Ctx& c, const Kernels& k, bool weighted, int64_t m) {
   p.j = weighted ? k.jkw : k.jk;
   p.r = weighted ? k.rkw : k.rk;
   p.jp = weighted ? k.jkpw : k.jkp;
-  p.jtpb = k.jtpb;
+  p.jtpb = (weighted && k.jwtpb > 0) ? k.jwtpb : k.jtpb;
   p.rtpb = k.rtpb;
   p.jptpb = k.jptpb;
   p.jsmem = weighted ? 0 : k.jsmem;
   p.jgrid = grid_for(c, p.j, p.jtpb, m, p.jsmem);
   p.jpgrid = p.jp ? grid_for(c, p.jp, p.jptpb, m) : 1;
-  if (k.jsplit) {  // two equal halves
+  const bool jsplit = (weighted && k.jwsplit >= 0) ? (k.jwsplit != 0) : k.jsplit;
+  if (jsplit) {  // two equal halves
     p.jgrid = p.jgrid < 2 ? 2 : p.jgrid + (p.jgrid & 1);
+  }
+  if (k.jsplit || k.jwsplit > 0) {  // the preconditioned (TSQR) kernel is always the dual-number one
     p.jpgrid = p.jpgrid < 2 ? 2 : p.jpgrid + (p.jpgrid & 1);
   }
   p.rgrid = grid_for(c, p.r, p.rtpb, m);

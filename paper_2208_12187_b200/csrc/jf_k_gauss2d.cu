@@ -24,6 +24,10 @@ static Kernels make() {
 }
 template <int L, int TPB, int MINB, int SEEDN = 4, int STG = 0>
 static void use_moment(Kernels& k) {
+  if (k.jwtpb == 0) {  // the dual-number kernel stays in use for weighted passes
+    k.jwtpb = k.jtpb;
+    k.jwsplit = k.jsplit ? 1 : 0;
+  }
   auto f = moment_pass_kernel<L, TPB, MINB, SEEDN, STG>;
   k.jk = f;
   k.jtpb = TPB;
@@ -32,6 +36,10 @@ static void use_moment(Kernels& k) {
 
 template <int L, int TC, int NW, int SEEDN = 4, int DBGZ = 0>
 static void use_task(Kernels& k) {
+  if (k.jwtpb == 0) {  // the dual-number kernel stays in use for weighted passes
+    k.jwtpb = k.jtpb;
+    k.jwsplit = k.jsplit ? 1 : 0;
+  }
   k.jk = moment_task_kernel<L, TC, NW, SEEDN, DBGZ>;
   k.jtpb = NW * 32;
   k.jsmem = moment_task_smem_bytes(NW);

@@ -1,6 +1,8 @@
 // jf_k_gauss2d_x2.cu — pass-kernel instances for ModelGauss2DRotX2 (see jf_pass.cuh).
 #include "jf_kernels.h"
-#include "jf_pass.cuh"
+#include <cstdlib>
+
+#include "jf_moment2.cuh"
 
 namespace jf {
 template <int C>
@@ -20,5 +22,28 @@ static Kernels make() {
   k.rtpb = PassCfg<ModelGauss2DRotX2, false>::TPB;
   return k;
 }
-Kernels kernels_gauss2d_x2(int coord) { return coord == COORD_EXPLICIT ? make<COORD_EXPLICIT>() : make<COORD_GRID>(); }
+template <int L, int TC, int NW>
+static void use_moment2(Kernels& k) {
+  if (k.jwtpb == 0) {  // the dual-number kernel stays in use for weighted passes
+    k.jwtpb = k.jtpb;
+    k.jwsplit = k.jsplit ? 1 : 0;
+  }
+  k.jk = moment2_task_kernel<L, TC, NW>;
+  k.jtpb = NW * 32;
+  k.jsmem = moment2_task_smem_bytes(NW);
+  k.jsplit = false;
+}
+void kernel_attrs_init_x2() {
+  cudaFuncSetAttribute((const void*)moment2_task_kernel<8, 8, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       moment2_task_smem_bytes(12));
+}
+Kernels kernels_gauss2d_x2(int coord) {
+  Kernels k = coord == COORD_EXPLICIT ? make<COORD_EXPLICIT>() : make<COORD_GRID>();
+  if (coord == COORD_GRID) {
+    // unweighted implicit grid: the moment-form J-pass (jf_moment2.cuh)
+    const char* v = getenv("JF_X2VARIANT");  // development aid: 9 = the dual-number kernel
+    if (!(v && atoi(v) == 9)) use_moment2<8, 8, 12>(k);
+  }
+  return k;
+}
 }  // namespace jf

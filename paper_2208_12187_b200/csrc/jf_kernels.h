@@ -19,6 +19,8 @@ struct Kernels {
   int jptpb = 256;             // threads per block of the preconditioned J kernel
   int jsmem = 0;               // dynamic shared memory of the J kernel (bytes)
   bool jsplit = false;         // J grid split in two halves (even grid >= 2)
+  int jwtpb = 0;               // weighted J kernel's block size / split when jk is a moment kernel
+  int jwsplit = -1;            //   (0 / -1: same as jtpb / jsplit)
   SmallFitFn small = nullptr;  // whole-fit single-block kernel (small m), unweighted / weighted
   SmallFitFn smallw = nullptr;
 };
@@ -31,4 +33,5 @@ Kernels kernels_gauss2d_x2(int coord);
 // device when its first context is created — never during a pass, when an
 // attribute call could wait on the spinning kernels of emulated peer ranks.
 void kernel_attrs_init();
+void kernel_attrs_init_x2();
 }  // namespace jf

@@ -57,6 +57,8 @@ CASES = [
     ("gauss2d W=2600x37", lambda: dg.make_gauss2d(2600, H=37)),
     ("gauss2d_x2 W=96", lambda: dg.make_gauss2d_x2(96)),
     ("gauss2d_x2 W=700x333", lambda: dg.make_gauss2d_x2(700, H=333)),
+    ("gauss2d_x2 W=2048x40", lambda: dg.make_gauss2d_x2(2048, H=40)),
+    ("gauss2d_x2 W=2600x31", lambda: dg.make_gauss2d_x2(2600, H=31)),
 ]
 
 
@@ -108,6 +110,17 @@ def test_nonfinite_counts_and_weighted_pass():
     check_pass(jf.jpass(pr.model, pr.z, pr.p0, y=pr.t, sigma=sig), ref)
 
 
+@pytest.mark.parametrize("make", [lambda: dg.make_gauss2d(300, H=77), lambda: dg.make_gauss2d_x2(160, H=90)],
+                         ids=["gauss2d", "gauss2d_x2"])
+def test_weighted_grid_pass_uses_dual_kernel_shape(make):
+    """Weighted implicit-grid passes run the dual-number kernels (the moment
+    kernels are unweighted) with their own launch shape."""
+    pr = make()
+    sig = np.random.default_rng(3).uniform(0.5, 2.0, pr.m)
+    ref = orp.jpass(pr.model, pr.coords(), pr.z, pr.p0, sigma=sig)
+    check_pass(jf.jpass(pr.model, pr.z, pr.p0, grid=pr.grid, sigma=sig), ref)
+
+
 def test_nonfinite_counts_moment_kernel():
     """Non-finite residuals in whole-task (fast path) and row-end chunks are
     counted exactly (per-chunk sum r^2 test + replay) in the moment J-pass."""
@@ -119,6 +132,11 @@ def test_nonfinite_counts_moment_kernel():
     _, _, _, bad = jf.jpass(pr.model, z, pr.p0, grid=pr.grid)
     _, bad_r = jf.residual_pass(pr.model, z, pr.p0, grid=pr.grid)
     assert bad == len(idx) and bad_r == len(idx)
+    pr2 = dg.make_gauss2d_x2(2600, H=23)  # the two-component moment kernel
+    z2 = pr2.z.copy()
+    z2[idx[:4]] = np.nan
+    z2[idx[4:]] = np.inf
+    assert jf.jpass(pr2.model, z2, pr2.p0, grid=pr2.grid)[3] == len(idx)
 
 
 def test_pass_is_bitwise_deterministic():
