@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
   const int cpr = (W + CW - 1) / CW;
   const int nblk = gridDim.x;
   int tcr = TC < cpr ? TC : cpr;
-  while (((H * (int64_t)((cpr + tcr - 1) / tcr)) + nblk - 1) / nblk > MAXT) ++tcr;
+  while (((H * (int64_t)((cpr + tcr - 1) / tcr)) + nblk - 1) / nblk > MAXT) tcr += (tcr < TC) ? 1 : TC;  // whole sub-runs
   const int tpr = (cpr + tcr - 1) / tcr;
   const int64_t ntask = H * (int64_t)tpr;
   const int64_t t_begin = (int64_t)blockIdx.x * ntask / nblk, t_end = (int64_t)(blockIdx.x + 1) * ntask / nblk;
@@ -266,11 +266,21 @@ __global__ void __launch_bounds__(NW * 32, 1)
     for (int i = 0; i < 3; ++i) Q1[i] = Q2[i] = R1[i] = R2[i] = 0.0;
     sr = srr = 0.0;
     bad = 0;
-    // origin of the running moments: X of the lane's first pixel of the task
-    const double Xo = (double)(cc0 * CW + lane);
-    bool fast = false;
-    {
-      const int c0 = cc0 * CW;
+    // origin of the running moments: X of the lane's first pixel of the
+    // current sub-run (runs of TC chunks; a task longer than TC chunks —
+    // large images, MAXT — is several sub-runs, the origin advanced between
+    // them by a Taylor shift)
+    double Xo = (double)(cc0 * CW + lane);
+    const int nsub = (ncc + TC - 1) / TC;
+    for (int sub = 0; sub < nsub; ++sub) {
+      if (sub > 0) {
+        shift(-(double)(TC * CW));
+        Xo += (double)(TC * CW);
+      }
+      const int ncs = min(TC, ncc - sub * TC);
+      const int ccs = cc0 + sub * TC;
+      const bool last_sub = (sub + 1 == nsub);
+      const int c0 = ccs * CW;
       const double da1 = Xo - x01, db1 = da1 + D * (TC * L - 1);
       const double da2 = Xo - x02, db2 = da2 + D * (TC * L - 1);
       const double qa1 = da1 * (a1 * da1 + b1 * dy1) + c1 * (dy1 * dy1);
@@ -284,17 +294,17 @@ __global__ void __launch_bounds__(NW * 32, 1)
       const bool ok = qa1 < 600.0 && qb1 < 600.0 && qa2 < 600.0 && qb2 < 600.0 && fabs(ra1) < 300.0 &&
                       fabs(rb1) < 300.0 && fabs(ra2) < 300.0 && fabs(rb2) < 300.0 &&
                       2.0 * a1 * D * D * (TC * L) < 300.0 && 2.0 * a2 * D * D * (TC * L) < 300.0;
-      fast = (ncc == TC) && (c0 + TC * CW <= W) && __all_sync(FULL, ok);  // warp-uniform
+      const bool fast = (ncs == TC) && (c0 + TC * CW <= W) && __all_sync(FULL, ok);  // warp-uniform
       if (fast) {
-        // whole task: two row recurrences, t = D (L j + k) from the task's first pixel
+        // TC chunks: two row recurrences, t = D (L j + k) from the sub-run's first pixel
         double E1 = exp(-qa1), S1 = exp(-ra1), E2 = exp(-qa2), S2 = exp(-ra2);
 #pragma unroll
         for (int j = 0; j < TC; ++j) {
           double zc[L];
 #pragma unroll
           for (int k = 0; k < L; ++k) zc[k] = zn[k];
-          if (j + 1 < TC) {
-            load(row, cc0 + j + 1);
+          if (j + 1 < TC || !last_sub) {
+            load(row, ccs + j + 1);
           } else {
             next = grab();
             if (next < nt) {
@@ -324,31 +334,32 @@ __global__ void __launch_bounds__(NW * 32, 1)
             }
           }
         }
-      }
-    }
-    for (int j = 0; j < (fast ? 0 : ncc); ++j) {
-      // ragged row end or unsafe exponent range: direct evaluation, t from the task's first pixel
-      double zc[L];
-#pragma unroll
-      for (int k = 0; k < L; ++k) zc[k] = zn[k];
-      if (j + 1 < ncc) {
-        load(row, cc0 + j + 1);
       } else {
-        next = grab();
-        if (next < nt) {
-          task_pos(next, trow, tcc0, tncc);
-          load(trow, tcc0);
-        }
-      }
-      const int c0 = (cc0 + j) * CW;
+        for (int j = 0; j < ncs; ++j) {
+          // ragged row end or unsafe exponent range: direct evaluation, t from the sub-run's first pixel
+          double zc[L];
 #pragma unroll
-      for (int k = 0; k < L; ++k) {
-        if (c0 + lane + 32 * k < W) {
-          const double X = (double)(c0 + lane + 32 * k);
-          const double d1 = X - x01, d2 = X - x02;
-          const double u1 = exp(-(d1 * (a1 * d1 + b1 * dy1) + c1 * (dy1 * dy1)));
-          const double u2 = exp(-(d2 * (a2 * d2 + b2 * dy2) + c2 * (dy2 * dy2)));
-          point(u1, u2, X - Xo, zc[k], true);
+          for (int k = 0; k < L; ++k) zc[k] = zn[k];
+          if (j + 1 < ncs || !last_sub) {
+            load(row, ccs + j + 1);
+          } else {
+            next = grab();
+            if (next < nt) {
+              task_pos(next, trow, tcc0, tncc);
+              load(trow, tcc0);
+            }
+          }
+          const int cj0 = (ccs + j) * CW;
+#pragma unroll
+          for (int k = 0; k < L; ++k) {
+            if (cj0 + lane + 32 * k < W) {
+              const double X = (double)(cj0 + lane + 32 * k);
+              const double d1 = X - x01, d2 = X - x02;
+              const double u1 = exp(-(d1 * (a1 * d1 + b1 * dy1) + c1 * (dy1 * dy1)));
+              const double u2 = exp(-(d2 * (a2 * d2 + b2 * dy2) + c2 * (dy2 * dy2)));
+              point(u1, u2, X - Xo, zc[k], true);
+            }
+          }
         }
       }
     }
