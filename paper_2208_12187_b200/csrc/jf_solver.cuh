@@ -875,14 +875,18 @@ __device__ __noinline__ void st_outer_top(FitState* st, SolverSmem& S) {
     return;
   }
   // register copies first: every load is issued before any store (the
-  // state lives in shared memory; interleaved stores would serialise them)
-  double dd[n], dh[n], gj[n], G[n][n];
+  // state lives in shared memory; interleaved stores would serialise them).
+  // n > 8: G read in place (a register copy would spill)
+  constexpr int NG = n <= 8 ? n : 1;
+  double dd[n], dh[n], gj[n], G[NG][NG];
   const bool bounded = st->bounded;
 #pragma unroll
   for (int j = 0; j < n; ++j) {
     gj[j] = st->g[j];
+    if constexpr (n <= 8) {
 #pragma unroll
-    for (int k = 0; k < n; ++k) G[j][k] = st->G[j * NMAX + k];
+      for (int k = 0; k < n; ++k) G[j][k] = st->G[j * NMAX + k];
+    }
   }
 #pragma unroll
   for (int j = 0; j < n; ++j) {
@@ -907,7 +911,9 @@ __device__ __noinline__ void st_outer_top(FitState* st, SolverSmem& S) {
   for (int i = 0; i < n; ++i) {  // B_hat = d G d (+ diag_h)
 #pragma unroll
     for (int j = 0; j < n; ++j) {
-      double b = dd[i] * G[i][j] * dd[j];
+      double b;
+      if constexpr (n <= 8) b = dd[i] * G[i][j] * dd[j];
+      else b = dd[i] * st->G[i * NMAX + j] * dd[j];
       if (i == j) b += dh[i];
       st->Gh[i * NMAX + j] = b;
       S.M[i][j] = b;  // the trial's copy (st_trial_begin)
