@@ -32,7 +32,7 @@ HBM = 6467.1e9
 P64 = 148 * 64 * 1.965e9  # FP64 instr/s
 # FP64 instructions per point of each J-pass as built (the
 # dual-number counts are SURVEY §8(d) d.3's), bytes per point of the inputs
-ALG = {"exp_decay": (16, 33), "gauss1d": (8, 43), "gauss2d_rot": (8, 19), "gauss2d_rot_x2": (8, 202)}
+ALG = {"exp_decay": (16, 33), "gauss1d": (8, 43), "gauss2d_rot": (8, 19), "gauss2d_rot_x2": (8, 41)}
 
 
 def problems():
