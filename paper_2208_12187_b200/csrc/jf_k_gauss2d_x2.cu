@@ -36,13 +36,20 @@ static void use_moment2(Kernels& k) {
 void kernel_attrs_init_x2() {
   cudaFuncSetAttribute((const void*)moment2_task_kernel<8, 8, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        moment2_task_smem_bytes(12));
+  cudaFuncSetAttribute((const void*)moment2_task_kernel<8, 8, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       moment2_task_smem_bytes(8));
+  cudaFuncSetAttribute((const void*)moment2_task_kernel<8, 4, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       moment2_task_smem_bytes(12));
 }
 Kernels kernels_gauss2d_x2(int coord) {
   Kernels k = coord == COORD_EXPLICIT ? make<COORD_EXPLICIT>() : make<COORD_GRID>();
   if (coord == COORD_GRID) {
     // unweighted implicit grid: the moment-form J-pass (jf_moment2.cuh)
     const char* v = getenv("JF_X2VARIANT");  // development aid: 9 = the dual-number kernel
-    if (!(v && atoi(v) == 9)) use_moment2<8, 8, 12>(k);
+    const int var = v ? atoi(v) : 0;
+    if (var == 1) use_moment2<8, 8, 8>(k);
+    else if (var == 2) use_moment2<8, 4, 12>(k);
+    else if (var != 9) use_moment2<8, 8, 12>(k);
   }
   return k;
 }

@@ -135,10 +135,10 @@ __device__ __forceinline__ int kalt_terms(const PreGauss2D& g, int x, int y, int
 // algebra as moments_to_kvec followed by apply_chain_kvec, composed once.
 constexpr int FMAP_COLS = MomLayout::NV + 1;
 template <class Pre>
-__device__ __forceinline__ void build_finish_map(const Pre& pre, double (*C)[FMAP_COLS], int lane) {
+__device__ __forceinline__ void build_finish_map(const Pre& pre, double (*C)[FMAP_COLS], int t0, int nthr) {
   using Model = ModelGauss2DRot;
   constexpr int N = Model::N, N1 = N + 1, KT = tri_count(N);
-  for (int t = lane; t < KT; t += 32) {
+  for (int t = t0; t < KT; t += nthr) {
     for (int i = 0; i < FMAP_COLS; ++i) C[t][i] = 0.0;
     int j = 0, rem = t;
     while (rem >= N1 - j) {
@@ -721,13 +721,17 @@ __global__ void __launch_bounds__(NW * 32, 1)
   // before its first task when the block has at least NW tasks (the task
   // counter balances its late start); otherwise the last warp, which then
   // takes no task, so the map is built while the other warps run the tasks
+  // (with fewer tasks than warps, every warp beyond the task count builds a
+  // share of the map's rows, one row per lane)
   const int map_warp = (nt < NW) ? NW - 1 : 0;
-  if (wid == map_warp) {
+  const bool map_builder = (nt < NW) ? (wid >= nt) : (wid == 0);
+  if (map_builder) {
     double xv[N];
 #pragma unroll
     for (int j = 0; j < N; ++j) xv[j] = xs[j];
     const auto pre = Model::template prologue<true>(xv);
-    build_finish_map(pre, fmap, lane);
+    if (nt < NW) build_finish_map(pre, fmap, (wid - nt) * 32 + lane, (NW - nt) * 32);
+    else build_finish_map(pre, fmap, lane, 32);
   }
 
   double P[5], Q[3], R[3], sr, srr;
@@ -804,7 +808,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
     }
   };
 
-  int task = (nt < NW && wid == map_warp) ? nt : grab();
+  int task = (nt < NW && map_builder) ? nt : grab();
+  (void)map_warp;
   int64_t trow = 0;
   int tcc0 = 0, tncc = 0;
   if (task < nt) {
