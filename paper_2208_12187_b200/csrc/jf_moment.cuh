@@ -697,14 +697,18 @@ __global__ void __launch_bounds__(NW * 32, 1)
   // tasks so the warps run out of work within about one chunk of each other;
   // measured slower at 4096^2 — the per-task overhead outweighs the balance)
   constexpr int TSPLIT = 0;
-  int tcr = TC < cpr ? TC : cpr;
-  while (((H * (int64_t)((cpr + tcr - 1) / tcr)) + nblk - 1) / nblk + TSPLIT * (tcr - 1) > MAXT) ++tcr;
+  // More tasks than MAXT slots: the block runs them in rounds of MAXT (the
+  // slot sums of each round are added in round order: still a fixed order).
+  const int tcr = TC < cpr ? TC : cpr;
   const int tpr = (cpr + tcr - 1) / tcr;  // tasks per row
   const int64_t ntask = H * (int64_t)tpr;
   const int64_t t_begin = (int64_t)blockIdx.x * ntask / nblk, t_end = (int64_t)(blockIdx.x + 1) * ntask / nblk;
   const int nt_big = (int)(t_end - t_begin);
   const int nbig = nt_big > TSPLIT ? nt_big - TSPLIT : 0;  // tasks kept whole
-  const int nt = nbig + (nt_big - nbig) * tcr;              // task slots (single-chunk tail tasks may be empty)
+  const int nt_all = nbig + (nt_big - nbig) * tcr;          // tasks (single-chunk tail tasks may be empty)
+  const int nround = nt_all > MAXT ? (nt_all + MAXT - 1) / MAXT : 1;
+  int rbase = 0;                                            // first task of the current round
+  int nt = nt_all < MAXT ? nt_all : MAXT;                   // tasks of the current round
 
   const double rho = exp(-2.0 * ga * D * D);
   const double* __restrict__ z = a.z;
@@ -723,14 +727,14 @@ __global__ void __launch_bounds__(NW * 32, 1)
   // takes no task, so the map is built while the other warps run the tasks
   // (with fewer tasks than warps, every warp beyond the task count builds a
   // share of the map's rows, one row per lane)
-  const int map_warp = (nt < NW) ? NW - 1 : 0;
-  const bool map_builder = (nt < NW) ? (wid >= nt) : (wid == 0);
+  const int map_warp = (nt_all < NW) ? NW - 1 : 0;
+  const bool map_builder = (nt_all < NW) ? (wid >= nt_all) : (wid == 0);
   if (map_builder) {
     double xv[N];
 #pragma unroll
     for (int j = 0; j < N; ++j) xv[j] = xs[j];
     const auto pre = Model::template prologue<true>(xv);
-    if (nt < NW) build_finish_map(pre, fmap, (wid - nt) * 32 + lane, (NW - nt) * 32);
+    if (nt_all < NW) build_finish_map(pre, fmap, (wid - nt_all) * 32 + lane, (NW - nt_all) * 32);
     else build_finish_map(pre, fmap, lane, 32);
   }
 
@@ -775,6 +779,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
   const int64_t row_b = t_begin / tpr;
   const int k_b = (int)(t_begin - row_b * tpr);
   auto task_pos = [&](int t, int64_t& row, int& cc0, int& ncc) {
+    t += rbase;
     int sub = -1;
     if (t >= nbig) {  // single-chunk tail task: chunk sub of whole task bt
       sub = (t - nbig) % tcr;
@@ -808,8 +813,16 @@ __global__ void __launch_bounds__(NW * 32, 1)
     }
   };
 
-  int task = (nt < NW && map_builder) ? nt : grab();
   (void)map_warp;
+  double bsum = 0.0;  // this thread's (entry, segment) share of the block partial, over the rounds
+  for (int rd = 0; rd < nround; ++rd) {
+  if (rd > 0) {
+    rbase = rd * MAXT;
+    nt = min(MAXT, nt_all - rbase);
+    if (tid == 0) next_task = 0;
+    __syncthreads();
+  }
+  int task = (nt_all < NW && map_builder) ? nt : grab();
   int64_t trow = 0;
   int tcc0 = 0, tncc = 0;
   if (task < nt) {
@@ -1048,12 +1061,18 @@ __global__ void __launch_bounds__(NW * 32, 1)
     }
     task = next;
   }
+  __syncthreads();
+  if (tid < NW * KS) {  // the round's slots, in slot order, into this thread's share
+    const int i = tid % KS, seg = tid / KS;
+    for (int t = seg; t < nt; t += NW) bsum += tslot[t][i];
+  }
+  __syncthreads();  // the slots are reused by the next round
+  }  // rounds
   if (a.dbg && lane == 0 && blockIdx.x * NW + wid < 16384) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     a.dbg[(blockIdx.x * NW + wid) * 4 + 2] = t;
   }
-  __syncthreads();
 
   // ---- block partial: the task slots summed in task order, then (unless
   // debugging the alt coordinates) mapped through the finish map here, so
@@ -1061,12 +1080,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
   const bool mapped = !a.no_chain;
   {
     static_assert(NW * KS <= TPB, "one (entry, segment) per thread");
-    if (tid < NW * KS) {
-      const int i = tid % KS, seg = tid / KS;
-      double s = 0.0;
-      for (int t = seg; t < nt; t += NW) s += tslot[t][i];
-      red[seg][i] = s;
-    }
+    if (tid < NW * KS) red[tid / KS][tid % KS] = bsum;
     __syncthreads();
     for (int k = tid; k < KS; k += TPB) {
       double s = 0.0;

@@ -173,15 +173,21 @@ __global__ void __launch_bounds__(NW * 32, 1)
   const int cpr = (W + CW - 1) / CW;
   const int nblk = gridDim.x;
   int tcr = TC < cpr ? TC : cpr;
-  while (((H * (int64_t)((cpr + tcr - 1) / tcr)) + nblk - 1) / nblk > MAXT) tcr += (tcr < TC) ? 1 : TC;  // whole sub-runs
+  // longer tasks (whole sub-runs of TC chunks, at most a row) while the block
+  // would have more than MAXT; beyond that the block runs rounds of MAXT tasks
+  while (((H * (int64_t)((cpr + tcr - 1) / tcr)) + nblk - 1) / nblk > MAXT && tcr < cpr)
+    tcr += (tcr < TC) ? 1 : TC;
   const int tpr = (cpr + tcr - 1) / tcr;
   const int64_t ntask = H * (int64_t)tpr;
   const int64_t t_begin = (int64_t)blockIdx.x * ntask / nblk, t_end = (int64_t)(blockIdx.x + 1) * ntask / nblk;
-  const int nt = (int)(t_end - t_begin);
+  const int nt_all = (int)(t_end - t_begin);
+  const int nround = nt_all > MAXT ? (nt_all + MAXT - 1) / MAXT : 1;
+  int rbase = 0;                             // first task of the current round
+  int nt = nt_all < MAXT ? nt_all : MAXT;    // tasks of the current round
   const int64_t row_b = t_begin / tpr;
   const int k_b = (int)(t_begin - row_b * tpr);
   auto task_pos = [&](int t, int64_t& row, int& cc0, int& ncc) {
-    const int g = k_b + t;
+    const int g = k_b + rbase + t;
     const int dr = g / tpr;
     row = row_b + dr;
     cc0 = (g - dr * tpr) * tcr;
@@ -246,6 +252,15 @@ __global__ void __launch_bounds__(NW * 32, 1)
     }
   };
 
+  constexpr int NSEG = TPB / KS > 0 ? (TPB / KS < NW ? TPB / KS : NW) : 1;
+  double bsum = 0.0;  // this thread's (entry, segment) share of the block partial, over the rounds
+  for (int rd = 0; rd < nround; ++rd) {
+  if (rd > 0) {
+    rbase = rd * MAXT;
+    nt = min(MAXT, nt_all - rbase);
+    if (tid == 0) next_task = 0;
+    __syncthreads();
+  }
   int task = grab();
   int64_t trow = 0;
   int tcc0 = 0, tncc = 0;
@@ -436,16 +451,16 @@ __global__ void __launch_bounds__(NW * 32, 1)
     task = next;
   }
   __syncthreads();
+  if (tid < NSEG * KS) {  // the round's slots, in slot order, into this thread's share
+    const int i = tid % KS, seg = tid / KS;
+    for (int t = seg; t < nt; t += NSEG) bsum += tslot[t][i];
+  }
+  __syncthreads();  // the slots are reused by the next round
+  }  // rounds
 
-  // ---- block partial: the task slots summed in task order
+  // ---- block partial: the task slots summed in task order (round by round)
   {
-    constexpr int NSEG = TPB / KS > 0 ? (TPB / KS < NW ? TPB / KS : NW) : 1;
-    if (tid < NSEG * KS) {
-      const int i = tid % KS, seg = tid / KS;
-      double s = 0.0;
-      for (int t = seg; t < nt; t += NSEG) s += tslot[t][i];
-      red[seg][i] = s;
-    }
+    if (tid < NSEG * KS) red[tid / KS][tid % KS] = bsum;
     __syncthreads();
     unsigned long long pol;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));

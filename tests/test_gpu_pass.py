@@ -121,6 +121,19 @@ def test_weighted_grid_pass_uses_dual_kernel_shape(make):
     check_pass(jf.jpass(pr.model, pr.z, pr.p0, grid=pr.grid, sigma=sig), ref)
 
 
+@pytest.mark.parametrize("make", [lambda: dg.make_gauss2d(64, H=17000), lambda: dg.make_gauss2d_x2(64, H=15000)],
+                         ids=["gauss2d", "gauss2d_x2"])
+def test_moment_kernel_task_rounds(make):
+    """Tall images give a block more tasks than its slots: the moment kernels
+    run them in rounds (fixed order) — same result, bitwise reproducible."""
+    pr = make()
+    ref = orp.jpass(pr.model, pr.coords(), pr.z, pr.p0)
+    a = jf.jpass(pr.model, pr.z, pr.p0, grid=pr.grid)
+    check_pass(a, ref)
+    b = jf.jpass(pr.model, pr.z, pr.p0, grid=pr.grid)
+    assert a[0] == b[0] and np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
+
+
 def test_nonfinite_counts_moment_kernel():
     """Non-finite residuals in whole-task (fast path) and row-end chunks are
     counted exactly (per-chunk sum r^2 test + replay) in the moment J-pass."""
