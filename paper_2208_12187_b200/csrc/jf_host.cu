@@ -785,9 +785,18 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
     } else {
       ge = it->second;
     }
+    const auto tl0 = std::chrono::steady_clock::now();
     CK(cudaGraphLaunch(ge, s));
+    const auto tl1 = std::chrono::steady_clock::now();
     CK(cudaMemcpyAsync(&h, c->d_state, sizeof(h), cudaMemcpyDeviceToHost, s));
+    const auto tl2 = std::chrono::steady_clock::now();
     CK(cudaStreamSynchronize(s));
+    if (getenv("JF_DEBUG_FIT_TIMES")) {  // development aid: host-side phases of the graph fit
+      const auto tl3 = std::chrono::steady_clock::now();
+      auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+      fprintf(stderr, "jf fit: prep->launch %.1f us, cudaGraphLaunch %.1f us, D2H enqueue %.1f us, sync %.1f us\n",
+              us(t0, tl0), us(tl0, tl1), us(tl1, tl2), us(tl2, tl3));
+    }
   } else {
     const int cap = 4 * h.max_nfev + 8;
     for (int iter = 0; iter < cap; ++iter) {
