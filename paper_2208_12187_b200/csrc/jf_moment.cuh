@@ -814,7 +814,9 @@ __global__ void __launch_bounds__(NW * 32, 1)
   };
 
   (void)map_warp;
-  double bsum = 0.0;  // this thread's (entry, segment) share of the block partial, over the rounds
+  // this thread's (entry, segment) share of the block partial, accumulated
+  // over the rounds in shared memory (keeps it out of the hot loop's registers)
+  if (tid < NW * KS) red[tid / KS][tid % KS] = 0.0;
   for (int rd = 0; rd < nround; ++rd) {
   if (rd > 0) {
     rbase = rd * MAXT;
@@ -1064,7 +1066,9 @@ __global__ void __launch_bounds__(NW * 32, 1)
   __syncthreads();
   if (tid < NW * KS) {  // the round's slots, in slot order, into this thread's share
     const int i = tid % KS, seg = tid / KS;
+    double bsum = red[seg][i];
     for (int t = seg; t < nt; t += NW) bsum += tslot[t][i];
+    red[seg][i] = bsum;
   }
   __syncthreads();  // the slots are reused by the next round
   }  // rounds
@@ -1080,8 +1084,6 @@ __global__ void __launch_bounds__(NW * 32, 1)
   const bool mapped = !a.no_chain;
   {
     static_assert(NW * KS <= TPB, "one (entry, segment) per thread");
-    if (tid < NW * KS) red[tid / KS][tid % KS] = bsum;
-    __syncthreads();
     for (int k = tid; k < KS; k += TPB) {
       double s = 0.0;
 #pragma unroll
