@@ -34,19 +34,19 @@ static void use_moment(Kernels& k) {
   k.jsmem = moment_smem_bytes(L, TPB, STG);
 }
 
-template <int L, int TC, int NW, int SEEDN = 4, int DBGZ = 0>
+template <int L, int TC, int NW, int SEEDN = 4, int DBGZ = 0, bool FASTP = true>
 static void use_task(Kernels& k) {
   if (k.jwtpb == 0) {  // the dual-number kernel stays in use for weighted passes
     k.jwtpb = k.jtpb;
     k.jwsplit = k.jsplit ? 1 : 0;
   }
-  k.jk = moment_task_kernel<L, TC, NW, SEEDN, DBGZ>;
+  k.jk = moment_task_kernel<L, TC, NW, SEEDN, DBGZ, FASTP>;
   k.jtpb = NW * 32;
   k.jsmem = moment_task_smem_bytes(NW);
 }
-template <int L, int TC, int NW, int SEEDN = 4, int DBGZ = 0>
+template <int L, int TC, int NW, int SEEDN = 4, int DBGZ = 0, bool FASTP = true>
 static void attr_task() {
-  cudaFuncSetAttribute((const void*)moment_task_kernel<L, TC, NW, SEEDN, DBGZ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute((const void*)moment_task_kernel<L, TC, NW, SEEDN, DBGZ, FASTP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        moment_task_smem_bytes(NW));
 }
 template <int L, int TPB, int MINB, int SEEDN, int STG>
@@ -62,6 +62,7 @@ void kernel_attrs_init() {
   attr_task<8, 8, 16>();
   attr_task<32, 2, 8, 2>();
   attr_task<16, 4, 12, 4, 1>();
+  attr_task<16, 4, 12, 4, 0, false>();
   attr_moment<16, 128, 3, 4, 3>();
   attr_moment<16, 128, 3, 4, 4>();
   attr_moment<8, 128, 4, 8, 4>();
@@ -89,6 +90,7 @@ Kernels kernels_gauss2d(int coord) {
       if (var == 34) use_task<8, 8, 16>(k);
       if (var == 35) use_task<32, 2, 8, 2>(k);
       if (var == 39) use_task<16, 4, 12, 4, 1>(k);  // compute-only probe (wrong results)
+      if (var == 40) use_task<16, 4, 12, 4, 0, false>(k);  // no whole-task fast path
       if (var == 13) use_moment<32, 128, 2, 2>(k);
       if (var == 20) use_moment<16, 128, 3, 4, 3>(k);
       if (var == 21) use_moment<16, 128, 3, 4, 4>(k);

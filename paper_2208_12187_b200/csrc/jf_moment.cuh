@@ -624,7 +624,7 @@ constexpr int MOMENT_MAXT = 112;  // task slots per block of moment_task_kernel
 __host__ __device__ constexpr int moment_task_smem_bytes(int NW) {
   return (MOMENT_MAXT * MomLayout::KS + NW * 13 * 33) * 8;
 }
-template <int L, int TC, int NW, int SEEDN = 4, int DBGZ = 0>
+template <int L, int TC, int NW, int SEEDN = 4, int DBGZ = 0, bool FASTP = true>
 __global__ void __launch_bounds__(NW * 32, 1)
     moment_task_kernel(const PassArgs* __restrict__ pa, FitState* __restrict__ st, cudaGraphConditionalHandle cond,
                        int use_cond) {
@@ -863,7 +863,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
       const double rb = D * (2.0 * ga * dxb + gb2 * dy) + ga * D * D;
       const bool ok = qa < 600.0 && qb < 600.0 && fabs(ra) < 300.0 && fabs(rb) < 300.0 &&
                       2.0 * ga * D * D * (TC * L) < 300.0;
-      fast = (ncc == TC) && (c0 + TC * CW <= W) && __all_sync(FULL, ok);  // warp-uniform
+      fast = FASTP && (ncc == TC) && (c0 + TC * CW <= W) && __all_sync(FULL, ok);  // warp-uniform
       if (fast) {
         org = dxa;
         E = exp(-qa);
