@@ -296,7 +296,7 @@ def main():
     achieved = BYTES_PER_POINT * m_local / t_j / 1e9
     fp64_achieved = 2.0 * ALG_FP64_INSTR_PER_POINT * m_local / t_j / 1e12
     roofline = {
-        "bound": "hbm", "kernel": "moment_task_kernel<16,4,12> (moment-form J-pass, n=7 implicit grid, fp64)",
+        "bound": "hbm", "kernel": "moment_task_kernel<16,4,12,4,0,2> (moment-form J-pass, n=7 implicit grid, fp64)",
         "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
         "traffic": None, "launch_us": t_j * 1e6,
         "alg_work": f"{BYTES_PER_POINT} B/point (z) x {m_local} points; "

@@ -34,7 +34,7 @@ static void use_moment(Kernels& k) {
   k.jsmem = moment_smem_bytes(L, TPB, STG);
 }
 
-template <int L, int TC, int NW, int SEEDN = 4, int DBGZ = 0, bool FASTP = true>
+template <int L, int TC, int NW, int SEEDN = 4, int DBGZ = 0, int FASTP = 1>
 static void use_task(Kernels& k) {
   if (k.jwtpb == 0) {  // the dual-number kernel stays in use for weighted passes
     k.jwtpb = k.jtpb;
@@ -44,7 +44,7 @@ static void use_task(Kernels& k) {
   k.jtpb = NW * 32;
   k.jsmem = moment_task_smem_bytes(NW);
 }
-template <int L, int TC, int NW, int SEEDN = 4, int DBGZ = 0, bool FASTP = true>
+template <int L, int TC, int NW, int SEEDN = 4, int DBGZ = 0, int FASTP = 1>
 static void attr_task() {
   cudaFuncSetAttribute((const void*)moment_task_kernel<L, TC, NW, SEEDN, DBGZ, FASTP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        moment_task_smem_bytes(NW));
@@ -55,14 +55,16 @@ static void attr_moment() {
                        cudaFuncAttributeMaxDynamicSharedMemorySize, moment_smem_bytes(L, TPB, STG));
 }
 void kernel_attrs_init() {
-  attr_task<16, 4, 12>();
+  attr_task<16, 4, 12, 4, 0, 2>();
   attr_task<16, 2, 12>();
   attr_task<16, 4, 16>();
   attr_task<16, 8, 12>();
   attr_task<8, 8, 16>();
   attr_task<32, 2, 8, 2>();
   attr_task<16, 4, 12, 4, 1>();
-  attr_task<16, 4, 12, 4, 0, false>();
+  attr_task<16, 4, 12, 4, 0, 0>();
+  attr_task<16, 4, 12, 4, 0, 1>();
+  attr_task<16, 4, 12, 4, 0, 2>();
   attr_moment<16, 128, 3, 4, 3>();
   attr_moment<16, 128, 3, 4, 4>();
   attr_moment<8, 128, 4, 8, 4>();
@@ -77,7 +79,7 @@ Kernels kernels_gauss2d(int coord) {
   if (coord == COORD_GRID) {
     // unweighted implicit grid: the moment-form J-pass (jf_moment.cuh),
     // task-scheduled, one block of 12 warps per SM
-    use_task<16, 4, 12>(k);
+    use_task<16, 4, 12, 4, 0, 2>(k);
     if (const char* v = getenv("JF_JVARIANT")) {  // development aid: alternative shapes
       const int var = atoi(v);
       if (var == 9) { k.jk = pass_kernel<ModelGauss2DRot, true, COORD_GRID, false>; k.jtpb = 256; k.jsmem = 0; }  // dual numbers
@@ -90,7 +92,8 @@ Kernels kernels_gauss2d(int coord) {
       if (var == 34) use_task<8, 8, 16>(k);
       if (var == 35) use_task<32, 2, 8, 2>(k);
       if (var == 39) use_task<16, 4, 12, 4, 1>(k);  // compute-only probe (wrong results)
-      if (var == 40) use_task<16, 4, 12, 4, 0, false>(k);  // no whole-task fast path
+      if (var == 40) use_task<16, 4, 12, 4, 0, 0>(k);  // no whole-task fast path
+      if (var == 42) use_task<16, 4, 12, 4, 0, 1>(k);  // unrolled whole-task fast path (r1i)
       if (var == 13) use_moment<32, 128, 2, 2>(k);
       if (var == 20) use_moment<16, 128, 3, 4, 3>(k);
       if (var == 21) use_moment<16, 128, 3, 4, 4>(k);

@@ -624,7 +624,7 @@ constexpr int MOMENT_MAXT = 112;  // task slots per block of moment_task_kernel
 __host__ __device__ constexpr int moment_task_smem_bytes(int NW) {
   return (MOMENT_MAXT * MomLayout::KS + NW * 13 * 33) * 8;
 }
-template <int L, int TC, int NW, int SEEDN = 4, int DBGZ = 0, bool FASTP = true>
+template <int L, int TC, int NW, int SEEDN = 4, int DBGZ = 0, int FASTP = 1>
 __global__ void __launch_bounds__(NW * 32, 1)
     moment_task_kernel(const PassArgs* __restrict__ pa, FitState* __restrict__ st, cudaGraphConditionalHandle cond,
                        int use_cond) {
@@ -863,8 +863,70 @@ __global__ void __launch_bounds__(NW * 32, 1)
       const double rb = D * (2.0 * ga * dxb + gb2 * dy) + ga * D * D;
       const bool ok = qa < 600.0 && qb < 600.0 && fabs(ra) < 300.0 && fabs(rb) < 300.0 &&
                       2.0 * ga * D * D * (TC * L) < 300.0;
-      fast = FASTP && (ncc == TC) && (c0 + TC * CW <= W) && __all_sync(FULL, ok);  // warp-uniform
-      if (fast) {
+      fast = (FASTP != 0) && (ncc == TC) && (c0 + TC * CW <= W) && __all_sync(FULL, ok);  // warp-uniform
+      if (fast && FASTP == 2) {
+        // rolled variant: the TC chunks as a loop (a quarter of the hot code),
+        // t = D k within the chunk, the origin moved per chunk (Taylor shift)
+        org = dxa;
+        E = exp(-qa);
+        Rr = exp(-ra);
+#pragma unroll 1
+        for (int j = 0; j < TC; ++j) {
+          double zc[L];
+#pragma unroll
+          for (int k = 0; k < L; ++k) zc[k] = zn[k];
+          if (j + 1 < TC) {
+            load(row, cc0 + j + 1);
+          } else {
+            next = grab();
+            if (next < nt) {
+              task_pos(next, trow, tcc0, tncc);
+              load(trow, tcc0);
+            }
+          }
+          if (j > 0) {
+            shift(-(double)CW);
+            org += (double)CW;
+          }
+          double cs = 0.0;
+          const double E_in = E, R_in = Rr;
+#pragma unroll
+          for (int k = 0; k < L; ++k) {
+            const double u = E;
+            const double r = fma(A, u, off) - zc[k];  // Eq. 1: r = h - z
+            const double u2 = u * u;
+            const double k1 = D * k, k2 = k1 * k1, k3 = k2 * k1, k4 = k2 * k2;
+            const double ur = u * r;
+            P[0] += u2;
+            Q[0] += u;
+            R[0] += ur;
+            if (k > 0) {
+              P[1] = fma(u2, k1, P[1]);
+              P[2] = fma(u2, k2, P[2]);
+              P[3] = fma(u2, k3, P[3]);
+              P[4] = fma(u2, k4, P[4]);
+              Q[1] = fma(u, k1, Q[1]);
+              Q[2] = fma(u, k2, Q[2]);
+              R[1] = fma(ur, k1, R[1]);
+              R[2] = fma(ur, k2, R[2]);
+            }
+            sr += r;
+            cs = fma(r, r, cs);
+            E *= Rr;
+            Rr *= rho;
+          }
+          srr += cs;
+          if (!isfinite(cs)) {  // rare: replay the chunk's residuals and count the non-finite ones
+            double e = E_in, rr = R_in;
+#pragma unroll
+            for (int k = 0; k < L; ++k) {
+              bad += isfinite(fma(A, e, off) - zc[k]) ? 0 : 1;
+              e *= rr;
+              rr *= rho;
+            }
+          }
+        }
+      } else if (fast) {
         org = dxa;
         E = exp(-qa);
         Rr = exp(-ra);
