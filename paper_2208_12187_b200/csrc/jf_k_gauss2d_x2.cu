@@ -22,13 +22,13 @@ static Kernels make() {
   k.rtpb = PassCfg<ModelGauss2DRotX2, false>::TPB;
   return k;
 }
-template <int L, int TC, int NW>
+template <int L, int TC, int NW, bool ROLLED = false>
 static void use_moment2(Kernels& k) {
   if (k.jwtpb == 0) {  // the dual-number kernel stays in use for weighted passes
     k.jwtpb = k.jtpb;
     k.jwsplit = k.jsplit ? 1 : 0;
   }
-  k.jk = moment2_task_kernel<L, TC, NW>;
+  k.jk = moment2_task_kernel<L, TC, NW, ROLLED>;
   k.jtpb = NW * 32;
   k.jsmem = moment2_task_smem_bytes(NW);
   k.jsplit = false;
@@ -40,6 +40,10 @@ void kernel_attrs_init_x2() {
                        moment2_task_smem_bytes(8));
   cudaFuncSetAttribute((const void*)moment2_task_kernel<8, 4, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        moment2_task_smem_bytes(12));
+  cudaFuncSetAttribute((const void*)moment2_task_kernel<8, 8, 12, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       moment2_task_smem_bytes(12));
+  cudaFuncSetAttribute((const void*)moment2_task_kernel<16, 4, 12, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       moment2_task_smem_bytes(12));
 }
 Kernels kernels_gauss2d_x2(int coord) {
   Kernels k = coord == COORD_EXPLICIT ? make<COORD_EXPLICIT>() : make<COORD_GRID>();
@@ -49,7 +53,9 @@ Kernels kernels_gauss2d_x2(int coord) {
     const int var = v ? atoi(v) : 0;
     if (var == 1) use_moment2<8, 8, 8>(k);
     else if (var == 2) use_moment2<8, 4, 12>(k);
-    else if (var != 9) use_moment2<8, 8, 12>(k);
+    else if (var == 4) use_moment2<16, 4, 12, true>(k);
+    else if (var == 5) use_moment2<8, 8, 12>(k);  // unrolled fast path
+    else if (var != 9) use_moment2<8, 8, 12, true>(k);
   }
   return k;
 }

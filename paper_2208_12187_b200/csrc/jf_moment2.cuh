@@ -118,7 +118,7 @@ __host__ __device__ constexpr int moment2_task_smem_bytes(int NW) {
   return (MOMENT2_MAXT * Mom2::KS + NW * Mom2::NRUN * 33) * 8;
 }
 
-template <int L, int TC, int NW>
+template <int L, int TC, int NW, bool ROLLED = false>
 __global__ void __launch_bounds__(NW * 32, 1)
     moment2_task_kernel(const PassArgs* __restrict__ pa, FitState* __restrict__ st, cudaGraphConditionalHandle cond,
                         int use_cond) {
@@ -288,9 +288,10 @@ __global__ void __launch_bounds__(NW * 32, 1)
     double Xo = (double)(cc0 * CW + lane);
     const int nsub = (ncc + TC - 1) / TC;
     for (int sub = 0; sub < nsub; ++sub) {
-      if (sub > 0) {
-        shift(-(double)(TC * CW));
-        Xo += (double)(TC * CW);
+      if (sub > 0) {  // origin -> the sub-run's first pixel
+        const double Xn = (double)((cc0 + sub * TC) * CW + lane);
+        shift(Xo - Xn);
+        Xo = Xn;
       }
       const int ncs = min(TC, ncc - sub * TC);
       const int ccs = cc0 + sub * TC;
@@ -313,8 +314,12 @@ __global__ void __launch_bounds__(NW * 32, 1)
       if (fast) {
         // TC chunks: two row recurrences, t = D (L j + k) from the sub-run's first pixel
         double E1 = exp(-qa1), S1 = exp(-ra1), E2 = exp(-qa2), S2 = exp(-ra2);
-#pragma unroll
+#pragma unroll(ROLLED ? 1 : TC)
         for (int j = 0; j < TC; ++j) {
+          if (ROLLED && j > 0) {  // rolled: t = D k within the chunk, origin moved per chunk
+            shift(-(double)CW);
+            Xo += (double)CW;
+          }
           double zc[L];
 #pragma unroll
           for (int k = 0; k < L; ++k) zc[k] = zn[k];
@@ -331,7 +336,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
           const double E1i = E1, S1i = S1, E2i = E2, S2i = S2;
 #pragma unroll
           for (int k = 0; k < L; ++k) {
-            point(E1, E2, D * (L * j + k), zc[k], false);
+            point(E1, E2, ROLLED ? D * k : D * (L * j + k), zc[k], false);
             E1 *= S1;
             S1 *= rho1;
             E2 *= S2;
