@@ -3,6 +3,7 @@
 
 #include "jf_kernels.h"
 #include "jf_moment.cuh"
+#include "jf_moment_stream.cuh"
 
 namespace jf {
 template <int C>
@@ -54,7 +55,25 @@ static void attr_moment() {
   cudaFuncSetAttribute((const void*)moment_pass_kernel<L, TPB, MINB, SEEDN, STG>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, moment_smem_bytes(L, TPB, STG));
 }
+template <int L, int NW, int SEEDN>
+static void use_stream(Kernels& k) {
+  if (k.jwtpb == 0) {  // the dual-number kernel stays in use for weighted passes
+    k.jwtpb = k.jtpb;
+    k.jwsplit = k.jsplit ? 1 : 0;
+  }
+  k.jk = moment_stream_kernel<L, NW, SEEDN>;
+  k.jtpb = NW * 32;
+  k.jsmem = moment_stream_smem_bytes(NW);
+}
+template <int L, int NW, int SEEDN>
+static void attr_stream() {
+  cudaFuncSetAttribute((const void*)moment_stream_kernel<L, NW, SEEDN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       moment_stream_smem_bytes(NW));
+}
 void kernel_attrs_init() {
+  attr_stream<16, 12, 8>();
+  attr_stream<16, 16, 8>();
+  attr_stream<8, 16, 8>();
   attr_task<16, 4, 12, 4, 0, 2>();
   attr_task<16, 2, 12>();
   attr_task<16, 4, 16>();
@@ -79,9 +98,12 @@ Kernels kernels_gauss2d(int coord) {
   if (coord == COORD_GRID) {
     // unweighted implicit grid: the moment-form J-pass (jf_moment.cuh),
     // task-scheduled, one block of 12 warps per SM
-    use_task<16, 4, 12, 4, 0, 2>(k);
+    use_stream<16, 12, 8>(k);
     if (const char* v = getenv("JF_JVARIANT")) {  // development aid: alternative shapes
       const int var = atoi(v);
+      if (var == 50) use_task<16, 4, 12, 4, 0, 2>(k);  // r1 task-scheduled kernel
+      if (var == 51) use_stream<16, 16, 8>(k);
+      if (var == 52) use_stream<8, 16, 8>(k);
       if (var == 9) { k.jk = pass_kernel<ModelGauss2DRot, true, COORD_GRID, false>; k.jtpb = 256; k.jsmem = 0; }  // dual numbers
       if (var == 1) use_moment<16, 128, 3>(k);  // static per-warp split (r1d)
       if (var == 11) use_moment<8, 128, 4>(k);

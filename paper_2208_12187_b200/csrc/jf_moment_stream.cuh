@@ -1,0 +1,483 @@
+// jf_moment_stream.cuh — the production J-pass for the rotated 2D Gaussian
+// (n = 7) on an implicit pixel grid, unweighted: the moment form of R34
+// (jf_moment.cuh) with a static, contiguous split of the image over warps.
+//
+// Same output as every other J-pass — the upper triangle of [J | r]^T [J | r]
+// (Eq. 2, Eq. 4, Eq. 5) plus the non-finite count —
+// from the 29 moments of jf_moment.cuh's MomLayout, mapped once per pass.
+//
+// Work split.  The image is a sequence of warp-chunks (32 L consecutive
+// pixels of one row; a row's last chunk may be partial).  Warp w of the grid
+// owns the contiguous chunk range [w nch / nw, (w+1) nch / nw): every warp
+// streams the same number of pixels (to one chunk) with no scheduling work,
+// so the warps of an SM finish together (measured: tools/jpass_probe.cu,
+// profiles/r2_jpass_probe.txt).  Lane l owns pixels l + 32 k of a chunk, so
+// every load of the warp reads 256 contiguous bytes; the next chunk is
+// prefetched into registers (two buffers, the loop unrolled by two chunks:
+// no register copies).
+//
+// Per point (the whole hot loop): u = E from the row recurrence
+// E_{k+1} = E_k R_k, R_{k+1} = R_k rho (2 DMUL), r = A u + off - z (2),
+// u^2, u r (2), the eleven step-index moments (11), sum r, sum r^2 (2):
+// 19 FP64 operations.  Moments run about a moving origin (the lane's first
+// pixel of the current chunk; a Taylor shift per chunk) and are folded with
+// dy^q into the thread's column of a shared-memory table at each row change
+// (reading R34).  A row segment whose exponent range is unsafe for the
+// recurrence (q >= 600 or a step factor beyond e^300 anywhere on it) is
+// evaluated with exp per point instead.
+//
+// Determinism: the chunk -> (warp, lane) map is a function of (m, W, grid),
+// every per-thread sum runs in chunk order, the block partial sums the
+// thread columns in thread order and the grid combine sums the block
+// partials in block order — a pass is bitwise reproducible.
+#pragma once
+
+#include "jf_moment.cuh"
+
+namespace jf {
+
+// Row t of the finish map (R33 + R34 composed): K-vector slot t = (j, k) of
+// [J | r]^T [J | r] in the paper's parameters as a linear combination of the
+// 29 moments (C[t][i], i < NV) and the point count (C[t][NV]).  Column j < 6
+// of J is f_j u psi_j(dx, dy) with psi_j a polynomial of degree <= 2 (6
+// coefficients over the monomials mono(2, p, q)):
+//   j = 0 (A):  f = 1,  psi = 1
+//   j = 1 (x0): f = A,  psi = 2a dx + 2b dy
+//   j = 2 (y0): f = A,  psi = 2b dx + 2 c2 dy
+//   j = 3..5 (sx, sy, th; s = j - 3): f = -A,
+//         psi = T[0][s] dx^2 + T[1][s] dx dy + T[2][s] dy^2   (T = d(a, 2b, c2)/d(sx, sy, th))
+// column 6 (offset) is 1, column 7 is r.  So G_jk = f_j f_k sum u^2 psi_j psi_k
+// (a product of two polynomials: the degree-4 family M2), G_j6 = f_j sum u psi_j
+// (M1), G_j7 = f_j sum u r psi_j (MR), G_66 = m, G_67 = sum r, G_77 = sum r^2.
+// Straight-line code per slot (one thread per slot).
+__device__ __forceinline__ void psi_poly(const PreGauss2D& g, int j, double (&c)[6], double& f) {
+  // monomial order mono(2, p, q): 1, dx, dx^2, dy, dx dy, dy^2
+#pragma unroll
+  for (int i = 0; i < 6; ++i) c[i] = 0.0;
+  if (j == 0) {
+    f = 1.0;
+    c[0] = 1.0;
+  } else if (j == 1) {
+    f = g.A;
+    c[1] = 2.0 * g.a;
+    c[3] = g.b2;
+  } else if (j == 2) {
+    f = g.A;
+    c[1] = g.b2;
+    c[3] = 2.0 * g.c;
+  } else {
+    const int sidx = j - 3;
+    f = -g.A;
+    c[2] = g.T[0 + sidx];
+    c[4] = g.T[3 + sidx];
+    c[5] = g.T[6 + sidx];
+  }
+}
+__device__ __forceinline__ void finish_map_row(const PreGauss2D& g, int t, double* row /* FMAP_COLS */) {
+  constexpr int N = 7;
+  int j = 0, rem = t;
+  while (rem >= N + 1 - j) {
+    rem -= N + 1 - j;
+    ++j;
+  }
+  const int k = j + rem;
+  double out[FMAP_COLS];
+#pragma unroll
+  for (int i = 0; i < FMAP_COLS; ++i) out[i] = 0.0;
+  constexpr int MP[6] = {0, 1, 2, 0, 1, 0}, MQ[6] = {0, 0, 0, 1, 1, 2};  // (p, q) of mono(2, ., .)
+  if (k < 6) {
+    double cj[6], ck[6], fj, fk;
+    psi_poly(g, j, cj, fj);
+    psi_poly(g, k, ck, fk);
+    const double f = fj * fk;
+#pragma unroll
+    for (int x = 0; x < 6; ++x)
+#pragma unroll
+      for (int y = 0; y < 6; ++y) {
+        const int idx = MomLayout::O2 + mono(4, MP[x] + MP[y], MQ[x] + MQ[y]);
+        out[idx] = fma(cj[x], ck[y], out[idx]);
+      }
+#pragma unroll
+    for (int i = 0; i < MomLayout::N2; ++i) out[MomLayout::O2 + i] *= f;
+  } else if (j < 6) {
+    double cj[6], fj;
+    psi_poly(g, j, cj, fj);
+    const int base = (k == 6) ? MomLayout::O1 : MomLayout::OR;
+#pragma unroll
+    for (int x = 0; x < 6; ++x) out[base + x] = fj * cj[x];
+  } else if (j == 6) {
+    out[k == 6 ? MomLayout::NV : MomLayout::OSR] = 1.0;
+  } else {
+    out[MomLayout::OSRR] = 1.0;
+  }
+#pragma unroll
+  for (int i = 0; i < FMAP_COLS; ++i) row[i] = out[i];
+}
+
+// dynamic shared memory: the per-thread folded-moment table [KS][TPB + 1]
+__host__ __device__ constexpr int moment_stream_smem_bytes(int NW) {
+  return MomLayout::KS * (NW * 32 + 1) * 8;
+}
+
+template <int L, int NW, int SEEDN>
+__global__ void __launch_bounds__(NW * 32, 1)
+    moment_stream_kernel(const PassArgs* __restrict__ pa, FitState* __restrict__ st, cudaGraphConditionalHandle cond,
+                         int use_cond) {
+  using Model = ModelGauss2DRot;
+  constexpr int N = Model::N, KT = tri_count(N), KS2 = KT + 1;
+  constexpr int TPB = NW * 32;
+  constexpr int KS = MomLayout::KS, NV = MomLayout::NV, NF = MomLayout::OSR;
+  constexpr int CW = 32 * L;
+  constexpr double D = 32.0;
+  const PassArgs& a = *pa;
+  if (!pass_begin<true, false>(a, st)) return;
+  const double* xs = (a.epilogue == EPI_FIT) ? st->x_eval : a.x;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  // development aid (JF_DEBUG_STAMPS): per-warp globaltimer stamps
+  auto stamp = [&](int slot) {
+    if (a.dbg && lane == 0 && blockIdx.x * NW + wid < 8000) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.dbg[(blockIdx.x * NW + wid) * 8 + slot] = t;
+      if (slot == 1) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        a.dbg[(blockIdx.x * NW + wid) * 8] = smid;
+      }
+    }
+  };
+  stamp(1);
+
+  extern __shared__ __align__(16) double dyn_stream[];  // [KS][TPB + 1]
+  auto col = [&](int i) -> double& { return dyn_stream[i * (TPB + 1) + tid]; };
+  __shared__ PreGauss2D spre;  // the pass's parameters incl. the chain-rule block (last block only)
+  __shared__ double red[NW][KS];
+  __shared__ double vec[KMAX];
+  __shared__ double scratch[combine_scratch(TPB)];
+  __shared__ double mom[KS];
+
+  double A, off, ga, gb2, gc, x0, y0;
+  {
+    double xv[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) xv[j] = xs[j];
+    const auto pre = Model::template prologue<true>(xv);
+    A = pre.g.A, off = pre.off, ga = pre.g.a, gb2 = pre.g.b2, gc = pre.g.c, x0 = pre.g.x0, y0 = pre.g.y0;
+    if (tid == 0) spre = pre.g;
+  }
+#pragma unroll
+  for (int i = 0; i < NF; ++i) col(i) = 0.0;
+  stamp(2);
+
+  const int W = (int)a.W;
+  const int64_t H = a.m / a.W;
+  const int64_t row0 = a.row0;
+  const int cpr = (W + CW - 1) / CW;
+  const int64_t nch = H * (int64_t)cpr;
+  const int64_t nw = (int64_t)gridDim.x * NW;
+  const int64_t gw = (int64_t)blockIdx.x * NW + wid;
+  const int64_t c_begin = gw * nch / nw, c_end = (gw + 1) * nch / nw;
+  const double rho = exp(-2.0 * ga * D * D);
+  const double* __restrict__ z = a.z;
+
+  double P[5], Q[3], R[3];
+#pragma unroll
+  for (int i = 0; i < 5; ++i) P[i] = 0.0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) Q[i] = R[i] = 0.0;
+  double sr = 0.0, srr = 0.0;
+  int bad = 0;
+
+  // moments about o -> about o - d (Pascal scheme)
+  auto shift = [&](double d) {
+#pragma unroll
+    for (int j = 1; j <= 4; ++j)
+#pragma unroll
+      for (int p = 4; p >= j; --p) P[p] = fma(d, P[p - 1], P[p]);
+#pragma unroll
+    for (int j = 1; j <= 2; ++j)
+#pragma unroll
+      for (int p = 2; p >= j; --p) {
+        Q[p] = fma(d, Q[p - 1], Q[p]);
+        R[p] = fma(d, R[p - 1], R[p]);
+      }
+  };
+  double org = 0.0;  // dx of the origin of the running row moments
+  // row moments (about dx = org) -> about dx = 0, times dy^q, into the thread's column
+  auto fold = [&](double dy) {
+    shift(org);
+    double dq[5];
+    dq[0] = 1.0;
+    dq[1] = dy;
+    dq[2] = dy * dy;
+    dq[3] = dq[2] * dy;
+    dq[4] = dq[2] * dq[2];
+#pragma unroll
+    for (int q = 0; q <= 4; ++q)
+#pragma unroll
+      for (int p = 0; p + q <= 4; ++p) {
+        double& m2 = col(MomLayout::O2 + mono(4, p, q));
+        m2 = fma(P[p], dq[q], m2);
+      }
+#pragma unroll
+    for (int q = 0; q <= 2; ++q)
+#pragma unroll
+      for (int p = 0; p + q <= 2; ++p) {
+        double& m1 = col(MomLayout::O1 + mono(2, p, q));
+        m1 = fma(Q[p], dq[q], m1);
+        double& mr = col(MomLayout::OR + mono(2, p, q));
+        mr = fma(R[p], dq[q], mr);
+      }
+#pragma unroll
+    for (int i = 0; i < 5; ++i) P[i] = 0.0;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) Q[i] = R[i] = 0.0;
+  };
+
+  // position of the chunk being processed (advanced incrementally)
+  int64_t row = c_begin / cpr;
+  int cc = (int)(c_begin - row * cpr) - 1;
+  int64_t cur_row = -1;
+  double dy = 0.0;
+  bool row_fast = false;   // the warp's chunks of this row are safe for the recurrence
+  bool carried = false;    // E, Rr continue from the previous chunk
+  int since_seed = 0;
+  double E = 0.0, Rr = 0.0;
+
+  // Load the next chunk in order (lane's points) into zz; a partial (row-end)
+  // chunk is predicated.  (lrow, lcc): position of the next chunk to load,
+  // advanced incrementally (no 64-bit division per chunk).
+  int64_t lrow = row;
+  int lcc = cc + 1;
+  auto load = [&](double (&zz)[L]) {
+    const int c0l = lcc * CW;
+    const double* zp = z + lrow * (int64_t)W + c0l + lane;
+    if (c0l + CW <= W) {  // warp-uniform
+#pragma unroll
+      for (int k = 0; k < L; ++k) zz[k] = __ldcs(zp + 32 * k);
+    } else {
+#pragma unroll
+      for (int k = 0; k < L; ++k) zz[k] = (c0l + lane + 32 * k < W) ? __ldcs(zp + 32 * k) : 0.0;
+    }
+    if (++lcc == cpr) {
+      lcc = 0;
+      ++lrow;
+    }
+  };
+
+  // One chunk: zc holds its points.
+  auto process = [&](const double (&zc)[L]) {
+    if (++cc == cpr) {
+      cc = 0;
+      ++row;
+    }
+    if (row != cur_row) {  // warp-uniform: fold the previous row, set up this one
+      if (cur_row >= 0) fold(dy);
+      cur_row = row;
+      dy = (double)(row + row0) - y0;
+      // the warp's chunks of this row: [cc, last]; q is convex and argR linear
+      // along the row, so the range ends bound them
+      const int64_t last_ch = min(c_end - 1, (row + 1) * (int64_t)cpr - 1);
+      const int cl = (int)(last_ch - row * cpr);
+      const double dxa = (double)(cc * CW + lane) - x0;
+      const double dxb = (double)(cl * CW + lane + 32 * (L - 1)) - x0;
+      const double qa = dxa * (ga * dxa + gb2 * dy) + gc * (dy * dy);
+      const double qb = dxb * (ga * dxb + gb2 * dy) + gc * (dy * dy);
+      const double ra = D * (2.0 * ga * dxa + gb2 * dy) + ga * D * D;
+      const double rb = D * (2.0 * ga * dxb + gb2 * dy) + ga * D * D;
+      const bool ok = qa < 600.0 && qb < 600.0 && fabs(ra) < 300.0 && fabs(rb) < 300.0 &&
+                      2.0 * ga * D * D * L * SEEDN < 300.0;
+      row_fast = __all_sync(FULL, ok);
+      carried = false;
+    }
+    const int c0 = cc * CW;
+    const double dx0 = (double)(c0 + lane) - x0;
+    shift(-(double)CW);  // origin -> this chunk's first pixel (zero moments at a row start)
+    org = dx0;
+    if (row_fast && c0 + CW <= W) {  // warp-uniform
+      if (!carried || ++since_seed >= SEEDN) {
+        const double q0 = dx0 * (ga * dx0 + gb2 * dy) + gc * (dy * dy);
+        const double argR = D * (2.0 * ga * dx0 + gb2 * dy) + ga * D * D;
+        E = exp(-q0);
+        Rr = exp(-argR);
+        since_seed = 0;
+        carried = true;
+      }
+      double cs = 0.0;
+      const double E_in = E, R_in = Rr;
+#pragma unroll
+      for (int k = 0; k < L; ++k) {
+        const double u = E;
+        const double r = fma(A, u, off) - zc[k];  // Eq. 1: r = h - z
+        const double u2 = u * u;
+        const double k1 = D * k, k2 = k1 * k1, k3 = k2 * k1, k4 = k2 * k2;
+        const double ur = u * r;
+        P[0] += u2;
+        Q[0] += u;
+        R[0] += ur;
+        if (k > 0) {
+          P[1] = fma(u2, k1, P[1]);
+          P[2] = fma(u2, k2, P[2]);
+          P[3] = fma(u2, k3, P[3]);
+          P[4] = fma(u2, k4, P[4]);
+          Q[1] = fma(u, k1, Q[1]);
+          Q[2] = fma(u, k2, Q[2]);
+          R[1] = fma(ur, k1, R[1]);
+          R[2] = fma(ur, k2, R[2]);
+        }
+        sr += r;
+        cs = fma(r, r, cs);
+        E *= Rr;
+        Rr *= rho;
+      }
+      srr += cs;
+      if (!isfinite(cs)) {  // rare: replay the chunk's residuals and count the non-finite ones
+        double e = E_in, rr = R_in;
+#pragma unroll
+        for (int k = 0; k < L; ++k) {
+          bad += isfinite(fma(A, e, off) - zc[k]) ? 0 : 1;
+          e *= rr;
+          rr *= rho;
+        }
+      }
+    } else {
+      // row end or an unsafe exponent range: exp per point
+      carried = false;
+#pragma unroll
+      for (int k = 0; k < L; ++k) {
+        if (c0 + lane + 32 * k < W) {
+          const double dx = dx0 + D * k;
+          const double u = exp(-(dx * (ga * dx + gb2 * dy) + gc * (dy * dy)));
+          const double r = fma(A, u, off) - zc[k];
+          bad += isfinite(r) ? 0 : 1;
+          const double u2 = u * u, t = D * k, t2 = t * t, ur = u * r;
+          P[0] += u2;
+          P[1] = fma(u2, t, P[1]);
+          P[2] = fma(u2, t2, P[2]);
+          P[3] = fma(u2, t2 * t, P[3]);
+          P[4] = fma(u2, t2 * t2, P[4]);
+          Q[0] += u;
+          Q[1] = fma(u, t, Q[1]);
+          Q[2] = fma(u, t2, Q[2]);
+          R[0] += ur;
+          R[1] = fma(ur, t, R[1]);
+          R[2] = fma(ur, t2, R[2]);
+          sr += r;
+          srr = fma(r, r, srr);
+        }
+      }
+    }
+  };
+
+  {
+    double za[L], zb[L];
+    if (c_begin < c_end) load(za);
+    for (int64_t ch = c_begin; ch < c_end; ch += 2) {
+      if (ch + 1 < c_end) load(zb);
+      process(za);
+      if (ch + 1 < c_end) {
+        if (ch + 2 < c_end) load(za);
+        process(zb);
+      }
+    }
+  }
+  if (cur_row >= 0) fold(dy);
+  stamp(3);
+  col(MomLayout::OSR) = sr;
+  col(MomLayout::OSRR) = srr;
+  col(NV) = (double)bad;
+  __syncthreads();
+
+  // ---- block partial: the thread columns summed in thread order (NW segments of 32)
+  static_assert(NW * KS <= TPB, "one (entry, segment) per thread");
+  if (tid < NW * KS) {
+    const int i = tid % KS, seg = tid / KS;
+    const double* c = dyn_stream + i * (TPB + 1) + seg * 32;
+    double s4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int j = 0; j < 32; ++j) s4[j & 3] += c[j];
+    red[seg][i] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+  }
+  __syncthreads();
+  if (tid < KS) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) s += red[w][tid];
+    // keep the partial in L2 for the last block (the image streams through evict-first)
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a.partials + (size_t)blockIdx.x * KS + tid),
+                 "d"(s), "l"(pol)
+                 : "memory");
+  }
+  stamp(4);
+  // ---- grid combine: the last block sums the block partials in block order
+  // (one L2 batch) while it builds the finish map, then maps once
+  __shared__ unsigned int tflag;
+  const int nblk = gridDim.x;
+  __syncthreads();
+  if (tid == 0) {
+    unsigned prev;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(prev) : "l"(a.ticket) : "memory");
+    tflag = (prev == (unsigned)(nblk - 1)) ? 1u : 0u;
+  }
+  __syncthreads();
+  if (!tflag) return;
+  dbg_tail(a, 1);
+  constexpr int NSEG = TPB / KS;
+  double v[16];
+  const int rk = tid % KS, rseg = tid / KS;
+  double s = 0.0;
+  if (tid < NSEG * KS) {  // first batch of loads in flight while the map is built
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int r = rseg + i * NSEG;
+      v[i] = (r < nblk) ? __ldcg(a.partials + (size_t)r * KS + rk) : 0.0;
+    }
+  }
+  double (*fmap)[FMAP_COLS] = reinterpret_cast<double (*)[FMAP_COLS]>(dyn_stream);  // the column table is free now
+  if (tid < KT) finish_map_row(spre, tid, fmap[tid]);
+  if (tid < NSEG * KS) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) s += v[i];
+    for (int r0 = rseg + 16 * NSEG; r0 < nblk; r0 += 16 * NSEG) {  // grids beyond 16 NSEG blocks
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int r = r0 + i * NSEG;
+        v[i] = (r < nblk) ? __ldcg(a.partials + (size_t)r * KS + rk) : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) s += v[i];
+    }
+    scratch[rseg * KS + rk] = s;
+  }
+  if (tid == 0) a.ticket[0] = 0u;
+  __syncthreads();
+  dbg_tail(a, 2);
+  if (tid < KS) {
+    double t = 0.0;
+#pragma unroll
+    for (int seg = 0; seg < NSEG; ++seg) t += scratch[seg * KS + tid];
+    mom[tid] = t;
+  }
+  __syncthreads();
+  if (tid < KT) {
+    double w = fmap[tid][NV] * (double)a.m;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) w = fma(fmap[tid][i], mom[i], w);
+    vec[tid] = w;
+  } else if (tid == KT) {
+    vec[KT] = mom[NV];  // non-finite count
+  }
+  __syncthreads();
+  dbg_tail(a, 5);
+  if (a.no_chain) {  // debug: the K-vector in the alt coordinates (first stage of R33 only)
+    moments_to_kvec(spre, (double)a.m, mom, vec);
+    __syncthreads();
+  }
+  dbg_tail(a, 6);
+  pass_tail<KS2, TPB, true>(a, st, vec, cond, use_cond);
+  dbg_tail(a, 7);
+}
+
+}  // namespace jf
