@@ -182,6 +182,16 @@ def make_gauss2d(W: int, seed: int = 3, k: int = 0, noise: float = 0.1, H: int |
     return Problem("gauss2d_rot", z, truth, p0, grid=(W, H, 0), name=f"gauss2d W={W}")
 
 
+def make_gauss2d_at(W: int, H: int, truth, seed: int = 30, noise: float = 0.1) -> Problem:
+    """A rotated 2D Gaussian + offset with GIVEN parameters (edge cases of the
+    pass: narrow, elongated, off-centre or off-image peaks); p0 = truth."""
+    rng = np.random.default_rng([seed, 0])
+    truth = np.asarray(truth, dtype=np.float64)
+    X, Y = grid_coords(W, H)
+    z = render("gauss2d_rot", (X, Y), truth) + noise * rng.standard_normal(W * H)
+    return Problem("gauss2d_rot", z, truth, truth.copy(), grid=(W, H, 0), name=f"gauss2d_at W={W} H={H}")
+
+
 def make_gauss2d_bounded(W: int, variant: str = "a", seed: int = 4, k: int = 0, noise: float = 0.1) -> Problem:
     """C4: as C3 with bounds.  a: loose; b: lb_off = off+0.2, ub_sx = 0.85 sx;
     c: as b with ub_sx = 0.6 sx.  p0 clipped to [lb+1e-3, ub-1e-3]."""

@@ -11,10 +11,14 @@
  * box bounds lb <= x <= ub (Coleman-Li reflective scaling, "SciPy's
  * adapted version"; reading R19).  h is one of a fixed set of built-in models
  * (jf_model).  Every per-iteration pass over the m data points runs in
- * hand-written sm_100a CUDA kernels: the model value, its Jacobian row by
- * forward-mode dual numbers, and a fused fp64 block reduction to
+ * hand-written sm_100a CUDA kernels and reduces, in fp64, to
  *     cost = 1/2 r^T r (Eq. 2),  g = J^T r (Eq. 4),  G = J^T J (Eq. 5, Gauss-Newton B),
- * never materialising J.  The n x n trust-region subproblem (Eq. 9-14,
+ * never materialising J.  The Jacobian is forward-mode: by dual
+ * numbers carrying the whole row for the 1-D models, explicit coordinates and
+ * weighted fits; for the rotated 2-D Gaussians on an implicit pixel grid
+ * (unweighted) by the moment form (readings R33-R35): the same
+ * partials regrouped as fixed linear combinations of per-pass moments of
+ * exp(-q) along image rows, mapped to (cost, g, G) once per pass.  The n x n trust-region subproblem (Eq. 9-14,
  * Alg. 2) runs in a single-warp device kernel; the iteration (Alg. 1, 3) is a
  * device state machine driven by a CUDA graph with a conditional WHILE node.
  *
@@ -86,7 +90,8 @@ typedef enum { JF_XSCALE_JAC = 0, JF_XSCALE_ONES = 1, JF_XSCALE_ARRAY = 2 } jf_x
  *  TSQR: R factor of W = [J | r] by CholeskyQR2 (a Gram pass, then a pass
  *        accumulating (W R1^-1)^T (W R1^-1); R = chol(.) R1), SVD of the scaled
  *        R by one-sided Jacobi (two passes per accepted step)
- *  AUTO: TSQR if cond(J D^-1)^2 estimated at x0 exceeds 1e6, else GRAM */
+ *  AUTO: TSQR if cond(J D^-1)^2 estimated at x0 — or at an accepted step —
+ *        exceeds 1e6, else GRAM (the default) */
 typedef enum { JF_SOLVE_AUTO = 0, JF_SOLVE_GRAM = 1, JF_SOLVE_TSQR = 2 } jf_solver;
 
 /* Which pass evaluates a trial point x + w (Eq. 15 needs f(x+w)):
@@ -115,7 +120,7 @@ typedef struct jf_opts {
   int32_t max_nfev;             /* 0 -> 100*n (R16)                                            */
   int32_t x_scale_mode;         /* jf_xscale, default JF_XSCALE_JAC                           */
   const double* x_scale;        /* host, n entries, used iff x_scale_mode == JF_XSCALE_ARRAY  */
-  int32_t solver;               /* jf_solver, default JF_SOLVE_GRAM (jf_pass: always the Gram) */
+  int32_t solver;               /* jf_solver, default JF_SOLVE_AUTO (jf_pass: always the Gram) */
   int32_t policy;               /* jf_policy, default JF_POLICY_SPECULATIVE                   */
   int64_t grid_w, grid_h;       /* implicit pixel grid for 2-D models when y == NULL          */
   int64_t grid_row0;            /* global row of this shard's first row (sharded images)      */
@@ -131,8 +136,22 @@ typedef struct jf_opts {
                                    0: host-driven loop (one kernel launch + flag read per trial) */
   int32_t trace_cap;            /* > 0: record up to trace_cap trials into trace[]             */
   double* trace;                /* host, trace_cap * JF_TRACE_FIELDS doubles, caller-owned     */
-  int64_t m_global;             /* sharded fits: total m over ranks (0 -> computed by the comm) */
+  int64_t m_global;             /* sharded fits: total m over ranks (0 -> summed over the ranks
+                                   by one combine through the comm at the start of the fit)      */
+  int64_t capacity;             /* > 0: size every pass and the fit's CUDA graph for `capacity`
+                                   points (>= m).  One cached graph then serves every m <=
+                                   capacity; m itself is read from device memory at run time
+                                   and points i >= m are never read (the masking of P:283-311
+                                   App. A without dummy data; reading R26).  0: sized for m   */
+  int32_t flags;                /* JF_FLAG_*, default 0                                         */
+  int32_t pad_opts_;
 } jf_opts;
+
+/* jf_opts.flags */
+#define JF_FLAG_BATCH_SHARED_Y 2  /* jf_curve_fit_batch: y holds ONE set of coordinates for all fits */
+#define JF_FLAG_ALT_COORDS 1  /* passes of the rotated Gaussians return W^T W in the alternative
+                                 coordinates (a, 2b, c2) of their quadratic form — the first
+                                 stage of the two-stage chain rule (reading R33) — for tests */
 
 /* One trace record per trial (Alg. 1-3 quantities), in this order:
  *  nit, nfev, njev, cost, cost_new, Delta, alpha, ratio, ||p_h||, ||step||, pred, branch
@@ -152,7 +171,7 @@ typedef struct jf_result {
   int32_t n, trace_len;
   int8_t active_mask[JF_MAX_N]; /* -1 lower, +1 upper, 0 free (bounded fits; R19)              */
   int32_t kernel_launches;      /* device kernels this call launched                          */
-  int32_t pad_;
+  int32_t graph_reused;         /* 1: the fit replayed an already-instantiated CUDA graph      */
   double t_upload_s, t_solve_s; /* host wall time of the H2D copies and of the solve           */
   double t_epilogue_s;          /* device time in the single-warp solver epilogues (globaltimer) */
   double epilogue_cycles[8];    /* SM cycles in: eigensolver, trial solve, Coleman-Li step
@@ -186,6 +205,33 @@ int32_t jf_model_kslots(int32_t model);
 int32_t jf_curve_fit(int32_t model, const double* y, const double* z, int64_t m,
                      const double* p0, int32_t n, const double* lb, const double* ub,
                      const jf_opts* opts, jf_result* out);
+
+/* jf_curve_fit_batch — many independent small fits in ONE kernel launch
+ * (Gpufit's regime, "slightly faster ... for small data
+ * lengths", "runs entirely in CUDA"): fit k minimises
+ * 1/2 sum_i (h(y_k,i; x) - z_k,i)^2 by the same TRF as
+ * jf_curve_fit, each fit on one warp (pass, subproblem and control), all
+ * fits of the batch in one persistent launch.
+ *  z: nfits * m doubles, fit k at z + k*m.  y: NULL (implicit grid / t from
+ *      opts, the same for every fit), or coordinates per fit (fit k at
+ *      y + k*d*m, layout as jf_curve_fit), or — with JF_FLAG_BATCH_SHARED_Y —
+ *      one set of d*m coordinates shared by all fits.  opts->sigma (optional):
+ *      nfits * m, like z.  Device pointers iff opts->inputs_on_device.
+ *  p0: host, nfits * n, or NULL (curve_fit's default p0 for every fit).
+ *  lb, ub: n each, shared by all fits, or NULL.
+ *  out: host, nfits records, written for every fit: status >= 0 the solver
+ *      status, < 0 that fit's error (JF_EINFEASIBLE p0 outside the bounds,
+ *      JF_ENONFINITE residuals not finite at p0, JF_EINVAL p0 not finite).
+ *  The speculative policy; opts->comm, capacity and trace are not used.
+ * Returns 0 (every fit ran; see out[k].status) or a JF_E* error.  Blocks.  */
+typedef struct jf_batch_result {
+  double x[JF_MAX_N];
+  double cost, optimality;
+  int32_t status, nfev, njev, nit;
+} jf_batch_result;
+int32_t jf_curve_fit_batch(int32_t model, const double* y, const double* z, int64_t m, int64_t nfits,
+                           const double* p0, int32_t n, const double* lb, const double* ub,
+                           const jf_opts* opts, jf_batch_result* out);
 
 /* jf_pass — one J-pass at x (Eq. 1, 2, 4, 5): cost = 1/2 r^T r,
  * grad[n] = J^T r, gram[n*n] = J^T J (row-major, symmetric), *nonfinite =
@@ -221,6 +267,19 @@ int32_t jf_trust_region_step(const double* hatG, const double* hatg, int32_t n, 
                              double Delta, double alpha_in, const jf_opts* opts,
                              double* p, double* alpha_out, int32_t* n_iter);
 
+/* jf_select_step — the device Coleman-Li step selection alone, for parity
+ * tests (reading R19/R20; "SciPy's adapted version"): given the scaled
+ * quadratic model B_hat (n*n row-major, incl. diag_h on the diagonal) and
+ * g_hat, the current x, bounds lb/ub (finite or +-INFINITY), the scaling d and
+ * the hat-space trust-region step p_h (n each, host), the radius Delta and
+ * theta, writes the chosen step (original space, n), step_h (hat space, n;
+ * may be NULL), the predicted reduction -Q(step_h) and the branch (0
+ * interior, 1 reflected, 2 truncated, 3 scaled gradient).  Blocks.         */
+int32_t jf_select_step(const double* hatB, const double* hatg, const double* x, const double* lb,
+                       const double* ub, const double* d, const double* p_h, int32_t n, double Delta,
+                       double theta, const jf_opts* opts, double* step, double* step_h, double* pred,
+                       int32_t* branch);
+
 /* Multi-GPU: data-parallel sharding over m (one process per GPU).  Each rank
  * owns a mailbox in its device memory; jf_comm_export() writes an IPC handle
  * for it, the caller all-gathers the handles (e.g. with torch.distributed),
@@ -235,6 +294,19 @@ int32_t jf_comm_export(const jf_comm* comm, uint8_t handle[JF_COMM_HANDLE_BYTES]
 int32_t jf_comm_connect(jf_comm* comm, const uint8_t* all_handles /* nranks * JF_COMM_HANDLE_BYTES */);
 int32_t jf_comm_create_local(int32_t nranks, int32_t device, jf_comm** comms /* nranks out */);
 int32_t jf_comm_destroy(jf_comm* comm);
+/* A pass kernel whose peers do not all arrive within timeout_ms reports
+ * JF_ECOMM (jf_pass*) or ends the fit with status JF_ECOMM instead of
+ * waiting forever.  Default 20000 ms.  Returns 0 or JF_EINVAL.              */
+int32_t jf_comm_set_timeout(jf_comm* comm, int32_t timeout_ms);
+/* One cross-rank combine of a KMAX-double vector through the mailboxes (the
+ * exchange every pass kernel ends with), timed on the device: *us receives
+ * the mean microseconds per combine over `reps` back-to-back combines of
+ * value v; *sum receives the rank-ordered sum of v over the ranks.  All
+ * ranks must call it together.  For latency measurements.  */
+int32_t jf_comm_bench(jf_comm* comm, double v, int32_t reps, double* sum, double* us);
+
+/* Drop every instantiated fit graph of `device` (the next fit builds afresh). */
+int32_t jf_graph_cache_clear(int32_t device);
 
 /* Human-readable name of a return code (static storage). */
 const char* jf_strerror(int32_t code);

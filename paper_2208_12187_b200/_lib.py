@@ -39,7 +39,17 @@ class jf_opts(C.Structure):
         ("use_graph", C.c_int32), ("trace_cap", C.c_int32),
         ("trace", C.POINTER(C.c_double)),
         ("m_global", C.c_int64),
+        ("capacity", C.c_int64), ("flags", C.c_int32), ("pad_opts_", C.c_int32),
     ]
+
+
+FLAG_ALT_COORDS = 1
+FLAG_BATCH_SHARED_Y = 2
+
+
+class jf_batch_result(C.Structure):
+    _fields_ = [("x", C.c_double * JF_MAX_N), ("cost", C.c_double), ("optimality", C.c_double),
+                ("status", C.c_int32), ("nfev", C.c_int32), ("njev", C.c_int32), ("nit", C.c_int32)]
 
 
 class jf_result(C.Structure):
@@ -50,7 +60,7 @@ class jf_result(C.Structure):
         ("status", C.c_int32), ("nfev", C.c_int32), ("njev", C.c_int32), ("nit", C.c_int32),
         ("n", C.c_int32), ("trace_len", C.c_int32),
         ("active_mask", C.c_int8 * JF_MAX_N),
-        ("kernel_launches", C.c_int32), ("pad_", C.c_int32),
+        ("kernel_launches", C.c_int32), ("graph_reused", C.c_int32),
         ("t_upload_s", C.c_double), ("t_solve_s", C.c_double),
         ("t_epilogue_s", C.c_double), ("epilogue_cycles", C.c_double * 8),
         ("timeline_len", C.c_int32), ("pad2_", C.c_int32), ("timeline_ns", C.c_double * 64),
@@ -80,6 +90,9 @@ def load() -> C.CDLL:
     lib.jf_curve_fit.argtypes = [C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.c_void_p,
                                  C.c_void_p, C.POINTER(jf_opts), C.POINTER(jf_result)]
     lib.jf_curve_fit.restype = C.c_int32
+    lib.jf_curve_fit_batch.argtypes = [C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p,
+                                       C.c_int32, C.c_void_p, C.c_void_p, C.POINTER(jf_opts), C.c_void_p]
+    lib.jf_curve_fit_batch.restype = C.c_int32
     lib.jf_pass.argtypes = [C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, dp, C.c_int32,
                             C.POINTER(jf_opts), dp, dp, dp, ip]
     lib.jf_pass.restype = C.c_int32
@@ -92,6 +105,9 @@ def load() -> C.CDLL:
     lib.jf_trust_region_step.argtypes = [dp, dp, C.c_int32, C.c_int64, C.c_double, C.c_double,
                                          C.POINTER(jf_opts), dp, dp, ip]
     lib.jf_trust_region_step.restype = C.c_int32
+    lib.jf_select_step.argtypes = [dp, dp, dp, dp, dp, dp, dp, C.c_int32, C.c_double, C.c_double,
+                                   C.POINTER(jf_opts), dp, dp, dp, ip]
+    lib.jf_select_step.restype = C.c_int32
     lib.jf_comm_create.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]
     lib.jf_comm_create.restype = C.c_int32
     lib.jf_comm_export.argtypes = [C.c_void_p, C.c_char_p]
@@ -102,6 +118,12 @@ def load() -> C.CDLL:
     lib.jf_comm_create_local.restype = C.c_int32
     lib.jf_comm_destroy.argtypes = [C.c_void_p]
     lib.jf_comm_destroy.restype = C.c_int32
+    lib.jf_comm_set_timeout.argtypes = [C.c_void_p, C.c_int32]
+    lib.jf_comm_set_timeout.restype = C.c_int32
+    lib.jf_comm_bench.argtypes = [C.c_void_p, C.c_double, C.c_int32, dp, dp]
+    lib.jf_comm_bench.restype = C.c_int32
+    lib.jf_graph_cache_clear.argtypes = [C.c_int32]
+    lib.jf_graph_cache_clear.restype = C.c_int32
     lib.jf_strerror.argtypes = [C.c_int32]
     lib.jf_strerror.restype = C.c_char_p
     lib.jf_version.argtypes = []
@@ -111,6 +133,8 @@ def load() -> C.CDLL:
 
 
 EXPORTED = ["jf_opts_default", "jf_model_nparams", "jf_model_ydim", "jf_model_kslots", "jf_curve_fit",
-            "jf_pass", "jf_residual_pass", "jf_pass_device", "jf_trust_region_step", "jf_comm_create",
+            "jf_curve_fit_batch",
+            "jf_pass", "jf_residual_pass", "jf_pass_device", "jf_trust_region_step", "jf_select_step",
+            "jf_comm_create",
             "jf_comm_export", "jf_comm_connect", "jf_comm_create_local", "jf_comm_destroy",
-            "jf_strerror", "jf_version"]
+            "jf_comm_set_timeout", "jf_comm_bench", "jf_graph_cache_clear", "jf_strerror", "jf_version"]

@@ -50,6 +50,16 @@ def _as_host(a) -> np.ndarray:
 class _Data:
     """Holds the (y, z, sigma) buffers alive and resolves their pointers."""
 
+    def keep_alive(self, stream_ptr):
+        """Tell torch's caching allocator that converted copies are in use on
+        the library's stream until the work enqueued there completes."""
+        if not self.on_device or not self._tmp:
+            return
+        import torch
+        s = torch.cuda.ExternalStream(stream_ptr) if stream_ptr else torch.cuda.current_stream()
+        for t in self._tmp:
+            t.record_stream(s)
+
     def __init__(self, y, z, sigma):
         self.on_device = _is_cuda(z)
         if self.on_device:
@@ -64,6 +74,8 @@ class _Data:
             self.yp = None if self.y is None else self.y.data_ptr()
             self.sp = None if self.sigma is None else self.sigma.data_ptr()
             self.m = int(self.z.numel())
+            self._tmp = [t for t, u in ((self.z, z), (self.y, y), (self.sigma, sigma))
+                         if t is not None and t.data_ptr() != u.data_ptr()]
         else:
             self.z = _as_host(z)
             self.y = None if y is None else _as_host(y)
@@ -74,9 +86,19 @@ class _Data:
             self.m = int(self.z.size)
 
 
+def _default_stream(on_device, stream):
+    """CUDA inputs: run on torch's current stream unless told otherwise, so
+    the library's work is ordered after the work that produced the inputs."""
+    if stream is None and on_device:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return stream
+
+
 def make_opts(*, grid=None, t0=0.0, dt=1.0, index0=0, sigma_ptr=None, on_device=False, device=0,
               stream=None, ftol=1e-8, xtol=1e-8, gtol=1e-8, max_nfev=0, x_scale="jac",
-              policy="speculative", use_graph=True, comm=None, m_global=0, solver="gram"):
+              policy="speculative", use_graph=True, comm=None, m_global=0, solver="auto", capacity=0,
+              alt_coords=False):
     lib = L.load()
     o = L.jf_opts()
     lib.jf_opts_default(C.byref(o))
@@ -99,6 +121,9 @@ def make_opts(*, grid=None, t0=0.0, dt=1.0, index0=0, sigma_ptr=None, on_device=
     o.sigma = sigma_ptr
     o.device = int(device)
     o.inputs_on_device = 1 if on_device else 0
+    o.capacity = int(capacity)
+    o.flags = L.FLAG_ALT_COORDS if alt_coords else 0
+    stream = _default_stream(on_device, stream)
     if stream is not None:
         o.stream = stream if isinstance(stream, int) else int(getattr(stream, "cuda_stream", stream))
     o.use_graph = 1 if use_graph else 0
@@ -122,6 +147,7 @@ class FitResult:
     nit: int
     active_mask: np.ndarray
     kernel_launches: int
+    graph_reused: int
     t_upload_s: float
     t_solve_s: float
     t_epilogue_s: float
@@ -160,12 +186,51 @@ def curve_fit(model, z, y=None, *, grid=None, p0=None, lb=None, ub=None, sigma=N
         gram=arr(res.gram, n * n).reshape(n, n), pcov=arr(res.pcov, n * n).reshape(n, n),
         status=res.status, nfev=res.nfev, njev=res.njev,
         nit=res.nit, active_mask=np.frombuffer(res.active_mask, dtype=np.int8, count=n).astype(np.int64),
-        kernel_launches=res.kernel_launches, t_upload_s=res.t_upload_s, t_solve_s=res.t_solve_s,
+        kernel_launches=res.kernel_launches, graph_reused=res.graph_reused, t_upload_s=res.t_upload_s, t_solve_s=res.t_solve_s,
         t_epilogue_s=res.t_epilogue_s, epilogue_cycles=arr(res.epilogue_cycles, 8),
         timeline_ns=arr(res.timeline_ns, res.timeline_len))
     if tr is not None:
         out.trace = tr[: res.trace_len].copy()
     return out
+
+
+@dataclass
+class BatchResult:
+    x: np.ndarray          # (nfits, n)
+    cost: np.ndarray
+    optimality: np.ndarray
+    status: np.ndarray
+    nfev: np.ndarray
+    njev: np.ndarray
+    nit: np.ndarray
+
+
+def curve_fit_batch(model, z, y=None, *, grid=None, p0=None, lb=None, ub=None, sigma=None, shared_y=False,
+                    **kw) -> BatchResult:
+    """jf_curve_fit_batch: one TRF fit per row of z (nfits x m) in one launch."""
+    lib = L.load()
+    mid = _model_id(model)
+    n = lib.jf_model_nparams(mid)
+    nfits, m = int(z.shape[0]), int(z.shape[1])
+    data = _Data(y, z.reshape(-1) if not _is_cuda(z) else z.reshape(-1), sigma)
+    opts, keep = make_opts(grid=grid, sigma_ptr=data.sp, on_device=data.on_device, **kw)
+    if shared_y:
+        opts.flags |= L.FLAG_BATCH_SHARED_Y
+    p0a = None if p0 is None else _as_host(p0).reshape(nfits, n)
+    lba = None if lb is None else _as_host(lb)
+    uba = None if ub is None else _as_host(ub)
+    out = (L.jf_batch_result * nfits)()
+    rc = lib.jf_curve_fit_batch(mid, data.yp, data.zp, m, nfits, None if p0a is None else p0a.ctypes.data, n,
+                                None if lba is None else lba.ctypes.data, None if uba is None else uba.ctypes.data,
+                                C.byref(opts), out)
+    if rc < 0:
+        raise JFError(rc, "jf_curve_fit_batch")
+    rec = np.frombuffer(out, dtype=np.dtype([("x", np.float64, L.JF_MAX_N), ("cost", np.float64),
+                                             ("optimality", np.float64), ("status", np.int32),
+                                             ("nfev", np.int32), ("njev", np.int32), ("nit", np.int32)]))
+    return BatchResult(x=rec["x"][:, :n].copy(), cost=rec["cost"].copy(), optimality=rec["optimality"].copy(),
+                       status=rec["status"].copy(), nfev=rec["nfev"].copy(), njev=rec["njev"].copy(),
+                       nit=rec["nit"].copy())
 
 
 def jpass(model, z, x, y=None, *, grid=None, sigma=None, **kw):
@@ -217,6 +282,8 @@ def pass_device(model, z, x_dev, kvec_dev, y=None, *, grid=None, sigma=None, res
                             1 if residual_only else 0, kvec_dev.data_ptr())
     if rc < 0:
         raise JFError(rc, "jf_pass_device")
+    # the pass runs asynchronously: converted temporaries must outlive it
+    data.keep_alive(opts.stream)
 
 
 def trust_region_step(hatG, hatg, m, Delta, alpha=0.0, device=0):
@@ -234,6 +301,29 @@ def trust_region_step(hatG, hatg, m, Delta, alpha=0.0, device=0):
     if rc < 0:
         raise JFError(rc, "jf_trust_region_step")
     return p, a.value, it.value
+
+
+def select_step(hatB, hatg, x, lb, ub, d, p_h, Delta, theta, device=0):
+    """jf_select_step: the device Coleman-Li step selection (R19/R20).
+    Returns (step, step_h, pred, branch)."""
+    lib = L.load()
+    a = [_as_host(v) for v in (hatB, hatg, x, lb, ub, d, p_h)]
+    n = a[1].size
+    step, step_h = np.zeros(n), np.zeros(n)
+    pred, br = C.c_double(), C.c_int32()
+    opts, _ = make_opts(device=device)
+    rc = lib.jf_select_step(*[_dptr(v) for v in a], n, float(Delta), float(theta), C.byref(opts), _dptr(step),
+                            _dptr(step_h), C.byref(pred), C.byref(br))
+    if rc < 0:
+        raise JFError(rc, "jf_select_step")
+    return step, step_h, pred.value, br.value
+
+
+def graph_cache_clear(device: int = 0):
+    """jf_graph_cache_clear: the next fit on `device` instantiates its graph afresh."""
+    rc = L.load().jf_graph_cache_clear(int(device))
+    if rc < 0:
+        raise JFError(rc, "jf_graph_cache_clear")
 
 
 def exchange_handles(blob: bytes, dist) -> bytes:
@@ -297,6 +387,20 @@ class Comm:
         c = cls.create(rank, world, device)
         c.connect(exchange_handles(c.export(), dist))
         return c
+
+    def set_timeout(self, ms: int):
+        """jf_comm_set_timeout: report JF_ECOMM when a peer is missing for ms."""
+        rc = self._lib.jf_comm_set_timeout(self.handle, int(ms))
+        if rc < 0:
+            raise JFError(rc, "jf_comm_set_timeout")
+
+    def bench(self, v: float, reps: int = 100):
+        """jf_comm_bench: (rank-ordered sum of v over the ranks, us per combine)."""
+        sm, us = C.c_double(), C.c_double()
+        rc = self._lib.jf_comm_bench(self.handle, float(v), int(reps), C.byref(sm), C.byref(us))
+        if rc < 0:
+            raise JFError(rc, "jf_comm_bench")
+        return sm.value, us.value
 
     def destroy(self):
         if self.handle:

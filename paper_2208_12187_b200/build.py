@@ -27,6 +27,8 @@ LIB = os.path.join(HERE, "libjfb200.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
               "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
+if os.environ.get("JF_DEV"):  # development build: per-warp timeline stamps, diagnostics (never shipped)
+    NVCC_FLAGS += ["-DJF_DEV=1"]
 
 
 def nvcc() -> str:

@@ -36,6 +36,7 @@ struct CommDev {
   double* mbox_data[8];
   unsigned long long* mbox_flag[8];
   unsigned long long epoch;  // host-side base; the device uses st->comm_epoch
+  unsigned long long timeout_ns;  // a peer that does not arrive within this is reported (JF_ECOMM)
 };
 
 // Kernel inputs that stay fixed during one call (device-resident, so a cached
@@ -62,6 +63,26 @@ struct PassArgs {
   int32_t no_chain;     // debug (JF_DEBUG_NOCHAIN): return the Gram in the alt coordinates (a, 2b, c2)
   unsigned long long* dbg; // debug (JF_DEBUG_STAMPS): per-warp [smid, t_start, t_loop_end, t_exit] (moment kernel)
   CommDev comm;
+};
+
+// Batched many-small-fits (jf_curve_fit_batch): one warp
+// per fit, the whole TRF of a fit inside one persistent kernel.
+struct BatchResult {  // = jf_batch_result (include/jf.h)
+  double x[NMAX];
+  double cost, optimality;
+  int32_t status, nfev, njev, nit;
+};
+struct QRState;
+struct FitState;
+struct BatchArgs {
+  PassArgs base;            // the arguments of fit 0 (z, y0, y1, wsig at their base pointers)
+  int64_t nfits;
+  int64_t z_stride;         // doubles between consecutive fits' z (and sigma)
+  int64_t y_stride;         // doubles between consecutive fits' coordinates (0: shared)
+  const double* p0;         // nfits x n, or nullptr: curve_fit's default p0 for every fit
+  const FitState* tmpl;     // configuration shared by every fit (bounds, tolerances, solver mode)
+  QRState* qr;              // one TSQR working set per block
+  BatchResult* out;         // nfits results
 };
 
 }  // namespace jf

@@ -8,6 +8,7 @@
 // a host-driven loop (use_graph = 0).  Graphs are cached per (model, mode,
 // grid, policy) and replayed for any data, so only the first fit pays the
 // instantiation (cf. JAX tracing).
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -24,11 +25,17 @@
 
 using namespace jf;
 
+namespace jf {  // jf_comm.cu
+int launch_comm_sum(const CommDev& cd, unsigned long long epoch, double v, double* d_out, int* d_err, cudaStream_t s);
+const void* comm_sum_kernel_ptr();
+}  // namespace jf
+
 namespace jf {  // jf_solver.cu
 const void* solver_kernel_ptr();
 int launch_solver(FitState* st, const double* kv, cudaStream_t s);
 int launch_tr_step(const double* hatG, const double* hatg, int n, int64_t m, double Delta, double alpha_in,
                    double* out, int dbg, cudaStream_t s);
+int launch_select_step(const double* in, int n, double Delta, double theta, double* out, cudaStream_t s);
 }  // namespace jf
 
 // A rank's view of the multi-GPU mailboxes (jf.h jf_comm_*).
@@ -40,6 +47,7 @@ struct jf_comm {
   bool local = false;             // created by jf_comm_create_local
   void* peer[8] = {nullptr};      // mapped mailboxes of all ranks
   bool opened[8] = {false};
+  unsigned long long timeout_ns = 20000000000ull;  // jf_comm_set_timeout
 };
 
 namespace {
@@ -53,6 +61,11 @@ Kernels get_kernels(int model, int coord) {
     case JF_GAUSS2D_ROT_X2: return kernels_gauss2d_x2(coord);
     default: return Kernels{};
   }
+}
+
+__global__ void inv_kernel(double* p, int64_t m) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = 1.0 / p[i];
 }
 
 int model_n(int model) {
@@ -101,7 +114,11 @@ struct Ctx {
   int nsm = 148;
   cudaStream_t stream = nullptr;
   PassArgs* d_args = nullptr;
-  PassArgs h_args;           // last upload to d_args (a repeated pass skips the copy)
+  PassArgs* h_args = nullptr;  // pinned: last upload to d_args (a repeated fit skips the copy)
+  // Pinned staging for every small host<->device copy: a pageable copy is
+  // synchronous inside the driver and can stall other threads' launches while
+  // it waits — fatal when those threads' ranks spin on a combine with ours.
+  double* h_pin = nullptr;
   bool h_args_valid = false;
   FitState* d_state = nullptr;
   FitState* h_state = nullptr;  // pinned
@@ -117,13 +134,27 @@ struct Ctx {
   double* d_scratch = nullptr;  // small per-call scratch (status word, subproblem I/O)
   QRState* d_qr = nullptr;      // TSQR working set
   std::map<GraphKey, cudaGraphExec_t> graphs;
+  // Calls may run on different streams but share the buffers above: each
+  // call waits for the previous call's work (event on its stream) before it
+  // enqueues anything, and records its own completion.
+  cudaEvent_t done = nullptr;
+  cudaStream_t done_stream = nullptr;
+  // batched fits (jf_curve_fit_batch)
+  FitState* d_tmpl = nullptr;
+  QRState* d_qr_batch = nullptr;
+  int qr_batch_cap = 0;
+  BatchResult* d_bout = nullptr;
+  size_t bout_cap = 0;
 };
 
 // Contexts: [0, 64) one per device; [64, 64 + 64*8) per (device, virtual rank)
 // of a jf_comm_create_local emulation, so emulated ranks run concurrently.
 Ctx g_ctx[64 + 64 * 8];
 constexpr int SCRATCH_DOUBLES = 1024;
+constexpr int PIN_DOUBLES = 1024;
 constexpr int TICKETS = 128;  // grid_reduce: [0] groups, [1 + g] blocks of group g (<= 127 groups)
+
+void preload_kernels();
 
 int ctx_init(Ctx& c, int dev) {
   if (c.ready) return 0;
@@ -138,12 +169,15 @@ int ctx_init(Ctx& c, int dev) {
     if (!attr_done[dev]) {
       kernel_attrs_init();
       kernel_attrs_init_x2();
+      preload_kernels();
       attr_done[dev] = true;
     }
   }
   CK(cudaMalloc(&c.d_args, sizeof(PassArgs)));
   CK(cudaMalloc(&c.d_state, sizeof(FitState)));
   CK(cudaMallocHost(&c.h_state, sizeof(FitState)));
+  CK(cudaMallocHost(&c.h_args, sizeof(PassArgs)));
+  CK(cudaMallocHost(&c.h_pin, sizeof(double) * PIN_DOUBLES));
   c.partial_blocks = c.nsm * 4;
   // block rows + group rows of the two-level grid reduction (jf_pass.cuh grid_reduce)
   CK(cudaMalloc(&c.d_partials, sizeof(double) * (size_t)(c.partial_blocks + c.partial_blocks / 16 + 1) * KMAX));
@@ -152,6 +186,7 @@ int ctx_init(Ctx& c, int dev) {
   CK(cudaMalloc(&c.d_x, sizeof(double) * NMAX));
   CK(cudaMalloc(&c.d_scratch, sizeof(double) * SCRATCH_DOUBLES));
   CK(cudaMalloc(&c.d_qr, sizeof(QRState)));
+  CK(cudaEventCreateWithFlags(&c.done, cudaEventDisableTiming));
   // no device-wide synchronisation here: emulated ranks (jf_comm_create_local)
   // may have pass kernels spinning on their mailboxes while a peer initialises
   CK(cudaMemsetAsync(c.d_ticket, 0, sizeof(unsigned int) * TICKETS, c.stream));
@@ -159,6 +194,28 @@ int ctx_init(Ctx& c, int dev) {
   CK(cudaStreamSynchronize(c.stream));
   c.ready = true;
   return 0;
+}
+
+// Load every kernel a fit or pass can launch into the context now (CUDA
+// loads modules lazily at a function's first launch, and loading waits for
+// running kernels: a rank whose first launch of a kernel happens while a peer
+// rank's kernel spins on its mailbox would stall until that peer times out).
+void preload_kernels() {
+  cudaFuncAttributes fa;
+  auto touch = [&](const void* f) {
+    if (f) cudaFuncGetAttributes(&fa, f);
+  };
+  for (int model = 0; model <= JF_GAUSS2D_ROT_X2; ++model)
+    for (int coord = 0; coord <= COORD_IMPLICIT_T; ++coord) {
+      const Kernels k = get_kernels(model, coord);
+      for (KernelFn f : {k.jk, k.rk, k.jkw, k.rkw}) touch((const void*)f);
+      touch((const void*)k.small);
+      touch((const void*)k.smallw);
+    }
+  touch(solver_kernel_ptr());
+  touch(comm_sum_kernel_ptr());
+  touch((const void*)inv_kernel);
+  cudaGetLastError();
 }
 
 // The grid of a pass kernel: enough blocks to fill every SM at the kernel's
@@ -189,29 +246,29 @@ int grid_for(Ctx& c, KernelFn f, int tpb, int64_t m, int smem = 0) {
   return (int)g;
 }
 
+// The point count launch shapes are sized for: the capacity when one is set
+// (jf_opts.capacity, N3: one cached graph serves every m <= capacity).
+int64_t pass_grid_m(const jf_opts& o, int64_t m) { return o.capacity > 0 ? o.capacity : m; }
+
+const PassArgs g_zero_args = {};  // the by-value args of launches that read device-resident ones
+
 // The two pass kernels a call uses, with their launch shapes.
 struct PassPair {
-  KernelFn j = nullptr, r = nullptr, jp = nullptr;
-  int jtpb = 256, rtpb = 256, jptpb = 256, jgrid = 1, rgrid = 1, jpgrid = 1, jsmem = 0;
+  KernelFn j = nullptr, r = nullptr;
+  int jtpb = 256, rtpb = 256, jgrid = 1, rgrid = 1, jsmem = 0;
 };
 
 PassPair select_pass(Ctx& c, const Kernels& k, bool weighted, int64_t m) {
   PassPair p;
   p.j = weighted ? k.jkw : k.jk;
   p.r = weighted ? k.rkw : k.rk;
-  p.jp = weighted ? k.jkpw : k.jkp;
   p.jtpb = (weighted && k.jwtpb > 0) ? k.jwtpb : k.jtpb;
   p.rtpb = k.rtpb;
-  p.jptpb = k.jptpb;
   p.jsmem = weighted ? 0 : k.jsmem;
   p.jgrid = grid_for(c, p.j, p.jtpb, m, p.jsmem);
-  p.jpgrid = p.jp ? grid_for(c, p.jp, p.jptpb, m) : 1;
   const bool jsplit = (weighted && k.jwsplit >= 0) ? (k.jwsplit != 0) : k.jsplit;
   if (jsplit) {  // two equal halves
     p.jgrid = p.jgrid < 2 ? 2 : p.jgrid + (p.jgrid & 1);
-  }
-  if (k.jsplit || k.jwsplit > 0) {  // the preconditioned (TSQR) kernel is always the dual-number one
-    p.jpgrid = p.jpgrid < 2 ? 2 : p.jpgrid + (p.jpgrid & 1);
   }
   p.rgrid = grid_for(c, p.r, p.rtpb, m);
   return p;
@@ -234,6 +291,7 @@ void fill_comm(CommDev& cd, const jf_comm* cm) {
     cd.mbox_flag[p] = (unsigned long long*)(base + MBOX_DATA_BYTES(cm->nranks));
   }
   cd.epoch = cm->epoch;
+  cd.timeout_ns = cm->timeout_ns;
 }
 
 struct Staged {
@@ -257,10 +315,6 @@ int ensure(double*& p, size_t& cap, size_t need, cudaStream_t s) {
   return 0;
 }
 
-__global__ void inv_kernel(double* p, int64_t m) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
-    p[i] = 1.0 / p[i];
-}
 
 // Validate the data description and make y/z/sigma available in HBM.
 int stage_inputs(Ctx& c, cudaStream_t s, int model, const double* y, const double* z, int64_t m,
@@ -320,7 +374,7 @@ int stage_inputs(Ctx& c, cudaStream_t s, int model, const double* y, const doubl
 }
 
 void fill_args(PassArgs& a, const Staged& sg, int64_t m, const jf_opts& o) {
-  memset(&a, 0, sizeof(a));
+  memset(&a, 0, sizeof(a));  // padding too: fit args are compared bytewise with the last upload
   a.z = sg.z;
   a.y0 = sg.y0;
   a.y1 = sg.y1;
@@ -380,18 +434,44 @@ void active_mask_host(const double* x, const double* lb, const double* ub, int n
   }
 }
 
-int launch_pass(const PassPair& k, bool jac, cudaStream_t s, PassArgs* d_args, FitState* d_state,
-                bool prec = false) {
-  KernelFn f = jac ? (prec ? k.jp : k.j) : k.r;
-  const int grid = jac ? (prec ? k.jpgrid : k.jgrid) : k.rgrid;
-  const int tpb = jac ? (prec ? k.jptpb : k.jtpb) : k.rtpb;
-  const int smem = (jac && !prec) ? k.jsmem : 0;
-  f<<<grid, tpb, smem, s>>>(d_args, d_state, (cudaGraphConditionalHandle)0, 0);
+// One pass kernel launch: d_args (device-resident, fits) or, with d_args ==
+// nullptr, the arguments by value (plain passes: immutable once enqueued or
+// captured into a graph).
+int launch_pass(const PassPair& k, bool jac, cudaStream_t s, const PassArgs* d_args, FitState* d_state,
+                const PassArgs& av) {
+  KernelFn f = jac ? k.j : k.r;
+  const int grid = jac ? k.jgrid : k.rgrid;
+  const int tpb = jac ? k.jtpb : k.rtpb;
+  const int smem = jac ? k.jsmem : 0;
+  f<<<grid, tpb, smem, s>>>(d_args, d_state, (cudaGraphConditionalHandle)0, 0, av);
   CK(cudaGetLastError());
   return 0;
 }
 
+bool capturing(cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  return cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone;
+}
+
+// Stream ordering of the context's shared buffers across calls (see Ctx::done).
+struct StreamOrder {
+  Ctx* c = nullptr;
+  cudaStream_t s = nullptr;
+  bool cap = false;
+  int begin(Ctx* c_, cudaStream_t s_) {
+    c = c_;
+    s = s_;
+    cap = capturing(s);
+    if (!cap && c->done_stream && c->done_stream != s) CK(cudaStreamWaitEvent(s, c->done, 0));
+    return 0;
+  }
+  ~StreamOrder() {
+    if (c && !cap && cudaEventRecord(c->done, s) == cudaSuccess) c->done_stream = s;
+  }
+};
+
 int build_graph(Ctx& c, const PassPair& k, int policy, bool qr, cudaGraphExec_t* out) {
+  (void)qr;
   cudaGraph_t g;
   CK(cudaGraphCreate(&g, 0));
   cudaGraphConditionalHandle h;
@@ -408,7 +488,9 @@ int build_graph(Ctx& c, const PassPair& k, int policy, bool qr, cudaGraphExec_t*
   PassArgs* pa = c.d_args;
   FitState* st = c.d_state;
   const double* kv = c.d_out;
-  void* pargs[4] = {&pa, &st, &h, &use};
+  PassArgs av;
+  memset(&av, 0, sizeof(av));  // unused: the fit's args are read from pa
+  void* pargs[5] = {&pa, &st, &h, &use, &av};
   void* sargs[4] = {&st, &kv, &h, &use};
   cudaKernelNodeParams kp;
   memset(&kp, 0, sizeof(kp));
@@ -455,8 +537,7 @@ int build_graph(Ctx& c, const PassPair& k, int policy, bool qr, cudaGraphExec_t*
   // U copies of the iteration per trip of the WHILE loop: the conditional
   // node's per-trip overhead is paid once per U iterations; copies after the
   // fit ended find nothing to do (phase DONE) and return at once.
-  int unroll = 2;
-  if (const char* e = getenv("JF_GRAPH_UNROLL")) unroll = atoi(e) < 1 ? 1 : atoi(e);
+  constexpr int unroll = 2;
   for (int u = 0; u < unroll; ++u) {
     if (policy == JF_POLICY_CONSERVATIVE) {
       kp.func = (void*)k.r;
@@ -465,12 +546,8 @@ int build_graph(Ctx& c, const PassPair& k, int policy, bool qr, cudaGraphExec_t*
       if (int e = add(kp, false)) return e;
       if (int e = add(sp, true)) return e;
     }
-    if (qr) {  // TSQR: the preconditioned second pass runs when the phase is PH_QR2
-      kp.func = (void*)k.jp;
-      kp.gridDim = dim3(k.jpgrid);
-      kp.blockDim = dim3(k.jptpb);
-      if (int e = add(kp, false)) return e;
-    }
+    // (TSQR: the J-pass kernel also runs the preconditioned second pass when
+    // the phase is PH_QR2 — no separate node)
     kp.func = (void*)k.j;
     kp.gridDim = dim3(k.jgrid);
     kp.blockDim = dim3(k.jtpb);
@@ -495,7 +572,7 @@ void jf_opts_default(jf_opts* o) {
   o->ftol = o->xtol = o->gtol = 1e-8;
   o->max_nfev = 0;
   o->x_scale_mode = JF_XSCALE_JAC;
-  o->solver = JF_SOLVE_GRAM;
+  o->solver = JF_SOLVE_AUTO;
   o->policy = JF_POLICY_SPECULATIVE;
   o->t0 = 0.0;
   o->dt = 1.0;
@@ -540,31 +617,32 @@ static int pass_common(int32_t model, const double* y, const double* z, int64_t 
   cudaStream_t s;
   int r = acquire(o, c, lk, s);
   if (r) return r;
+  StreamOrder order;
+  if ((r = order.begin(c, s))) return r;
   Staged sg;
   r = stage_inputs(*c, s, model, y, z, m, o, sg);
   if (r) return r;
   Kernels kk = get_kernels(model, sg.coord);
   if (!kk.jk) return JF_EINVAL;
-  const PassPair k = select_pass(*c, kk, sg.wsig != nullptr, m);
+  const PassPair k = select_pass(*c, kk, sg.wsig != nullptr, pass_grid_m(o, m));
   PassArgs a;
-  memset(&a, 0, sizeof(a));  // padding too: the args are compared bytewise with the last upload
   fill_args(a, sg, m, o);
   a.epilogue = EPI_NONE;
-  a.no_chain = getenv("JF_DEBUG_NOCHAIN") ? 1 : 0;
-  const char* stamps = residual_only ? nullptr : getenv("JF_DEBUG_STAMPS");  // development aid: per-warp timeline
-  if (stamps) {
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) stamps = nullptr;
-  }
+  a.no_chain = (o.flags & JF_FLAG_ALT_COORDS) ? 1 : 0;
+#if JF_DEV  // development builds: per-warp timeline of the moment J-pass (tools/stamps2.py)
+  const char* stamps = (residual_only || order.cap) ? nullptr : getenv("JF_DEBUG_STAMPS");
   static unsigned long long* d_dbg = nullptr;
   constexpr int DBG_N = 4 * 16384;
   if (stamps && !d_dbg) CK(cudaMalloc(&d_dbg, sizeof(unsigned long long) * DBG_N));
   a.dbg = stamps ? d_dbg : nullptr;
   if (stamps) CK(cudaMemsetAsync(d_dbg, 0, sizeof(unsigned long long) * DBG_N, s));
+#endif
   if (x_on_device) {
     a.x = x;
   } else {
-    CK(cudaMemcpyAsync(c->d_x, x, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    double* hx = c->h_pin + 512;  // (the previous call's copy finished: calls are stream-ordered)
+    memcpy(hx, x, sizeof(double) * n);
+    CK(cudaMemcpyAsync(c->d_x, hx, sizeof(double) * n, cudaMemcpyHostToDevice, s));
     a.x = c->d_x;
   }
   a.partials = c->d_partials;
@@ -576,15 +654,11 @@ static int pass_common(int32_t model, const double* y, const double* z, int64_t 
     fill_comm(a.comm, o.comm);
     o.comm->epoch += 1;
   }
-  if (!c->h_args_valid || memcmp(&c->h_args, &a, sizeof(a)) != 0) {
-    // source: the context's persistent copy (a copy captured into a CUDA
-    // graph must not read a stack buffer at replay)
-    c->h_args = a;
-    c->h_args_valid = true;
-    CK(cudaMemcpyAsync(c->d_args, &c->h_args, sizeof(a), cudaMemcpyHostToDevice, s));
-  }
-  r = launch_pass(k, !residual_only, s, c->d_args, c->d_state);
+  // the arguments travel by value with the launch (immutable once enqueued
+  // or captured into a graph)
+  r = launch_pass(k, !residual_only, s, nullptr, c->d_state, a);
   if (r) return r;
+#if JF_DEV
   if (stamps) {
     static unsigned long long h_dbg[DBG_N];
     CK(cudaMemcpyAsync(h_dbg, d_dbg, sizeof(h_dbg), cudaMemcpyDeviceToHost, s));
@@ -594,14 +668,15 @@ static int pass_common(int32_t model, const double* y, const double* z, int64_t 
       fclose(f);
     }
   }
-  if (host_out) {
-    const int KS = residual_only ? 2 : tri_count(n) + 1;
-    CK(cudaMemcpyAsync(host_out, a.out, sizeof(double) * KS, cudaMemcpyDeviceToHost, s));
-  }
+#endif
+  const int KSo = residual_only ? 2 : tri_count(n) + 1;
+  if (host_out) CK(cudaMemcpyAsync(c->h_pin, a.out, sizeof(double) * KSo, cudaMemcpyDeviceToHost, s));
   if (sync) {
-    int err = 0;
-    CK(cudaMemcpyAsync(&err, a.err, sizeof(int), cudaMemcpyDeviceToHost, s));
+    int* herr = (int*)(c->h_pin + 256);
+    CK(cudaMemcpyAsync(herr, a.err, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    const int err = *herr;
+    if (host_out) memcpy(host_out, c->h_pin, sizeof(double) * KSo);
     if (err) {
       CK(cudaMemsetAsync(a.err, 0, sizeof(int), s));
       CK(cudaStreamSynchronize(s));
@@ -655,7 +730,8 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
   if (opts) o = *opts;
   else jf_opts_default(&o);
   if (model_n(model) < 0 || n != model_n(model) || !z || m < 1) return fail(JF_EINVAL);
-  if (o.comm && o.m_global < m) return fail(JF_EINVAL);
+  if (o.comm && o.m_global != 0 && o.m_global < m) return fail(JF_EINVAL);
+  if (o.capacity < 0 || (o.capacity > 0 && o.capacity < m)) return fail(JF_EINVAL);
   out->n = n;
   // ---- bounds and initial point (R18, R19)
   double L[NMAX], U[NMAX], X0[NMAX], XS[NMAX];
@@ -694,13 +770,34 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
   cudaStream_t s;
   int r = acquire(o, c, lk, s);
   if (r) return fail(r);
+  StreamOrder order;
+  if ((r = order.begin(c, s))) return fail(r);
+  if (order.cap) return fail(JF_EINVAL);  // a fit synchronises: it cannot be captured
   Staged sg;
   r = stage_inputs(*c, s, model, y, z, m, o, sg);
   if (r) return fail(r);
   out->t_upload_s = sg.upload_s;
   Kernels kk = get_kernels(model, sg.coord);
   if (!kk.jk) return fail(JF_EINVAL);
-  const PassPair k = select_pass(*c, kk, sg.wsig != nullptr, m);
+  const int64_t mg = pass_grid_m(o, m);  // launch shapes are sized for the capacity (N3)
+  const PassPair k = select_pass(*c, kk, sg.wsig != nullptr, mg);
+  int64_t m_global = m;
+  if (o.comm) {
+    m_global = o.m_global;
+    if (m_global == 0) {  // R6 needs the global m: one combine of the ranks' m at the start
+      o.comm->epoch += 1;
+      CommDev cd;
+      fill_comm(cd, o.comm);
+      double* d_m = c->d_scratch + 4;
+      int* d_err = (int*)(c->d_scratch + 5);
+      if (launch_comm_sum(cd, o.comm->epoch, (double)m, d_m, d_err, s)) return fail(JF_ECUDA);
+      CK(cudaMemcpyAsync(c->h_pin, d_m, sizeof(double), cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(c->h_pin + 1, d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      if (*(int*)(c->h_pin + 1)) return fail(JF_ECOMM);
+      m_global = (int64_t)c->h_pin[0];
+    }
+  }
 
   // trace buffer
   if (o.trace_cap > 0) {
@@ -720,7 +817,7 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
   h.policy = o.policy;
   h.trace_cap = o.trace_cap > 0 ? o.trace_cap : 0;
   h.trace = c->d_trace;
-  h.m_global = o.comm ? o.m_global : m;
+  h.m_global = m_global;
   h.ftol = o.ftol;
   h.xtol = o.xtol;
   h.gtol = o.gtol;
@@ -735,6 +832,8 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
   // preconditioned-pass node in the graph
   const bool qr = (o.solver == JF_SOLVE_TSQR || o.solver == JF_SOLVE_AUTO);
   h.qr_mode = (o.solver == JF_SOLVE_TSQR) ? 1 : (o.solver == JF_SOLVE_AUTO ? 2 : 0);
+  h.auto_mode = (o.solver == JF_SOLVE_AUTO) ? 1 : 0;
+  h.kappa2_gn = 0.0;
   h.qr = c->d_qr;
   h.prec = c->d_qr->prec;
   h.phase = PH_INIT_J;
@@ -756,18 +855,17 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
   }
   auto t0 = std::chrono::steady_clock::now();
   CK(cudaMemcpyAsync(c->d_state, &h, sizeof(h), cudaMemcpyHostToDevice, s));
-  if (!c->h_args_valid || memcmp(&c->h_args, &a, sizeof(a)) != 0) {  // a repeated fit skips the copy
-    c->h_args = a;
+  if (!c->h_args_valid || memcmp(c->h_args, &a, sizeof(a)) != 0) {  // a repeated fit skips the copy
+    *c->h_args = a;
     c->h_args_valid = true;
-    CK(cudaMemcpyAsync(c->d_args, &c->h_args, sizeof(a), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(c->d_args, c->h_args, sizeof(a), cudaMemcpyHostToDevice, s));
   }
   int launches = 0;
   // small m: the whole fit in one single-block kernel (state in shared memory)
   const int n64_est = 10 + 8 * n + (n + 1) * (n + 2) / 2;
-  double small_budget = 1.0e6;
-  if (const char* e = getenv("JF_SMALL_WORK")) small_budget = atof(e);
-  const bool small = !o.comm && !qr && o.policy == JF_POLICY_SPECULATIVE && kk.small &&
-                     (double)m * n64_est <= small_budget;
+  constexpr double small_budget = 1.0e6;  // fp64 operations of one pass that one block absorbs
+  const bool small = !o.comm && o.policy == JF_POLICY_SPECULATIVE && kk.small &&
+                     (double)mg * n64_est <= small_budget;
   if (small) {
     SmallFitFn f = sg.wsig ? kk.smallw : kk.small;
     f<<<1, 256, 0, s>>>(c->d_args, c->d_state);
@@ -784,24 +882,16 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
       c->graphs[key] = ge;
     } else {
       ge = it->second;
+      out->graph_reused = 1;
     }
-    const auto tl0 = std::chrono::steady_clock::now();
     CK(cudaGraphLaunch(ge, s));
-    const auto tl1 = std::chrono::steady_clock::now();
     CK(cudaMemcpyAsync(&h, c->d_state, sizeof(h), cudaMemcpyDeviceToHost, s));
-    const auto tl2 = std::chrono::steady_clock::now();
     CK(cudaStreamSynchronize(s));
-    if (getenv("JF_DEBUG_FIT_TIMES")) {  // development aid: host-side phases of the graph fit
-      const auto tl3 = std::chrono::steady_clock::now();
-      auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
-      fprintf(stderr, "jf fit: prep->launch %.1f us, cudaGraphLaunch %.1f us, D2H enqueue %.1f us, sync %.1f us\n",
-              us(t0, tl0), us(tl0, tl1), us(tl1, tl2), us(tl2, tl3));
-    }
   } else {
     const int cap = 4 * h.max_nfev + 8;
     for (int iter = 0; iter < cap; ++iter) {
       const bool jac = (o.policy == JF_POLICY_CONSERVATIVE) ? (h.phase != PH_TRIAL_R) : true;
-      r = launch_pass(k, jac, s, c->d_args, c->d_state, h.phase == PH_QR2);
+      r = launch_pass(k, jac, s, c->d_args, c->d_state, g_zero_args);  // J kernels also run PH_QR2
       if (r) return fail(r);
       if (launch_solver(c->d_state, c->d_out, s)) return fail(JF_ECUDA);
       CK(cudaMemcpyAsync(&h, c->d_state, sizeof(h), cudaMemcpyDeviceToHost, s));
@@ -835,7 +925,10 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
   if (bounded) active_mask_host(h.x, L, U, n, o.xtol, out->active_mask);
   out->trace_len = h.trace_len < o.trace_cap ? h.trace_len : o.trace_cap;
   if (o.trace_cap > 0 && out->trace_len > 0)
-    CK(cudaMemcpy(o.trace, c->d_trace, sizeof(double) * TRACE_FIELDS * out->trace_len, cudaMemcpyDeviceToHost));
+  {
+    CK(cudaMemcpyAsync(o.trace, c->d_trace, sizeof(double) * TRACE_FIELDS * out->trace_len, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  }
   if (h.error) return fail(h.error);
   if (h.cont) return fail(JF_ECUDA);  // loop did not terminate
   out->status = h.status;
@@ -849,6 +942,163 @@ int32_t jf_curve_fit(int32_t model, const double* y, const double* z, int64_t m,
   const int32_t r = fit_impl(model, y, z, m, p0, n, lb, ub, opts, out);
   if (r < 0) out->status = r;
   return r;
+}
+
+// ------------------------------------------------- batched many small fits
+int32_t jf_curve_fit_batch(int32_t model, const double* y, const double* z, int64_t m, int64_t nfits,
+                           const double* p0, int32_t n, const double* lb, const double* ub, const jf_opts* opts,
+                           jf_batch_result* out) {
+  static_assert(sizeof(jf_batch_result) == sizeof(BatchResult), "jf_batch_result layout");
+  jf_opts o;
+  if (opts) o = *opts;
+  else jf_opts_default(&o);
+  const int d = model_d(model);
+  if (model_n(model) < 0 || n != model_n(model) || !z || !out || m < 1 || nfits < 1 || o.comm) return JF_EINVAL;
+  if (o.x_scale_mode < 0 || o.x_scale_mode > 2 || o.solver < 0 || o.solver > 2) return JF_EINVAL;
+  double L[NMAX], U[NMAX], XS[NMAX];
+  bool bounded = false;
+  for (int j = 0; j < n; ++j) {
+    L[j] = lb ? lb[j] : -INFINITY;
+    U[j] = ub ? ub[j] : INFINITY;
+    if (std::isnan(L[j]) || std::isnan(U[j]) || !(L[j] < U[j])) return JF_EINVAL;
+    if (std::isfinite(L[j]) || std::isfinite(U[j])) bounded = true;
+    XS[j] = 1.0;
+  }
+  if (o.x_scale_mode == JF_XSCALE_ARRAY) {
+    if (!o.x_scale) return JF_EINVAL;
+    for (int j = 0; j < n; ++j) {
+      if (!std::isfinite(o.x_scale[j]) || !(o.x_scale[j] > 0)) return JF_EINVAL;
+      XS[j] = 1.0 / o.x_scale[j];
+    }
+  }
+  int coord = COORD_EXPLICIT;
+  if (!y) {
+    if (d == 2) {
+      if (o.grid_w < 1 || o.grid_h < 1 || o.grid_w * o.grid_h != m) return JF_EINVAL;
+      coord = COORD_GRID;
+    } else {
+      if (!std::isfinite(o.t0) || !std::isfinite(o.dt)) return JF_EINVAL;
+      coord = COORD_IMPLICIT_T;
+    }
+  }
+  const bool shared_y = (o.flags & JF_FLAG_BATCH_SHARED_Y) != 0;
+  Kernels kk = get_kernels(model, coord);
+  BatchFn f = o.sigma ? kk.batchw : kk.batch;
+  if (!f) return JF_EINVAL;
+  Ctx* c;
+  std::unique_lock<std::mutex> lk;
+  cudaStream_t s;
+  int r = acquire(o, c, lk, s);
+  if (r) return r;
+  StreamOrder order;
+  if ((r = order.begin(c, s))) return r;
+  if (order.cap) return JF_EINVAL;
+  // ---- data in HBM
+  const size_t nz = (size_t)nfits * m;
+  const size_t ny = (coord == COORD_EXPLICIT) ? (size_t)d * m * (shared_y ? 1 : nfits) : 0;
+  const size_t nw = o.sigma ? nz : 0;
+  const size_t np0 = p0 ? (size_t)nfits * n : 0;
+  BatchArgs ba;
+  memset(&ba, 0, sizeof(ba));
+  const double *zd = z, *yd = y, *wd = o.sigma, *pd = p0;
+  const size_t need = (o.inputs_on_device ? 0 : nz + ny) + nw + np0;
+  if (int e = ensure(c->d_in, c->in_cap, need, s)) return e;
+  double* q = c->d_in;
+  if (!o.inputs_on_device) {
+    CK(cudaMemcpyAsync(q, z, sizeof(double) * nz, cudaMemcpyHostToDevice, s));
+    zd = q;
+    q += nz;
+    if (ny) {
+      CK(cudaMemcpyAsync(q, y, sizeof(double) * ny, cudaMemcpyHostToDevice, s));
+      yd = q;
+      q += ny;
+    }
+  }
+  if (nw) {  // 1 / sigma
+    CK(cudaMemcpyAsync(q, o.sigma, sizeof(double) * nw, o.inputs_on_device ? cudaMemcpyDeviceToDevice
+                                                                           : cudaMemcpyHostToDevice, s));
+    inv_kernel<<<c->nsm * 4, 256, 0, s>>>(q, (int64_t)nw);
+    CK(cudaGetLastError());
+    wd = q;
+    q += nw;
+  }
+  if (np0) {  // p0 always from the host
+    CK(cudaMemcpyAsync(q, p0, sizeof(double) * np0, cudaMemcpyHostToDevice, s));
+    pd = q;
+    q += np0;
+  }
+  // ---- the shared configuration (a FitState template)
+  if (!c->d_tmpl) CK(cudaMalloc(&c->d_tmpl, sizeof(FitState)));
+  FitState& h = *c->h_state;
+  memset(&h, 0, sizeof(h));
+  h.n = n;
+  h.bounded = bounded ? 1 : 0;
+  h.jacmode = (o.x_scale_mode == JF_XSCALE_JAC) ? 1 : 0;
+  h.max_nfev = o.max_nfev > 0 ? o.max_nfev : 100 * n;
+  h.policy = JF_POLICY_SPECULATIVE;
+  h.m_global = m;
+  h.ftol = o.ftol;
+  h.xtol = o.xtol;
+  h.gtol = o.gtol;
+  for (int j = 0; j < NMAX; ++j) {
+    h.lb[j] = j < n ? L[j] : 0.0;
+    h.ub[j] = j < n ? U[j] : 0.0;
+    h.xs_inv[j] = j < n ? XS[j] : 1.0;
+  }
+  h.qr_mode = (o.solver == JF_SOLVE_TSQR) ? 1 : (o.solver == JF_SOLVE_AUTO ? 2 : 0);
+  h.auto_mode = (o.solver == JF_SOLVE_AUTO) ? 1 : 0;
+  h.phase = PH_INIT_J;
+  h.status = STATUS_NONE;
+  h.cont = 1;
+  CK(cudaMemcpyAsync(c->d_tmpl, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+  // ---- launch: one warp per fit, persistent blocks
+  static std::mutex occ_mu;
+  static std::map<std::pair<int, const void*>, int> occ_cache;
+  int occ = 1;
+  {
+    std::lock_guard<std::mutex> g(occ_mu);
+    auto key = std::make_pair(c->dev, (const void*)f);
+    auto it = occ_cache.find(key);
+    if (it == occ_cache.end()) {
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, 32, 0) != cudaSuccess || occ < 1) occ = 1;
+      occ_cache[key] = occ;
+    } else {
+      occ = it->second;
+    }
+  }
+  const int grid = (int)std::min<int64_t>(nfits, (int64_t)c->nsm * occ);
+  if (c->qr_batch_cap < grid) {
+    if (c->d_qr_batch) CK(cudaFreeAsync(c->d_qr_batch, s));
+    CK(cudaMallocAsync((void**)&c->d_qr_batch, sizeof(QRState) * grid, s));
+    c->qr_batch_cap = grid;
+  }
+  if (c->bout_cap < (size_t)nfits) {
+    if (c->d_bout) CK(cudaFreeAsync(c->d_bout, s));
+    CK(cudaMallocAsync((void**)&c->d_bout, sizeof(BatchResult) * nfits, s));
+    c->bout_cap = nfits;
+  }
+  Staged sg;
+  sg.z = zd;
+  sg.coord = coord;
+  if (coord == COORD_EXPLICIT) {
+    sg.y0 = yd;
+    sg.y1 = (d == 2) ? yd + m : nullptr;
+  }
+  sg.wsig = wd;
+  fill_args(ba.base, sg, m, o);
+  ba.base.epilogue = EPI_NONE;
+  ba.nfits = nfits;
+  ba.z_stride = m;
+  ba.y_stride = (coord == COORD_EXPLICIT && !shared_y) ? (int64_t)d * m : 0;
+  ba.p0 = pd;
+  ba.tmpl = c->d_tmpl;
+  ba.qr = c->d_qr_batch;
+  ba.out = c->d_bout;
+  f<<<grid, 32, 0, s>>>(ba);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, c->d_bout, sizeof(BatchResult) * nfits, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return 0;
 }
 
 // ----------------------------------------------------- subproblem test hook
@@ -873,13 +1123,48 @@ extern "C" int32_t jf_trust_region_step(const double* hatG, const double* hatg, 
   double* dout = dg + n;
   CK(cudaMemcpyAsync(dG, hatG, sizeof(double) * n * n, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(dg, hatg, sizeof(double) * n, cudaMemcpyHostToDevice, s));
-  if (launch_tr_step(dG, dg, n, m, Delta, alpha_in, dout, getenv("JF_DEBUG") != nullptr, s)) return JF_ECUDA;
+  if (launch_tr_step(dG, dg, n, m, Delta, alpha_in, dout, 0, s)) return JF_ECUDA;
   double hout[2 * NMAX + 2];
   CK(cudaMemcpyAsync(hout, dout, sizeof(hout), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   for (int j = 0; j < n; ++j) p[j] = hout[j];
   if (alpha_out) *alpha_out = hout[2 * NMAX];
   if (n_iter) *n_iter = (int32_t)hout[2 * NMAX + 1];
+  return 0;
+}
+
+extern "C" int32_t jf_select_step(const double* hatB, const double* hatg, const double* x, const double* lb,
+                                  const double* ub, const double* d, const double* p_h, int32_t n, double Delta,
+                                  double theta, const jf_opts* opts, double* step, double* step_h, double* pred,
+                                  int32_t* branch) {
+  jf_opts o;
+  if (opts) o = *opts;
+  else jf_opts_default(&o);
+  if (!hatB || !hatg || !x || !lb || !ub || !d || !p_h || !step || n < 1 || n > NMAX || !(Delta > 0)) return JF_EINVAL;
+  Ctx* c;
+  std::unique_lock<std::mutex> lk;
+  cudaStream_t s;
+  int r = acquire(o, c, lk, s);
+  if (r) return r;
+  StreamOrder order;
+  if ((r = order.begin(c, s))) return r;
+  double hin[NMAX * NMAX + 6 * NMAX];
+  memcpy(hin, hatB, sizeof(double) * n * n);
+  const double* src[6] = {hatg, x, lb, ub, d, p_h};
+  for (int q = 0; q < 6; ++q) memcpy(hin + n * n + q * n, src[q], sizeof(double) * n);
+  double* din = c->d_scratch + 8;
+  double* dout = din + NMAX * NMAX + 6 * NMAX;
+  CK(cudaMemcpyAsync(din, hin, sizeof(double) * (n * n + 6 * n), cudaMemcpyHostToDevice, s));
+  if (launch_select_step(din, n, Delta, theta, dout, s)) return JF_ECUDA;
+  double hout[2 * NMAX + 2];
+  CK(cudaMemcpyAsync(hout, dout, sizeof(hout), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  for (int j = 0; j < n; ++j) {
+    step[j] = hout[j];
+    if (step_h) step_h[j] = hout[NMAX + j];
+  }
+  if (pred) *pred = hout[2 * NMAX];
+  if (branch) *branch = (int32_t)hout[2 * NMAX + 1];
   return 0;
 }
 
@@ -984,6 +1269,65 @@ int32_t jf_comm_create_local(int32_t nranks, int32_t device, jf_comm** comms) {
     }
   }
   for (int r = 0; r < nranks; ++r) comms[r] = cs[r];
+  return 0;
+}
+
+int32_t jf_comm_set_timeout(jf_comm* comm, int32_t timeout_ms) {
+  if (!comm || timeout_ms < 1) return JF_EINVAL;
+  comm->timeout_ns = (unsigned long long)timeout_ms * 1000000ull;
+  return 0;
+}
+
+int32_t jf_comm_bench(jf_comm* comm, double v, int32_t reps, double* sum, double* us) {
+  if (!comm || reps < 1) return JF_EINVAL;
+  jf_opts o;
+  jf_opts_default(&o);
+  o.device = comm->device;
+  o.comm = comm;
+  Ctx* c;
+  std::unique_lock<std::mutex> lk;
+  cudaStream_t s;
+  int r = acquire(o, c, lk, s);
+  if (r) return r;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  double* d_v = c->d_scratch + 4;
+  int* d_err = (int*)(c->d_scratch + 5);
+  CommDev cd;
+  fill_comm(cd, comm);
+  comm->epoch += 1;  // one warm-up combine
+  if (launch_comm_sum(cd, comm->epoch, v, d_v, d_err, s)) return JF_ECUDA;
+  CK(cudaEventRecord(e0, s));
+  for (int i = 0; i < reps; ++i) {
+    comm->epoch += 1;
+    if (launch_comm_sum(cd, comm->epoch, v, d_v, d_err, s)) return JF_ECUDA;
+  }
+  CK(cudaEventRecord(e1, s));
+  CK(cudaMemcpyAsync(c->h_pin, d_v, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(c->h_pin + 1, d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const double hv = c->h_pin[0];
+  const int herr = *(int*)(c->h_pin + 1);
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (herr) return JF_ECOMM;
+  if (sum) *sum = hv;
+  if (us) *us = 1e3 * ms / reps;
+  return 0;
+}
+
+int32_t jf_graph_cache_clear(int32_t device) {
+  if (device < 0 || device >= 64) return JF_EINVAL;
+  Ctx& c = g_ctx[device];
+  std::lock_guard<std::mutex> g(c.mu);
+  if (!c.ready) return 0;
+  if (cudaSetDevice(device) != cudaSuccess) return JF_ECUDA;
+  if (c.done_stream) cudaEventSynchronize(c.done);
+  for (auto& kv : c.graphs) cudaGraphExecDestroy(kv.second);
+  c.graphs.clear();
   return 0;
 }
 

@@ -10,12 +10,11 @@ static Kernels make() {
   k.rk = pass_kernel<ModelExpDecay, false, C, false>;
   k.jkw = pass_kernel<ModelExpDecay, true, C, true>;
   k.rkw = pass_kernel<ModelExpDecay, false, C, true>;
-  k.jkp = pass_kernel<ModelExpDecay, true, C, false, PassCfg<ModelExpDecay, true>::P, PassCfg<ModelExpDecay, true>::TPB, PassCfg<ModelExpDecay, true>::MINB, true>;
-  k.jkpw = pass_kernel<ModelExpDecay, true, C, true, PassCfg<ModelExpDecay, true>::P, PassCfg<ModelExpDecay, true>::TPB, PassCfg<ModelExpDecay, true>::MINB, true>;
   k.jtpb = PassCfg<ModelExpDecay, true>::TPB;
-  k.jptpb = PassCfg<ModelExpDecay, true>::TPB;
   k.jsplit = PassCfg<ModelExpDecay, true>::SPLIT;
   k.small = fit_small_kernel<ModelExpDecay, C, false>;
+  k.batch = fit_batch_kernel<ModelExpDecay, C, false>;
+  k.batchw = fit_batch_kernel<ModelExpDecay, C, true>;
   k.smallw = fit_small_kernel<ModelExpDecay, C, true>;
   k.rtpb = PassCfg<ModelExpDecay, false>::TPB;
   return k;

@@ -10,12 +10,11 @@ static Kernels make() {
   k.rk = pass_kernel<ModelGauss1D, false, C, false>;
   k.jkw = pass_kernel<ModelGauss1D, true, C, true>;
   k.rkw = pass_kernel<ModelGauss1D, false, C, true>;
-  k.jkp = pass_kernel<ModelGauss1D, true, C, false, PassCfg<ModelGauss1D, true>::P, PassCfg<ModelGauss1D, true>::TPB, PassCfg<ModelGauss1D, true>::MINB, true>;
-  k.jkpw = pass_kernel<ModelGauss1D, true, C, true, PassCfg<ModelGauss1D, true>::P, PassCfg<ModelGauss1D, true>::TPB, PassCfg<ModelGauss1D, true>::MINB, true>;
   k.jtpb = PassCfg<ModelGauss1D, true>::TPB;
-  k.jptpb = PassCfg<ModelGauss1D, true>::TPB;
   k.jsplit = PassCfg<ModelGauss1D, true>::SPLIT;
   k.small = fit_small_kernel<ModelGauss1D, C, false>;
+  k.batch = fit_batch_kernel<ModelGauss1D, C, false>;
+  k.batchw = fit_batch_kernel<ModelGauss1D, C, true>;
   k.smallw = fit_small_kernel<ModelGauss1D, C, true>;
   k.rtpb = PassCfg<ModelGauss1D, false>::TPB;
   return k;

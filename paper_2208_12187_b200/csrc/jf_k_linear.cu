@@ -10,12 +10,11 @@ static Kernels make() {
   k.rk = pass_kernel<ModelLinear, false, C, false>;
   k.jkw = pass_kernel<ModelLinear, true, C, true>;
   k.rkw = pass_kernel<ModelLinear, false, C, true>;
-  k.jkp = pass_kernel<ModelLinear, true, C, false, PassCfg<ModelLinear, true>::P, PassCfg<ModelLinear, true>::TPB, PassCfg<ModelLinear, true>::MINB, true>;
-  k.jkpw = pass_kernel<ModelLinear, true, C, true, PassCfg<ModelLinear, true>::P, PassCfg<ModelLinear, true>::TPB, PassCfg<ModelLinear, true>::MINB, true>;
   k.jtpb = PassCfg<ModelLinear, true>::TPB;
-  k.jptpb = PassCfg<ModelLinear, true>::TPB;
   k.jsplit = PassCfg<ModelLinear, true>::SPLIT;
   k.small = fit_small_kernel<ModelLinear, C, false>;
+  k.batch = fit_batch_kernel<ModelLinear, C, false>;
+  k.batchw = fit_batch_kernel<ModelLinear, C, true>;
   k.smallw = fit_small_kernel<ModelLinear, C, true>;
   k.rtpb = PassCfg<ModelLinear, false>::TPB;
   return k;

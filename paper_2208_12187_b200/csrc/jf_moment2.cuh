@@ -23,7 +23,7 @@
 // chain-rule blocks (apply_chain_kvec) and hands off.
 #pragma once
 
-#include "jf_moment.cuh"
+#include "jf_moment_stream.cuh"
 
 namespace jf {
 
@@ -121,7 +121,7 @@ __host__ __device__ constexpr int moment2_task_smem_bytes(int NW) {
 template <int L, int TC, int NW, bool ROLLED = false>
 __global__ void __launch_bounds__(NW * 32, 1)
     moment2_task_kernel(const PassArgs* __restrict__ pa, FitState* __restrict__ st, cudaGraphConditionalHandle cond,
-                        int use_cond) {
+                        int use_cond, const PassArgs av) {
   using Model = ModelGauss2DRotX2;
   using Pre = typename Model::Pre;
   constexpr int N = Model::N, KT = tri_count(N), KS2 = KT + 1;
@@ -130,8 +130,11 @@ __global__ void __launch_bounds__(NW * 32, 1)
   constexpr int CW = 32 * L;
   constexpr int MAXT = MOMENT2_MAXT;
   constexpr double D = 32.0;
-  const PassArgs& a = *pa;
-  if (!pass_begin<true, false>(a, st)) return;
+  const PassArgs& a = pa ? *pa : av;  // fits: device-resident args (graph replay); else by value
+  if (!pass_begin<true, false>(a, st)) {
+    qr2_dispatch<ModelGauss2DRotX2, COORD_GRID, false, NW * 32>(a, st, cond, use_cond);  // TSQR second pass
+    return;
+  }
   const double* xs = (a.epilogue == EPI_FIT) ? st->x_eval : a.x;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
 
@@ -155,6 +158,11 @@ __global__ void __launch_bounds__(NW * 32, 1)
     A2 = pre.g2.A, a2 = pre.g2.a, b2 = pre.g2.b2, c2 = pre.g2.c, x02 = pre.g2.x0, y02 = pre.g2.y0;
     off = pre.off;
   }
+  if (!moment_form_accurate(a1, b1, c1) || !moment_form_accurate(a2, b2, c2)) {  // (jf_moment_stream.cuh)
+    pass_body_ool<Model, true, COORD_GRID, false, PassCfg<Model, true>::P, TPB, false>(a, st, cond, use_cond);
+    return;
+  }
+
   if (tid == 0) next_task = 0;
   if (tid < 25) {
     const int p = tid / 5, i = tid % 5;

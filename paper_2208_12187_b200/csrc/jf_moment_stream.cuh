@@ -19,12 +19,14 @@
 // Per point (the whole hot loop): u = E from the row recurrence
 // E_{k+1} = E_k R_k, R_{k+1} = R_k rho (2 DMUL), r = A u + off - z (2),
 // u^2, u r (2), the eleven step-index moments (11), sum r, sum r^2 (2):
-// 19 FP64 operations.  Moments run about a moving origin (the lane's first
-// pixel of the current chunk; a Taylor shift per chunk) and are folded with
-// dy^q into the thread's column of a shared-memory table at each row change
-// (reading R34).  A row segment whose exponent range is unsafe for the
-// recurrence (q >= 600 or a step factor beyond e^300 anywhere on it) is
-// evaluated with exp per point instead.
+// 19 FP64 operations.  A chunk's moments are taken about the lane's pixel
+// k = (L-1)/2 of the chunk (compile-time powers of the step index), moved to
+// dx = 0 by a Taylor shift when the chunk ends and added to the row's; the
+// row's are folded with dy^q into the thread's column of a shared-memory
+// table at each row change (reading R34).  A row segment whose exponent range
+// is unsafe for the recurrence (q >= 600 or a step factor beyond e^300
+// anywhere on it) is evaluated with exp per point instead, and a pass whose
+// peak is narrower than MOMENT_MIN_WIDTH runs the dual-number body.
 //
 // Determinism: the chunk -> (warp, lane) map is a function of (m, W, grid),
 // every per-thread sum runs in chunk order, the block partial sums the
@@ -114,28 +116,49 @@ __device__ __forceinline__ void finish_map_row(const PreGauss2D& g, int t, doubl
   for (int i = 0; i < FMAP_COLS; ++i) row[i] = out[i];
 }
 
-// dynamic shared memory: the per-thread folded-moment table [KS][TPB + 1]
-__host__ __device__ constexpr int moment_stream_smem_bytes(int NW) {
-  return MomLayout::KS * (NW * 32 + 1) * 8;
+// Where the moment form keeps the pass's accuracy.  Its two regroupings
+// cancel for some peak shapes: the chunk-to-row Taylor shift when the peak is
+// narrow (amplification ~ (256 px / w)^4, w the smallest principal width
+// sqrt(1 / (2 lambda_max)) of the quadratic form [[a, b], [b, c2]]), and the
+// chain-rule map T^T (moment Gram) T when it is elongated (the columns
+// -A u (dx^2, dx dy, dy^2) become nearly dependent; ~ aspect^4).  Outside
+// (w < 48 px or aspect > 12) the pass runs the dual-number body, whose
+// per-point rank-1 update does not cancel.
+constexpr double MOMENT_MIN_WIDTH = 48.0, MOMENT_MAX_ASPECT = 12.0;
+__device__ __forceinline__ bool moment_form_accurate(double a, double b2, double c) {
+  const double hb = 0.5 * b2, hd = 0.5 * (a - c);
+  const double rt = sqrt(fma(hd, hd, hb * hb));
+  const double lmax = 0.5 * (a + c) + rt, lmin = 0.5 * (a + c) - rt;
+  return 2.0 * lmax * MOMENT_MIN_WIDTH * MOMENT_MIN_WIDTH <= 1.0 &&
+         lmax <= MOMENT_MAX_ASPECT * MOMENT_MAX_ASPECT * lmin;
 }
 
-template <int L, int NW, int SEEDN>
+// dynamic shared memory: the per-thread folded-moment table [KS][TPB + 1]
+// followed by the per-thread row moments [11][TPB + 1]
+__host__ __device__ constexpr int moment_stream_smem_bytes(int NW) {
+  return (MomLayout::KS + 11) * (NW * 32 + 1) * 8;  // + the row moments (11 per thread)
+}
+
+template <int L, int NW, int SEEDN, int FALLBACK = 1>
 __global__ void __launch_bounds__(NW * 32, 1)
     moment_stream_kernel(const PassArgs* __restrict__ pa, FitState* __restrict__ st, cudaGraphConditionalHandle cond,
-                         int use_cond) {
+                         int use_cond, const PassArgs av) {
   using Model = ModelGauss2DRot;
   constexpr int N = Model::N, KT = tri_count(N), KS2 = KT + 1;
   constexpr int TPB = NW * 32;
   constexpr int KS = MomLayout::KS, NV = MomLayout::NV, NF = MomLayout::OSR;
   constexpr int CW = 32 * L;
   constexpr double D = 32.0;
-  const PassArgs& a = *pa;
-  if (!pass_begin<true, false>(a, st)) return;
+  const PassArgs& a = pa ? *pa : av;  // fits: device-resident args (graph replay); else by value
+  if (!pass_begin<true, false>(a, st)) {
+    if constexpr (FALLBACK != 0) qr2_dispatch<Model, COORD_GRID, false, NW * 32>(a, st, cond, use_cond);  // TSQR second pass
+    return;
+  }
   const double* xs = (a.epilogue == EPI_FIT) ? st->x_eval : a.x;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  // development aid (JF_DEBUG_STAMPS): per-warp globaltimer stamps
+  // development builds only (JF_DEV): per-warp globaltimer stamps (tools/stamps2.py)
   auto stamp = [&](int slot) {
-    if (a.dbg && lane == 0 && blockIdx.x * NW + wid < 8000) {
+    if (JF_DEV && a.dbg && lane == 0 && blockIdx.x * NW + wid < 8000) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       a.dbg[(blockIdx.x * NW + wid) * 8 + slot] = t;
@@ -165,6 +188,10 @@ __global__ void __launch_bounds__(NW * 32, 1)
     A = pre.g.A, off = pre.off, ga = pre.g.a, gb2 = pre.g.b2, gc = pre.g.c, x0 = pre.g.x0, y0 = pre.g.y0;
     if (tid == 0) spre = pre.g;
   }
+  if (FALLBACK != 0 && !moment_form_accurate(ga, gb2, gc)) {
+    pass_body_ool<Model, true, COORD_GRID, false, PassCfg<Model, true>::P, TPB, false>(a, st, cond, use_cond);
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < NF; ++i) col(i) = 0.0;
   stamp(2);
@@ -180,58 +207,81 @@ __global__ void __launch_bounds__(NW * 32, 1)
   const double rho = exp(-2.0 * ga * D * D);
   const double* __restrict__ z = a.z;
 
-  double P[5], Q[3], R[3];
+  // Moments of the current chunk about the lane's chunk origin o_c (its
+  // pixel k = KC: t = D (k - KC), compile-time), and of the current row about
+  // dx = 0 (each chunk folded in by a Taylor shift when it ends).  Keeping the
+  // chunk moments local bounds the shift's cancellation by (|t| + |o_c|) / w
+  // over the chunk that holds the mass (w: the peak's width along the row):
+  // the origin never travels along the row with accumulated mass.
+  constexpr int KC = (L - 1) / 2;
+  constexpr int NR = 11;  // row moments: RP[0..4], RQ[0..2], RR[0..2] (shared-memory column, per thread)
+  double P[5], Q[3], R[3];  // chunk, about o_c
 #pragma unroll
   for (int i = 0; i < 5; ++i) P[i] = 0.0;
 #pragma unroll
   for (int i = 0; i < 3; ++i) Q[i] = R[i] = 0.0;
+  auto rowm = [&](int i) -> double& { return dyn_stream[(KS + i) * (TPB + 1) + tid]; };
+#pragma unroll
+  for (int i = 0; i < NR; ++i) rowm(i) = 0.0;
   double sr = 0.0, srr = 0.0;
   int bad = 0;
 
-  // moments about o -> about o - d (Pascal scheme)
-  auto shift = [&](double d) {
+  // the chunk's moments about o_c -> about dx = 0 (Pascal scheme: t -> t + o_c),
+  // added to the row's; the chunk's moments restart from zero
+  auto chunk_fold = [&](double oc) {
 #pragma unroll
     for (int j = 1; j <= 4; ++j)
 #pragma unroll
-      for (int p = 4; p >= j; --p) P[p] = fma(d, P[p - 1], P[p]);
+      for (int p = 4; p >= j; --p) P[p] = fma(oc, P[p - 1], P[p]);
 #pragma unroll
     for (int j = 1; j <= 2; ++j)
 #pragma unroll
       for (int p = 2; p >= j; --p) {
-        Q[p] = fma(d, Q[p - 1], Q[p]);
-        R[p] = fma(d, R[p - 1], R[p]);
+        Q[p] = fma(oc, Q[p - 1], Q[p]);
+        R[p] = fma(oc, R[p - 1], R[p]);
       }
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+      rowm(i) += P[i];
+      P[i] = 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      rowm(5 + i) += Q[i];
+      rowm(8 + i) += R[i];
+      Q[i] = R[i] = 0.0;
+    }
   };
-  double org = 0.0;  // dx of the origin of the running row moments
-  // row moments (about dx = org) -> about dx = 0, times dy^q, into the thread's column
+  // row moments (about dx = 0) times dy^q into the thread's column
   auto fold = [&](double dy) {
-    shift(org);
     double dq[5];
     dq[0] = 1.0;
     dq[1] = dy;
     dq[2] = dy * dy;
     dq[3] = dq[2] * dy;
     dq[4] = dq[2] * dq[2];
+    double rp[NR];
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+      rp[i] = rowm(i);
+      rowm(i) = 0.0;
+    }
 #pragma unroll
     for (int q = 0; q <= 4; ++q)
 #pragma unroll
       for (int p = 0; p + q <= 4; ++p) {
         double& m2 = col(MomLayout::O2 + mono(4, p, q));
-        m2 = fma(P[p], dq[q], m2);
+        m2 = fma(rp[p], dq[q], m2);
       }
 #pragma unroll
     for (int q = 0; q <= 2; ++q)
 #pragma unroll
       for (int p = 0; p + q <= 2; ++p) {
         double& m1 = col(MomLayout::O1 + mono(2, p, q));
-        m1 = fma(Q[p], dq[q], m1);
+        m1 = fma(rp[5 + p], dq[q], m1);
         double& mr = col(MomLayout::OR + mono(2, p, q));
-        mr = fma(R[p], dq[q], mr);
+        mr = fma(rp[8 + p], dq[q], mr);
       }
-#pragma unroll
-    for (int i = 0; i < 5; ++i) P[i] = 0.0;
-#pragma unroll
-    for (int i = 0; i < 3; ++i) Q[i] = R[i] = 0.0;
   };
 
   // position of the chunk being processed (advanced incrementally)
@@ -292,8 +342,6 @@ __global__ void __launch_bounds__(NW * 32, 1)
     }
     const int c0 = cc * CW;
     const double dx0 = (double)(c0 + lane) - x0;
-    shift(-(double)CW);  // origin -> this chunk's first pixel (zero moments at a row start)
-    org = dx0;
     if (row_fast && c0 + CW <= W) {  // warp-uniform
       if (!carried || ++since_seed >= SEEDN) {
         const double q0 = dx0 * (ga * dx0 + gb2 * dy) + gc * (dy * dy);
@@ -310,12 +358,12 @@ __global__ void __launch_bounds__(NW * 32, 1)
         const double u = E;
         const double r = fma(A, u, off) - zc[k];  // Eq. 1: r = h - z
         const double u2 = u * u;
-        const double k1 = D * k, k2 = k1 * k1, k3 = k2 * k1, k4 = k2 * k2;
+        const double k1 = D * (k - KC), k2 = k1 * k1, k3 = k2 * k1, k4 = k2 * k2;
         const double ur = u * r;
         P[0] += u2;
         Q[0] += u;
         R[0] += ur;
-        if (k > 0) {
+        if (k != KC) {
           P[1] = fma(u2, k1, P[1]);
           P[2] = fma(u2, k2, P[2]);
           P[3] = fma(u2, k3, P[3]);
@@ -350,7 +398,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
           const double u = exp(-(dx * (ga * dx + gb2 * dy) + gc * (dy * dy)));
           const double r = fma(A, u, off) - zc[k];
           bad += isfinite(r) ? 0 : 1;
-          const double u2 = u * u, t = D * k, t2 = t * t, ur = u * r;
+          const double u2 = u * u, t = D * (k - KC), t2 = t * t, ur = u * r;
           P[0] += u2;
           P[1] = fma(u2, t, P[1]);
           P[2] = fma(u2, t2, P[2]);
@@ -367,6 +415,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
         }
       }
     }
+    chunk_fold(dx0 + D * KC);
   };
 
   {

@@ -26,6 +26,8 @@
 // condition — so a whole fit is one graph launch.
 #pragma once
 
+#include <cstdio>
+
 #include "jf_common.cuh"
 #include "jf_dual.cuh"
 #include "jf_models.cuh"
@@ -62,10 +64,18 @@ struct Part {
 // parameter whose partial is identically 1 (the offset); unweighted, its
 // diagonal slot is the point count, kept as an integer (cnt).  The non-finite
 // count is kept by the part that starts at row 0.
-template <class Model, bool JAC, int RL, int RH, bool PREC = false, class H>
+//
+// Rotated Gaussians (Model::NT > 0): the dual numbers give the row in the
+// alternative coordinates (a, 2b, c2) of each quadratic form; the chain-rule
+// block T (R33) maps it to (sx, sy, th) here, per point, before the rank-1
+// update (chain = true; false: the alt-coordinate Gram, JF_FLAG_ALT_COORDS).
+// Per point, not on the reduced Gram: for an elongated peak the alt columns
+// -A u (dx^2, dx dy, dy^2) are nearly dependent and T^T (W_alt^T W_alt) T
+// would cancel catastrophically.
+template <class Model, bool JAC, int RL, int RH, bool PREC = false, class H, class Pre>
 __device__ __forceinline__ void accumulate(double (&acc)[Part<Model, JAC, RL, RH>::K], int& bad, int& cnt,
                                            const H& h, double z, double wsig, bool weighted,
-                                           const double* __restrict__ prec = nullptr) {
+                                           const double* __restrict__ prec, const Pre& pre, bool chain) {
   constexpr int N = Model::N;
   if constexpr (JAC) {
     constexpr int CC = Model::CONST_COL;
@@ -81,6 +91,18 @@ __device__ __forceinline__ void accumulate(double (&acc)[Part<Model, JAC, RL, RH
     }
     if constexpr (RL == 0) bad += isfinite(w[N]) ? 0 : 1;
     ++cnt;
+    if constexpr (!PREC && Model::NT > 0) {
+      if (chain) {
+#pragma unroll
+        for (int g = 0; g < Model::NT; ++g) {
+          const int b = Model::tbase(g);
+          const double* T = Model::tblock(pre, g);
+          const double u0 = w[b], u1 = w[b + 1], u2 = w[b + 2];
+#pragma unroll
+          for (int q = 0; q < 3; ++q) w[b + q] = fma(u0, T[q], fma(u1, T[3 + q], u2 * T[6 + q]));
+        }
+      }
+    }
     if constexpr (PREC) {
       // TSQR (CholeskyQR2) second pass: the row of W P, P = R1^-1 upper
       // triangular ((n+1) x (n+1), shared memory), so the accumulated Gram is
@@ -166,7 +188,7 @@ __device__ __forceinline__ void block_partial_part(double (&acc)[Part<Model, JAC
     double s = 0.0;
 #pragma unroll
     for (int w = 0; w < NW; ++w) s += red[w][k];
-    part[(size_t)blockIdx.x * (KT + 1) + k] = s;
+    part[k] = s;  // the caller passes this block's row
   }
 }
 
@@ -229,11 +251,20 @@ __host__ __device__ constexpr int combine_scratch(int tpb) { return tpb; }
 // Tickets: a.ticket[0] (groups), a.ticket[1 + g] (blocks of group g); each
 // is reset by its last user, ready for the next launch.
 constexpr int GROUP = 16;
-// development aid (JF_DEBUG_STAMPS): timestamps of the last block's tail phases
+// Development builds only (JF_DEV=1 python -m paper_2208_12187_b200.build):
+// timestamps of the last block's tail phases for tools/stamps2.py.
+#ifndef JF_DEV
+#define JF_DEV 0
+#endif
 __device__ __forceinline__ void dbg_tail(const PassArgs& a, int i) {
+#if JF_DEV
   if (a.dbg && threadIdx.x == 0) {
     a.dbg[4 * 16384 - 16 + i] = clock64();  // SM cycles (all tail stamps are on the last block's SM)
   }
+#else
+  (void)a;
+  (void)i;
+#endif
 }
 template <int KS, int TPB>
 __device__ __forceinline__ bool grid_reduce(const PassArgs& a, double* out, double* scratch /* TPB doubles */) {
@@ -377,7 +408,7 @@ __device__ __forceinline__ bool comm_combine(const CommDev& cm, unsigned long lo
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     while (*f < epoch) {
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-      if (t1 - t0 > 20000000000ull) {  // 20 s: a peer is gone
+      if (t1 - t0 > cm.timeout_ns) {  // a peer is gone (jf_comm_set_timeout)
         timed_out = 1;
         break;
       }
@@ -385,6 +416,13 @@ __device__ __forceinline__ bool comm_combine(const CommDev& cm, unsigned long lo
   }
   __threadfence_system();
   __syncthreads();
+#if JF_DEV
+  if (timed_out && threadIdx.x == 0) {
+    printf("comm timeout: rank %d epoch %llu flags:", me, epoch);
+    for (int p = 0; p < R; ++p) printf(" %llu", *(volatile unsigned long long*)(cm.mbox_flag[me] + p));
+    printf("\n");
+  }
+#endif
   if (timed_out) return false;
   // 4. sum in rank order (identical on every rank)
   const double* box = cm.mbox_data[me] + (size_t)par * R * KMAX;
@@ -510,7 +548,7 @@ __device__ __forceinline__ void grid_recur_loop(const PassArgs& a, const auto& p
       for (int k = 0; k < L; ++k) {
         const double X = X0 + 32.0 * k;
         const auto h = Model::template point_e<JAC>(pre, X, Y, E);
-        accumulate<Model, JAC, RL, RH, PREC>(acc, bad, cnt, h, zc[k], WGT ? wc[k] : 1.0, WGT, prec);
+        accumulate<Model, JAC, RL, RH, PREC>(acc, bad, cnt, h, zc[k], WGT ? wc[k] : 1.0, WGT, prec, pre, !a.no_chain);
 #pragma unroll
         for (int g = 0; g < NE; ++g) {
           E[g] *= R[g];
@@ -524,7 +562,7 @@ __device__ __forceinline__ void grid_recur_loop(const PassArgs& a, const auto& p
         if (col0 + 32 * k < W) {
           const double X = X0 + 32.0 * k;
           const auto h = Model::template point<JAC>(pre, X, Y);
-          accumulate<Model, JAC, RL, RH, PREC>(acc, bad, cnt, h, zc[k], WGT ? wc[k] : 1.0, WGT, prec);
+          accumulate<Model, JAC, RL, RH, PREC>(acc, bad, cnt, h, zc[k], WGT ? wc[k] : 1.0, WGT, prec, pre, !a.no_chain);
         }
       }
     }
@@ -599,10 +637,10 @@ __device__ __forceinline__ void run_part(const PassArgs& a, const Pre& pre, int 
   auto eval = [&](double X, double Y, double zz, double ww) {
     if constexpr (TWO) {
       const auto h = Model::template point<JAC>(pre, X, Y);
-      accumulate<Model, JAC, RL, RH, PREC>(acc, bad, cnt, h, zz, ww, weighted, prec);
+      accumulate<Model, JAC, RL, RH, PREC>(acc, bad, cnt, h, zz, ww, weighted, prec, pre, !a.no_chain);
     } else {
       const auto h = Model::template point<JAC>(pre, X);
-      accumulate<Model, JAC, RL, RH, PREC>(acc, bad, cnt, h, zz, ww, weighted, prec);
+      accumulate<Model, JAC, RL, RH, PREC>(acc, bad, cnt, h, zz, ww, weighted, prec, pre, !a.no_chain);
     }
   };
   // main loop: full groups of P points, straight-line (no per-point predicate)
@@ -716,19 +754,13 @@ __device__ __forceinline__ void pass_tail(const PassArgs& a, FitState* __restric
   }
 }
 
-// The pass kernel.  epilogue == EPI_FIT: one pass of a fit (st is the state).
-template <class Model, bool JAC, int COORD, bool WGT, int P = PassCfg<Model, JAC>::P,
-          int TPB = PassCfg<Model, JAC>::TPB, int MINB = PassCfg<Model, JAC>::MINB, bool PREC = false>
-__global__ void __launch_bounds__(TPB, MINB)
-    pass_kernel(const PassArgs* __restrict__ pa, FitState* __restrict__ st, cudaGraphConditionalHandle cond,
-                int use_cond) {
-  (void)cond;
-  (void)use_cond;
+// The body of a pass (everything after pass_begin).  PREC: the TSQR
+// (CholeskyQR2) second pass, rows of W multiplied by P = R1^-1.
+template <class Model, bool JAC, int COORD, bool WGT, int P, int TPB, bool PREC>
+__device__ __forceinline__ void pass_body(const PassArgs& a, FitState* __restrict__ st,
+                                          cudaGraphConditionalHandle cond, int use_cond) {
   using Sh = PassShape<Model, JAC>;
   constexpr int KT = Sh::KT, KS = Sh::KS;
-  const PassArgs& a = *pa;
-
-  if (!pass_begin<JAC, PREC>(a, st)) return;
   const double* xs = (a.epilogue == EPI_FIT) ? st->x_eval : a.x;
   double xv[Model::N];
 #pragma unroll
@@ -741,7 +773,7 @@ __global__ void __launch_bounds__(TPB, MINB)
   if constexpr (PREC) {
     constexpr int N1 = Model::N + 1;
     const double* src = (a.epilogue == EPI_FIT) ? st->prec : a.precond;
-    for (int k = threadIdx.x; k < N1 * N1; k += TPB) prec_s[k] = src[k];
+    for (int k = threadIdx.x; k < N1 * N1; k += TPB) prec_s[k] = __ldcg(src + k);
     if (threadIdx.x == 0) {
       for (int g = 0; g < Model::NT; ++g)
         for (int q = 0; q < 9; ++q) prec_s[N1 * N1 + 9 * g + q] = Model::tblock(pre, g)[q];
@@ -758,19 +790,50 @@ __global__ void __launch_bounds__(TPB, MINB)
     // split triangle: rows [0, 4) by the first half of the grid, [4, n+1) by the second
     const int half = gridDim.x / 2;
     if ((int)blockIdx.x < half) {
-      run_part<Model, JAC, COORD, WGT, P, TPB, 0, 4, PREC>(a, pre, blockIdx.x, half, red, a.partials, prec);
+      run_part<Model, JAC, COORD, WGT, P, TPB, 0, 4, PREC>(a, pre, blockIdx.x, half, red, a.partials + (size_t)blockIdx.x * KS, prec);
     } else {
-      run_part<Model, JAC, COORD, WGT, P, TPB, 4, NP1, PREC>(a, pre, blockIdx.x - half, gridDim.x - half, red, a.partials, prec);
+      run_part<Model, JAC, COORD, WGT, P, TPB, 4, NP1, PREC>(a, pre, blockIdx.x - half, gridDim.x - half, red,
+                                                            a.partials + (size_t)blockIdx.x * KS, prec);
     }
   } else {
-    run_part<Model, JAC, COORD, WGT, P, TPB, 0, (JAC ? NP1 : 1), PREC>(a, pre, blockIdx.x, gridDim.x, red, a.partials, prec);
+    run_part<Model, JAC, COORD, WGT, P, TPB, 0, (JAC ? NP1 : 1), PREC>(a, pre, blockIdx.x, gridDim.x, red,
+                                                                       a.partials + (size_t)blockIdx.x * KS, prec);
   }
   if (!grid_reduce<KS, TPB>(a, vec, scratch)) return;
-  if constexpr (JAC && Model::NT > 0 && !PREC) {
-    if (!a.no_chain) apply_chain_kvec<Model, TPB>(pre, vec, scratch);
-  }
 
   pass_tail<KS, TPB, JAC>(a, st, vec, cond, use_cond);
+}
+
+// The same body out of line: a fallback inside another kernel (the moment
+// kernels) keeps its registers out of the caller's hot loop.
+template <class Model, bool JAC, int COORD, bool WGT, int P, int TPB, bool PREC>
+__device__ __noinline__ void pass_body_ool(const PassArgs& a, FitState* __restrict__ st,
+                                           cudaGraphConditionalHandle cond, int use_cond) {
+  pass_body<Model, JAC, COORD, WGT, P, TPB, PREC>(a, st, cond, use_cond);
+}
+
+// In a fit, a J-pass kernel also serves the TSQR second pass (phase PH_QR2):
+// the graph needs no separate node (and no empty launch per trial) for it.
+template <class Model, int COORD, bool WGT, int TPB>
+__device__ __forceinline__ bool qr2_dispatch(const PassArgs& a, FitState* __restrict__ st,
+                                             cudaGraphConditionalHandle cond, int use_cond) {
+  if (a.epilogue != EPI_FIT || st->phase != PH_QR2) return false;
+  pass_body_ool<Model, true, COORD, WGT, PassCfg<Model, true>::P, TPB, true>(a, st, cond, use_cond);
+  return true;
+}
+
+// The pass kernel.  epilogue == EPI_FIT: one pass of a fit (st is the state).
+template <class Model, bool JAC, int COORD, bool WGT, int P = PassCfg<Model, JAC>::P,
+          int TPB = PassCfg<Model, JAC>::TPB, int MINB = PassCfg<Model, JAC>::MINB, bool PREC = false>
+__global__ void __launch_bounds__(TPB, MINB)
+    pass_kernel(const PassArgs* __restrict__ pa, FitState* __restrict__ st, cudaGraphConditionalHandle cond,
+                int use_cond, const PassArgs av) {
+  const PassArgs& a = pa ? *pa : av;  // fits: device-resident args (graph replay); else by value
+  if (!pass_begin<JAC, PREC>(a, st)) {
+    if constexpr (JAC && !PREC) qr2_dispatch<Model, COORD, WGT, TPB>(a, st, cond, use_cond);
+    return;
+  }
+  pass_body<Model, JAC, COORD, WGT, P, TPB, PREC>(a, st, cond, use_cond);
 }
 
 // ---------------------------------------------------------------- small m
@@ -790,6 +853,7 @@ __global__ void __launch_bounds__(256, 1) fit_small_kernel(const PassArgs* __res
   __shared__ SolverSmem S;
   __shared__ double red[TPB / 32][KT + 1];
   __shared__ double kvec[KT + 1];
+  __shared__ double prec_s[NP1 * NP1 + 9 * Model::NT + 1];  // TSQR second pass: P = R1^-1 and the chain blocks
   const PassArgs& a = *pa;
   {
     constexpr int NW = sizeof(FitState) / 8;
@@ -806,11 +870,18 @@ __global__ void __launch_bounds__(256, 1) fit_small_kernel(const PassArgs* __res
 #pragma unroll
     for (int j = 0; j < Model::N; ++j) xv[j] = st.x_eval[j];
     const auto pre = Model::template prologue<true>(xv);
-    run_part<Model, true, COORD, WGT, P, TPB, 0, NP1, false>(a, pre, 0, 1, red, kvec, nullptr);
-    __syncthreads();
-    if constexpr (Model::NT > 0) {
-      __shared__ double ctmp[KT];
-      apply_chain_kvec<Model, TPB>(pre, kvec, ctmp);
+    if (st.phase == PH_QR2) {  // TSQR (CholeskyQR2): the preconditioned pass at x (solver AUTO / TSQR)
+      for (int k = threadIdx.x; k < NP1 * NP1; k += TPB) prec_s[k] = __ldcg(st.prec + k);  // written by lane 0 this launch
+      if (threadIdx.x == 0) {
+        for (int g = 0; g < Model::NT; ++g)
+          for (int q = 0; q < 9; ++q) prec_s[NP1 * NP1 + 9 * g + q] = Model::tblock(pre, g)[q];
+      }
+      __syncthreads();
+      run_part<Model, true, COORD, WGT, P, TPB, 0, NP1, true>(a, pre, 0, 1, red, kvec, prec_s);
+      __syncthreads();
+    } else {
+      run_part<Model, true, COORD, WGT, P, TPB, 0, NP1, false>(a, pre, 0, 1, red, kvec, nullptr);
+      __syncthreads();
     }
     if (threadIdx.x < 32) solver_step<Model::N>(&st, S, kvec, true);
   }
@@ -820,6 +891,112 @@ __global__ void __launch_bounds__(256, 1) fit_small_kernel(const PassArgs* __res
     const unsigned long long* src = reinterpret_cast<const unsigned long long*>(&st);
     unsigned long long* dst = reinterpret_cast<unsigned long long*>(gst);
     for (int k = threadIdx.x; k < NW; k += TPB) dst[k] = src[k];
+  }
+}
+
+// ------------------------------------------------------ batched small fits
+// Many independent fits in ONE launch (Gpufit's regime, P:260/P:267 — "runs
+// entirely in CUDA"): each block is one warp and runs whole fits, one after
+// another (block b: fits b, b + grid, ...), with the fit state and the
+// subproblem workspace in shared memory.  Per fit: the initial point
+// (caller's p0 or curve_fit's default, strictly feasible when bounded), then
+// [J-pass over the fit's m points by the warp -> solver step] until the state
+// machine ends the fit; the result is written per fit.  The same pass body
+// (run_part) and solver step (solver_step) as every other path.
+template <class Model, int COORD, bool WGT>
+__global__ void __launch_bounds__(32, 8) fit_batch_kernel(const BatchArgs ba) {
+  constexpr int TPB = 32;
+  constexpr int N = Model::N;
+  constexpr int KT = PassShape<Model, true>::KT;
+  constexpr int NP1 = N + 1;
+  constexpr int P = (N <= 4) ? 2 : 1;
+  __shared__ FitState st;
+  __shared__ SolverSmem S;
+  __shared__ PassArgs a;
+  __shared__ double red[1][KT + 1];
+  __shared__ double kvec[KT + 1];
+  __shared__ double prec_s[NP1 * NP1 + 9 * Model::NT + 1];
+  __shared__ int skip;
+  const int lane = threadIdx.x;
+  const int64_t nfits = ba.nfits;
+  for (int64_t f = blockIdx.x; f < nfits; f += gridDim.x) {
+    {  // the shared configuration, then this fit's initial point and data
+      constexpr int NW = sizeof(FitState) / 8;
+      const unsigned long long* src = reinterpret_cast<const unsigned long long*>(ba.tmpl);
+      unsigned long long* dst = reinterpret_cast<unsigned long long*>(&st);
+      for (int k = lane; k < NW; k += TPB) dst[k] = __ldg(src + k);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      a = ba.base;
+      a.z = ba.base.z + f * ba.z_stride;
+      if (ba.base.wsig) a.wsig = ba.base.wsig + f * ba.z_stride;
+      if (ba.base.y0) a.y0 = ba.base.y0 + f * ba.y_stride;
+      if (ba.base.y1) a.y1 = ba.base.y1 + f * ba.y_stride;
+      int bad = 0;
+      for (int j = 0; j < N; ++j) {
+        const double lo = st.lb[j], hi = st.ub[j];
+        double x0;
+        if (ba.p0) {
+          x0 = ba.p0[f * N + j];
+        } else {  // curve_fit's default initial guess
+          const bool lf = isfinite(lo), uf = isfinite(hi);
+          x0 = (lf && uf) ? 0.5 * (lo + hi) : (lf ? lo + 1.0 : (uf ? hi - 1.0 : 1.0));
+        }
+        if (!isfinite(x0)) bad = -1;
+        else if (x0 < lo || x0 > hi) bad = bad ? bad : -2;  // R18: p0 outside the bounds
+        if (st.bounded) x0 = strict_feasible_r(x0, lo, hi, 1e-10);
+        st.x[j] = x0;
+        st.x_eval[j] = x0;
+      }
+      st.qr = ba.qr + blockIdx.x;
+      st.prec = st.qr->prec;
+      skip = bad;
+    }
+    __syncwarp();
+    if (skip) {
+      if (lane == 0) {
+        BatchResult& o = ba.out[f];
+        for (int j = 0; j < NMAX; ++j) o.x[j] = j < N ? st.x[j] : 0.0;
+        o.cost = o.optimality = 0.0;
+        o.status = skip;
+        o.nfev = o.njev = o.nit = 0;
+      }
+      __syncwarp();
+      continue;
+    }
+    for (int iter = 0; iter < 4 * st.max_nfev + 8 && st.cont; ++iter) {
+      double xv[N];
+#pragma unroll
+      for (int j = 0; j < N; ++j) xv[j] = st.x_eval[j];
+      const auto pre = Model::template prologue<true>(xv);
+      if (st.phase == PH_QR2) {  // TSQR (CholeskyQR2) second pass (solver AUTO / TSQR)
+        for (int k = lane; k < NP1 * NP1; k += TPB) prec_s[k] = __ldcg(st.prec + k);
+        if (lane == 0) {
+          for (int g = 0; g < Model::NT; ++g)
+            for (int q = 0; q < 9; ++q) prec_s[NP1 * NP1 + 9 * g + q] = Model::tblock(pre, g)[q];
+        }
+        __syncwarp();
+        run_part<Model, true, COORD, WGT, P, TPB, 0, NP1, true>(a, pre, 0, 1, red, kvec, prec_s);
+        __syncwarp();
+      } else {
+        run_part<Model, true, COORD, WGT, P, TPB, 0, NP1, false>(a, pre, 0, 1, red, kvec, nullptr);
+        __syncwarp();
+      }
+      solver_step<N>(&st, S, kvec, true);
+      __syncwarp();
+    }
+    if (lane == 0) {
+      BatchResult& o = ba.out[f];
+      for (int j = 0; j < NMAX; ++j) o.x[j] = j < N ? st.x[j] : 0.0;
+      o.cost = st.cost;
+      o.optimality = st.gnorm;
+      o.status = st.error ? st.error : (st.cont ? -4 : st.status);
+      o.nfev = st.nfev;
+      o.njev = st.njev;
+      o.nit = st.nit;
+    }
+    __syncwarp();
   }
 }
 

@@ -87,4 +87,44 @@ int launch_tr_step(const double* hatG, const double* hatg, int n, int64_t m, dou
   return cudaGetLastError() == cudaSuccess ? 0 : -4;
 }
 
+// The Coleman-Li step selection alone (jf_select_step, parity hook): lane 0
+// runs select_step<n> on the scaled quadratic model B_hat (incl. diag_h).
+__global__ void select_step_kernel(const double* in, int n, double Delta, double theta, double* out) {
+  __shared__ SolverSmem S;
+  // in: B_hat (n*n) | g_hat | x | lb | ub | d | p_h   (n each)
+  const int lane = threadIdx.x;
+  for (int e = lane; e < n * n; e += 32) S.M[e / n][e % n] = in[e];
+  __syncwarp();
+  if (lane == 0) {
+    const double* gh = in + n * n;
+    const double* x = gh + n;
+    const double* lb = x + n;
+    const double* ub = lb + n;
+    const double* d = ub + n;
+    const double* ph = d + n;
+    double step[NMAX], step_h[NMAX], pred = 0.0;
+    int branch = -1;
+    switch (n) {
+#define JF_SEL_CASE(N) \
+  case N: select_step<N>(S, x, lb, ub, gh, d, ph, Delta, theta, step, step_h, pred, branch); break;
+      JF_SEL_CASE(1) JF_SEL_CASE(2) JF_SEL_CASE(3) JF_SEL_CASE(4) JF_SEL_CASE(5) JF_SEL_CASE(6) JF_SEL_CASE(7)
+      JF_SEL_CASE(8) JF_SEL_CASE(9) JF_SEL_CASE(10) JF_SEL_CASE(11) JF_SEL_CASE(12) JF_SEL_CASE(13)
+      JF_SEL_CASE(14) JF_SEL_CASE(15) JF_SEL_CASE(16)
+#undef JF_SEL_CASE
+      default: break;
+    }
+    for (int j = 0; j < n; ++j) {
+      out[j] = step[j];
+      out[NMAX + j] = step_h[j];
+    }
+    out[2 * NMAX] = pred;
+    out[2 * NMAX + 1] = branch;
+  }
+}
+
+int launch_select_step(const double* in, int n, double Delta, double theta, double* out, cudaStream_t s) {
+  select_step_kernel<<<1, 32, 0, s>>>(in, n, Delta, theta, out);
+  return cudaGetLastError() == cudaSuccess ? 0 : -4;
+}
+
 }  // namespace jf

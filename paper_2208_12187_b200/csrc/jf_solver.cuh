@@ -508,9 +508,11 @@ __device__ __forceinline__ double inv_fro2(const double (&L)[n][n], const double
 }
 
 template <int n>
-__device__ __noinline__ int gn_fastpath(SolverSmem& S, int64_t m, const double* gh, double Delta, double* p) {
+__device__ __noinline__ int gn_fastpath(SolverSmem& S, int64_t m, const double* gh, double Delta, double* p,
+                                        double& kappa2) {
   double L[n][n], Y[n][n], cinv[n];
   double tr = 0.0;
+  kappa2 = INFINITY;
 #pragma unroll
   for (int i = 0; i < n; ++i) {
 #pragma unroll
@@ -519,6 +521,7 @@ __device__ __noinline__ int gn_fastpath(SolverSmem& S, int64_t m, const double* 
   }
   if (!chol_reg<n>(L, cinv)) return 0;
   const double fro = inv_fro2<n>(L, cinv, Y);
+  kappa2 = tr * fro;  // >= cond(B_hat) (lambda_max <= tr, lambda_min >= 1 / ||L^-1||_F^2)
   if (!(m >= n && rsqrt(fro) > 2.0 * DBL_EPSILON * (double)m * sqrt(tr))) return 0;
   double w[n], pr[n];
 #pragma unroll
@@ -707,6 +710,19 @@ __device__ __forceinline__ double strict_feasible0(double x, double lb, double u
   return xn;
 }
 
+// strict feasibility with rstep > 0 (R18/R19: the bounded start): an active
+// bound (within rstep max(1, |bound|)) moves to bound +- that; still outside
+// -> midpoint.
+__device__ __forceinline__ double strict_feasible_r(double x, double lb, double ub, double rstep) {
+  double xn = x;
+  const double ld = x - lb, ud = ub - x;
+  const double lt = rstep * fmax(1.0, fabs(lb)), ut = rstep * fmax(1.0, fabs(ub));
+  if (isfinite(lb) && ld <= fmin(ud, lt)) xn = lb + lt;
+  else if (isfinite(ub) && ud <= fmin(ld, ut)) xn = ub - ut;
+  if (xn < lb || xn > ub) xn = 0.5 * (lb + ub);
+  return xn;
+}
+
 // Coleman-Li vector v, dv (R19)
 __device__ __forceinline__ void cl_vector(double x, double g, double lb, double ub, double& v, double& dv) {
   v = 1.0;
@@ -793,7 +809,9 @@ __device__ __noinline__ void st_trial_begin(FitState* st, SolverSmem& S, bool ha
     S.need_eig = 1;  // TSQR: the SVD of R_hat, no Cholesky shortcut
   } else if (!st->have_eig) {
     const long long c0 = clock64();
-    S.fast = gn_fastpath<n>(S, st->m_global, st->gh, st->Delta, S.w3);
+    double k2;
+    S.fast = gn_fastpath<n>(S, st->m_global, st->gh, st->Delta, S.w3, k2);
+    st->kappa2_gn = k2;
     st->prof[1] += clock64() - c0;
     if (!S.fast) S.need_eig = 1;
   }
@@ -1000,6 +1018,16 @@ __device__ __forceinline__ double kappa2_estimate(FitState* st, SolverSmem& S) {
   return tr * inv_fro2<n>(L, cinv, Y);
 }
 
+// AUTO along the trajectory: at an accepted step of a Gram-mode fit whose last
+// Gauss-Newton Cholesky bounded cond(B_hat)^2 above 1e6 (or failed), the
+// column-scaled Gram at the new x decides whether the fit continues in TSQR
+// mode (the same test as at x0; a cheap trigger keeps it off the common path).
+template <int n>
+__device__ __forceinline__ void st_auto_recheck(FitState* st, SolverSmem& S) {
+  if (st->auto_mode && !st->qr_mode && !(st->kappa2_gn <= 1.0e6) && kappa2_estimate<n>(st, S) > 1.0e6)
+    st->qr_mode = 1;
+}
+
 // Initialisation after the J-pass at x0 (Alg. 1 l.137-138; R3, R4, R18).
 template <int n>
 __device__ __noinline__ void st_init_finish(FitState* st, SolverSmem& S) {
@@ -1062,6 +1090,7 @@ __device__ __noinline__ void st_end_inner(FitState* st, SolverSmem& S, bool have
     st_take_pass<n>(st, st->kv);
     st->cost = st->cost_new;  // SciPy keeps the trial's cost
     st->njev = st->njev + 1;
+    st_auto_recheck<n>(st, S);
     if (st->qr_mode && st_qr_begin<n>(st, S, st->kv, 1)) return;  // nit counts after the QR pass
     if (st->jacmode) st_update_scale<n>(st, false);
     st->prof[5] += clock64() - c0;
@@ -1145,6 +1174,7 @@ __device__ __noinline__ void fit_after_pass(FitState* st, SolverSmem& S, const d
     st_take_pass<n>(st, st->kv);  // g, G at the accepted x (cost kept: SciPy)
     st->cost = st->cost_new;
     st->njev = st->njev + 1;
+    st_auto_recheck<n>(st, S);
     if (st->qr_mode && st_qr_begin<n>(st, S, st->kv, 1)) return;
     if (st->jacmode) st_update_scale<n>(st, false);
     st->nit = st->nit + 1;

@@ -48,7 +48,8 @@ struct FitState {
   long long prof[8];          // SM cycles: eig, trial solve, select_step, fit_after_pass, after_trial,
                               // accept (take_pass + scale), outer_top (pre-trial), trial finish
   double cost, cost_new, Delta, alpha, gnorm, theta, actual;
-  double pred, hn, step_norm, Delta_used, ratio, pad4;
+  double pred, hn, step_norm, Delta_used, ratio;
+  double kappa2_gn;  // cond(B_hat)^2 bound from the last Gauss-Newton Cholesky (tr B_hat ||L^-1||_F^2; +inf if none)
   double x[NMAX], x_eval[NMAX];
   double g[NMAX], G[NMAX * NMAX], scale_inv[NMAX];
   // hat space of the current iterate (reused by rejected trials, R15)
@@ -57,7 +58,8 @@ struct FitState {
   double kv[KMAX];  // K-vector of the last pass
   double pcov[NMAX * NMAX];  // parameter covariance at the final x (curve_fit's pcov)
   int32_t pcov_done, qr_mode;  // qr_mode: TSQR (CholeskyQR2 + SVD of R) instead of the Gram eigensolver
-  int32_t qr_after, pad8;      // what follows the PH_QR2 pass: 0 initialisation, 1 an accepted step
+  int32_t qr_after;            // what follows the PH_QR2 pass: 0 initialisation, 1 an accepted step
+  int32_t auto_mode;           // solver AUTO: Gram until the conditioning calls for TSQR (checked at x0 and at accepted steps)
   QRState* qr;                 // device TSQR working set
   double* prec;                // = qr->prec (read by the preconditioned pass kernel)
 };

@@ -17,6 +17,10 @@ CASES = {
     "C3_1024_seed3": lambda: dg.make_gauss2d(1024, seed=3),
     "C4b_1024_seed4": lambda: dg.make_gauss2d_bounded(1024, "b"),
     "C4c_1024_seed4": lambda: dg.make_gauss2d_bounded(1024, "c"),
+    # C5 (n = 13) at reduced sizes: SURVEY c.5 gives SciPy 8/8 at 2048; these
+    # sizes run the moment kernel's whole-row tasks inside a fit
+    "C5_1024_seed5": lambda: dg.make_gauss2d_x2(1024, seed=5),
+    "C5_2048_seed5": lambda: dg.make_gauss2d_x2(2048, seed=5),
 }
 
 

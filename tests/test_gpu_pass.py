@@ -207,9 +207,9 @@ def _alt_coefs(sx, sy, th):
 
 @pytest.mark.parametrize("name,make", [c for c in CASES if c[0].startswith("gauss2d")],
                          ids=[c[0] for c in CASES if c[0].startswith("gauss2d")])
-def test_jpass_first_stage_alt_coordinates(name, make, monkeypatch):
+def test_jpass_first_stage_alt_coordinates(name, make):
     """Stage one of the two-stage chain rule (jf_models.cuh PreGauss2D) alone:
-    with the map T^T M T switched off (JF_DEBUG_NOCHAIN), the pass returns
+    with the map T^T M T switched off (JF_FLAG_ALT_COORDS), the pass returns
     the Gram of [J_alt | r] whose shape columns are d h / d(a, 2b, c2) =
     -A E (dx^2, dx dy, dy^2) — written out here from the quadratic form, so a
     wrong stage-two map cannot hide behind a compensating stage-one error."""
@@ -227,5 +227,57 @@ def test_jpass_first_stage_alt_coordinates(name, make, monkeypatch):
     Ja = np.stack(cols + [np.ones_like(X)], 1)
     r = dg.render(pr.model, (X, Y), x) - pr.z
     ref = (0.5 * float(r @ r), Ja.T @ r, Ja.T @ Ja, 0)
-    monkeypatch.setenv("JF_DEBUG_NOCHAIN", "1")
-    check_pass(jf.jpass(pr.model, pr.z, x, grid=pr.grid), ref, tol=1e-9)
+    check_pass(jf.jpass(pr.model, pr.z, x, grid=pr.grid, alt_coords=True), ref, tol=1e-9)
+
+
+EDGE = [  # (A, x0, y0, sx, sy, theta, off) on a 4096-wide image
+    ("narrow 2px", (1.5, 2047.3, 511.7, 2.0, 2.5, 0.4, 0.2)),
+    ("needle 3x1500px", (1.2, 1900.0, 500.0, 3.0, 1500.0, 0.3, 0.1)),
+    ("off-image centre", (2.0, -300.0, 1300.0, 400.0, 250.0, 2.1, 0.3)),
+    ("edge centre", (1.0, 4095.0, 0.0, 60.0, 900.0, 1.2, 0.05)),
+    ("wide flat", (0.8, 2000.0, 600.0, 30000.0, 20000.0, 0.7, 0.4)),
+    ("aspect 10 at the moment form's limit", (1.3, 2100.0, 480.0, 60.0, 600.0, 0.9, 0.25)),
+    ("width 50 at the moment form's limit", (1.1, 1500.0, 700.0, 50.0, 70.0, 2.5, 0.15)),
+]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name,truth", EDGE, ids=[e[0] for e in EDGE])
+def test_jpass_edge_shapes_full_width(name, truth):
+    """The moment kernel's recurrence / direct-evaluation switch (exponent
+    guards q < 600, |argR| < 300 per row segment) at T's row length: narrow,
+    needle-like, off-image and edge-centred peaks and a nearly flat one, on a
+    4096 x 1024 band, at the truth and a perturbed point."""
+    pr = dg.make_gauss2d_at(4096, 1024, truth)
+    for x in (pr.truth, pr.truth * np.array([1.05, 1.0, 1.0, 1.3, 0.8, 1.0, 1.1]) + np.array([0, 2.5, -1.5, 0, 0, 0.05, 0])):
+        ref = orp.jpass(pr.model, pr.coords(), pr.z, x)
+        check_pass(jf.jpass(pr.model, torch.as_tensor(pr.z).cuda(), x, grid=pr.grid), ref)
+        cr, _ = orp.residual_pass(pr.model, pr.coords(), pr.z, x)
+        c, _ = jf.residual_pass(pr.model, pr.z, x, grid=pr.grid)
+        assert abs(c - cr) <= TOL * cr
+
+
+@pytest.mark.parametrize("name,truth", EDGE, ids=[e[0] for e in EDGE])
+def test_jpass_edge_shapes_small(name, truth):
+    """The same shapes scaled to a 640 x 77 image (ragged row ends)."""
+    s = 640 / 4096
+    t = np.array(truth) * np.array([1, s, s, s, s, 1, 1])
+    t[3:5] = np.maximum(t[3:5], [0.7, 0.9])  # (sx == sy would make the theta column identically 0)
+    pr = dg.make_gauss2d_at(640, 77, t)
+    ref = orp.jpass(pr.model, pr.coords(), pr.z, pr.truth)
+    check_pass(jf.jpass(pr.model, pr.z, pr.truth, grid=pr.grid), ref)
+
+
+@pytest.mark.parametrize("comp2", [(1.0, 300.0, 40.0, 2.5, 2.0, 0.3), (0.9, 420.0, 30.0, 5.0, 120.0, 1.0),
+                                   (1.2, 380.0, 35.0, 60.0, 90.0, 2.0)],
+                         ids=["narrow", "needle", "moderate"])
+def test_jpass_two_gaussians_edge_shapes(comp2):
+    """The n = 13 moment kernel's accuracy switch: a narrow or elongated second
+    component sends the pass to the dual-number body; a moderate one stays."""
+    W, H = 600, 70
+    X, Y = dg.grid_coords(W, H)
+    p1 = np.array([1.5, 150.0, 30.0, 80.0, 100.0, 0.7])
+    truth = np.concatenate([p1, comp2, [0.2]])
+    z = dg.render("gauss2d_rot_x2", (X, Y), truth) + 0.1 * np.random.default_rng(8).standard_normal(W * H)
+    ref = orp.jpass("gauss2d_rot_x2", (X, Y), z, truth)
+    check_pass(jf.jpass("gauss2d_rot_x2", z, truth, grid=(W, H, 0)), ref)

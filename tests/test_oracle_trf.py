@@ -315,3 +315,63 @@ def test_pcov_matches_curve_fit_library():
     # full rank: pcov = inv(J^T J) * s^2
     J = models.jac(pr.model, pr.t, res["x"])
     assert np.allclose(res["pcov"], np.linalg.inv(J.T @ J) * 2 * res["cost"] / (pr.m - 4), rtol=1e-9)
+
+
+def test_default_p0_matches_curve_fit_library():
+    """p0 = None (jf.h: 'curve_fit's default initial guess'): the oracle's
+    default_p0 equals the point SciPy curve_fit evaluates first — ones
+    unbounded; with bounds the midpoint of two finite bounds, lb + 1 / ub - 1
+    with one (the point is interior, so least_squares' strict-feasibility
+    step leaves it unchanged)."""
+    import warnings
+    from scipy.optimize import curve_fit as sp_curve_fit
+    pr = dg.make_exp_decay()
+    cases = [
+        (np.full(3, -np.inf), np.full(3, np.inf)),
+        (np.array([0.0, -np.inf, -2.0]), np.array([4.0, 3.0, np.inf])),
+        (np.array([-1.0, 0.5, -np.inf]), np.array([np.inf, 2.5, 0.0])),
+    ]
+    for lb, ub in cases:
+        first = []
+
+        def f(t, a, b, c):  # curve_fit counts the parameters from the signature
+            if not first:
+                first.append(np.array([a, b, c]))
+            return models.h(pr.model, t, np.array([a, b, c]))
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            try:
+                sp_curve_fit(f, pr.t, pr.z, bounds=(lb, ub), method="trf", max_nfev=1)
+            except RuntimeError:
+                pass  # max_nfev reached: only the first point matters
+        got = trf.default_p0(3, lb, ub)
+        assert np.array_equal(got, first[0]), (lb, ub, got, first[0])
+        if np.any(np.isfinite(lb)) or np.any(np.isfinite(ub)):
+            assert not np.allclose(got, 1.0)  # the bounded rule is exercised
+
+
+@pytest.mark.parametrize("name,make", [TRAJ_CASES[0], TRAJ_CASES[1], TRAJ_CASES[3]],
+                         ids=[TRAJ_CASES[k][0] for k in (0, 1, 3)])
+def test_array_x_scale_matches_library(name, make):
+    """x_scale given as an array (D = diag(1/x_scale), reading R3): the same
+    trajectory as SciPy least_squares(x_scale=array), compared after 3 and
+    after all evaluations.  The offset starts near 0 with a small scale, so
+    the trust region binds early and the scaling shapes the iterates: using
+    x_scale in place of 1/x_scale (or ones) gives different early iterates."""
+    pr = make()
+    y = pr.coords()
+    p0 = pr.p0.copy()
+    p0[-1] = 1e-3                                   # the offset (last parameter of every model)
+    xs = np.geomspace(0.5, 2.0, pr.n)
+    xs[-1] = 1e-2
+    for mx in (3, None):
+        res = trf.fit(pr.model, y, pr.z, p0, x_scale=xs, max_nfev=mx)
+        ref = least_squares(lambda x: models.h(pr.model, y, x) - pr.z, p0,
+                            jac=lambda x: models.jac(pr.model, y, x), method="trf",
+                            tr_solver="exact", x_scale=xs, max_nfev=mx)
+        assert (res["status"], res["nfev"], res["njev"]) == (ref.status, ref.nfev, ref.njev)
+        assert np.allclose(res["x"], ref.x, rtol=1e-10, atol=1e-12)
+        if mx == 3 and pr.grid is None:  # (2-D: the positions dominate Delta0; the scaling does not bind)
+            for other in (1.0 / xs, "ones"):
+                o = trf.fit(pr.model, y, pr.z, p0, x_scale=other, max_nfev=3)
+                assert not np.allclose(o["x"], res["x"], rtol=1e-6, atol=0)
