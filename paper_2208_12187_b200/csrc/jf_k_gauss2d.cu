@@ -1,6 +1,4 @@
 // jf_k_gauss2d.cu — pass-kernel instances for ModelGauss2DRot (see jf_pass.cuh).
-#include <cstdlib>
-
 #include "jf_kernels.h"
 #include "jf_moment_stream.cuh"
 
@@ -29,10 +27,7 @@ constexpr int JL = 16, JNW = 12, JSEED = 8;
 void kernel_attrs_init() {
   cudaFuncSetAttribute((const void*)moment_stream_kernel<JL, JNW, JSEED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        moment_stream_smem_bytes(JNW));
-#if JF_DEV
-  cudaFuncSetAttribute((const void*)moment_stream_kernel<JL, JNW, JSEED, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       moment_stream_smem_bytes(JNW));
-#endif
+
 }
 
 Kernels kernels_gauss2d(int coord) {
@@ -43,12 +38,9 @@ Kernels kernels_gauss2d(int coord) {
     k.jwtpb = k.jtpb;
     k.jwsplit = k.jsplit ? 1 : 0;
     k.jk = moment_stream_kernel<JL, JNW, JSEED>;
-#if JF_DEV  // development builds: kernel variants for A/B timing
-    if (const char* v = getenv("JF_JVARIANT"))
-      if (atoi(v) == 1) k.jk = moment_stream_kernel<JL, JNW, JSEED, 0>;
-#endif
     k.jtpb = JNW * 32;
     k.jsmem = moment_stream_smem_bytes(JNW);
+
   }
   return k;
 }

@@ -18,6 +18,13 @@ KEYS = [
     "sm__cycles_elapsed.avg.per_second", "sm__cycles_active.avg", "sm__cycles_active.max", "sm__cycles_elapsed.avg",
     "dram__throughput.avg.pct_of_peak_sustained_elapsed", "smsp__inst_executed.sum",
     "smsp__sass_inst_executed_op_local_ld.sum",
+    # FP64 per-operation counts (thread instructions), FP32 pipe and SFU (the north star's ncu evidence list)
+    "sm__sass_thread_inst_executed_op_dfma_pred_on.sum", "sm__sass_thread_inst_executed_op_dadd_pred_on.sum",
+    "sm__sass_thread_inst_executed_op_dmul_pred_on.sum", "sm__inst_executed_pipe_fp64.sum",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "sm__inst_executed_pipe_xu.sum",
+    "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
 ]
 
 
