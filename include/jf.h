@@ -145,6 +145,13 @@ typedef struct jf_opts {
                                    App. A without dummy data; reading R26).  0: sized for m   */
   int32_t flags;                /* JF_FLAG_*, default 0                                         */
   int32_t pad_opts_;
+  const double* x_host;         /* jf_pass_device: optional host copy of x_dev's n values, read at
+                                   the call.  The rotated 2D Gaussian's moment J-pass then takes its
+                                   parameter-only prologue (the quadratic form's a, 2b, c2 from
+                                   sx, sy, theta; R34) precomputed by the call instead of computing
+                                   it in every thread — as inside jf_curve_fit, where the solver
+                                   kernel computes it.  NULL (default): computed in the kernel.
+                                   Must equal x_dev's contents; other calls ignore it.          */
 } jf_opts;
 
 /* jf_opts.flags */

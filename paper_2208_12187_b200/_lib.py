@@ -40,6 +40,7 @@ class jf_opts(C.Structure):
         ("trace", C.POINTER(C.c_double)),
         ("m_global", C.c_int64),
         ("capacity", C.c_int64), ("flags", C.c_int32), ("pad_opts_", C.c_int32),
+        ("x_host", C.POINTER(C.c_double)),
     ]
 
 

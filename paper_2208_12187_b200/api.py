@@ -269,8 +269,11 @@ def residual_pass(model, z, x, y=None, *, grid=None, sigma=None, **kw):
     return cost.value, bad.value
 
 
-def pass_device(model, z, x_dev, kvec_dev, y=None, *, grid=None, sigma=None, residual_only=False, **kw):
-    """jf_pass_device: enqueue one pass on opts.stream (all CUDA tensors)."""
+def pass_device(model, z, x_dev, kvec_dev, y=None, *, grid=None, sigma=None, residual_only=False, x_host=None,
+                **kw):
+    """jf_pass_device: enqueue one pass on opts.stream (all CUDA tensors).
+    x_host: optional host copy of x_dev (opts.x_host: the moment J-pass then
+    takes its parameter-only prologue from the call, as inside a fit)."""
     lib = L.load()
     mid = _model_id(model)
     n = lib.jf_model_nparams(mid)
@@ -278,6 +281,12 @@ def pass_device(model, z, x_dev, kvec_dev, y=None, *, grid=None, sigma=None, res
     if not data.on_device:
         raise ValueError("pass_device needs CUDA tensors")
     opts, keep = make_opts(grid=grid, sigma_ptr=data.sp, on_device=True, **kw)
+    if x_host is not None:
+        xh = _as_host(x_host)
+        if xh.size != n:
+            raise ValueError("x_host must hold the n parameters")
+        keep.append(xh)
+        opts.x_host = _dptr(xh)
     rc = lib.jf_pass_device(mid, data.yp, data.zp, data.m, x_dev.data_ptr(), n, C.byref(opts),
                             1 if residual_only else 0, kvec_dev.data_ptr())
     if rc < 0:

@@ -62,6 +62,10 @@ struct PassArgs {
   int32_t use_comm;     // 1: combine across ranks through the mailboxes
   int32_t no_chain;     // debug (JF_DEBUG_NOCHAIN): return the Gram in the alt coordinates (a, 2b, c2)
   unsigned long long* dbg; // debug (JF_DEBUG_STAMPS): per-warp [smid, t_start, t_loop_end, t_exit] (moment kernel)
+  // the parameter-only prologue of the n = 7 moment J-pass, precomputed for
+  // x by the caller (host x) — {A, x0, y0, a, 2b, c2, off, rho}; has_pre = 0: in-kernel
+  double pre[8];
+  int32_t has_pre, pad_pre;
   CommDev comm;
 };
 

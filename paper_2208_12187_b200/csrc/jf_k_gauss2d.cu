@@ -21,12 +21,14 @@ static Kernels make() {
 }
 
 // The moment-form J-pass (R34): L = 16 points per lane per warp-chunk, 12
-// warps per block (one block per SM), recurrence re-seeded every 8 chunks.
-constexpr int JL = 16, JNW = 12, JSEED = 8;
+// warps per block (one block per SM), recurrence re-seeded every 8 chunks,
+// z staged by bulk copies (TMA) through a 3-chunk ring per warp.
+constexpr int JL = 16, JNW = 12, JSEED = 8, JSTG = 3;
+#define JSTREAM moment_stream_kernel<JL, JNW, JSEED, JSTG>
 
 void kernel_attrs_init() {
-  cudaFuncSetAttribute((const void*)moment_stream_kernel<JL, JNW, JSEED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       moment_stream_smem_bytes(JNW));
+  cudaFuncSetAttribute((const void*)JSTREAM, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       moment_stream_smem_bytes(JNW, JL, JSTG));
 
 }
 
@@ -37,9 +39,9 @@ Kernels kernels_gauss2d(int coord) {
     // the dual-number kernel and its launch shape
     k.jwtpb = k.jtpb;
     k.jwsplit = k.jsplit ? 1 : 0;
-    k.jk = moment_stream_kernel<JL, JNW, JSEED>;
+    k.jk = JSTREAM;
     k.jtpb = JNW * 32;
-    k.jsmem = moment_stream_smem_bytes(JNW);
+    k.jsmem = moment_stream_smem_bytes(JNW, JL, JSTG);
 
   }
   return k;

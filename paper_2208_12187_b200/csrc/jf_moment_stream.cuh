@@ -133,46 +133,12 @@ __device__ __forceinline__ bool moment_form_accurate(double a, double b2, double
          lmax <= MOMENT_MAX_ASPECT * MOMENT_MAX_ASPECT * lmin;
 }
 
-// Out-of-line pieces of the moment kernel's rare paths (row changes, unsafe
-// or partial chunks): kept out of the hot loop's register allocation.
+// Out-of-line pieces of the moment kernel's rare paths (unsafe or partial
+// chunks): kept out of the hot loop's register allocation.
 struct StreamAcc {
   double P[5], Q[3], R[3], sr, srr;
   int bad;
 };
-// The thread's row moments (about dx = 0; shared-memory rows NR0.. of its
-// column) times dy^q into its moment column (rows 0..26), row moments cleared.
-static __device__ __noinline__ void stream_row_fold(double* __restrict__ colbase, int stride, double dy) {
-  constexpr int NR0 = MomLayout::KS;
-  auto c = [&](int i) -> double& { return colbase[i * stride]; };
-  double dq[5];
-  dq[0] = 1.0;
-  dq[1] = dy;
-  dq[2] = dy * dy;
-  dq[3] = dq[2] * dy;
-  dq[4] = dq[2] * dq[2];
-  double rp[11];
-#pragma unroll
-  for (int i = 0; i < 11; ++i) {
-    rp[i] = c(NR0 + i);
-    c(NR0 + i) = 0.0;
-  }
-#pragma unroll
-  for (int q = 0; q <= 4; ++q)
-#pragma unroll
-    for (int p = 0; p + q <= 4; ++p) {
-      double& m2 = c(MomLayout::O2 + mono(4, p, q));
-      m2 = fma(rp[p], dq[q], m2);
-    }
-#pragma unroll
-  for (int q = 0; q <= 2; ++q)
-#pragma unroll
-    for (int p = 0; p + q <= 2; ++p) {
-      double& m1 = c(MomLayout::O1 + mono(2, p, q));
-      m1 = fma(rp[5 + p], dq[q], m1);
-      double& mr = c(MomLayout::OR + mono(2, p, q));
-      mr = fma(rp[8 + p], dq[q], mr);
-    }
-}
 // A chunk by exp per point (row end, or an exponent range unsafe for the
 // recurrence): points c0 + lane + 32 k < W, z read from global memory,
 // moments about the chunk origin t = D (k - KC).
@@ -206,43 +172,56 @@ __device__ __noinline__ void stream_direct_chunk(StreamAcc& acc, const double* _
   }
 }
 
-// dynamic shared memory: the per-thread folded-moment table [KS][TPB + 1]
-// followed by the per-thread row moments [11][TPB + 1]
-__host__ __device__ constexpr int moment_stream_smem_bytes(int NW) {
-  return (MomLayout::KS + 11) * (NW * 32 + 1) * 8;  // + the row moments (11 per thread)
+// ---- TMA staging of z (1D bulk copies into a per-warp shared-memory ring)
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  unsigned done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+// One elected lane: bytes from global src into shared dst, completing on bar
+// (L2 evict-first: the image is read once per pass).
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
+                                           unsigned long long pol) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
 }
 
-// The end of a moment-form pass (both kernels): the block partial (the thread
-// columns of the moment table col[KS][TPB + 1] summed in thread order), the
-// grid combine (the last block sums the block partials in block order while
-// it builds the finish map), the map, the hand-off.
+// dynamic shared memory of the n = 7 moment J-pass: the z ring [NW][STG][32 L]
+__host__ __device__ constexpr int moment_stream_smem_bytes(int NW, int L, int STG) { return NW * STG * 32 * L * 8; }
+
+// The end of a moment-form pass: the block partial (the warps' moment vectors
+// wpart[NW][KS] summed in warp order), the grid combine (the last block sums
+// the block partials in block order), the finish map (fmap_mem: KT rows of
+// FMAP_COLS, built by the block's first idle warp), the hand-off.
 template <int NW>
 __device__ __forceinline__ void moment_stream_tail(const PassArgs& a, FitState* __restrict__ st,
                                                    cudaGraphConditionalHandle cond, int use_cond,
-                                                   double* dyn_stream, const PreGauss2D& spre, double off) {
+                                                   const double (*wpart)[MomLayout::KS], const double* fmap_mem,
+                                                   const PreGauss2D& spre) {
   constexpr int N = 7, KT = tri_count(N), KS2 = KT + 1;
   constexpr int TPB = NW * 32;
   constexpr int KS = MomLayout::KS, NV = MomLayout::NV;
   const int tid = threadIdx.x;
-  __shared__ double red[NW][KS];
   __shared__ double vec[KMAX];
   __shared__ double scratch[combine_scratch(TPB)];
   __shared__ double mom[KS];
-  // ---- block partial: the thread columns summed in thread order (NW segments of 32)
-  static_assert(NW * KS <= TPB, "one (entry, segment) per thread");
-  if (tid < NW * KS) {
-    const int i = tid % KS, seg = tid / KS;
-    const double* c = dyn_stream + i * (TPB + 1) + seg * 32;
-    double s4[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-    for (int j = 0; j < 32; ++j) s4[j & 3] += c[j];
-    red[seg][i] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
-  }
-  __syncthreads();
   if (tid < KS) {
     double s = 0.0;
 #pragma unroll
-    for (int w = 0; w < NW; ++w) s += red[w][tid];
+    for (int w = 0; w < NW; ++w) s += wpart[w][tid];
     // keep the partial in L2 for the last block (the image streams through evict-first)
     unsigned long long pol;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
@@ -274,8 +253,7 @@ __device__ __forceinline__ void moment_stream_tail(const PassArgs& a, FitState* 
       v[i] = (r < nblk) ? __ldcg(a.partials + (size_t)r * KS + rk) : 0.0;
     }
   }
-  double (*fmap)[FMAP_COLS] = reinterpret_cast<double (*)[FMAP_COLS]>(dyn_stream);  // the column table is free now
-  if (tid < KT) finish_map_row(spre, tid, fmap[tid]);
+  const double (*fmap)[FMAP_COLS] = reinterpret_cast<const double (*)[FMAP_COLS]>(fmap_mem);
   if (tid < NSEG * KS) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) s += v[i];
@@ -319,23 +297,48 @@ __device__ __forceinline__ void moment_stream_tail(const PassArgs& a, FitState* 
   dbg_tail(a, 7);
 }
 
-template <int L, int NW, int SEEDN>
+// Moment entry i (< OSR) of the layout as (row-moment index v, dy power q):
+// M2[mono(4, p, q)] <- RP[p] dy^q, M1 / MR[mono(2, p, q)] <- RQ[p] / RR[p] dy^q.
+__device__ __forceinline__ void fold_index(int i, int& v, int& q) {
+  q = 0;
+  if (i < MomLayout::O1) {
+    int r = i;
+    while (r >= 5 - q) r -= 5 - q++;
+    v = r;
+  } else {
+    const bool mr = i >= MomLayout::OR;
+    int r = i - (mr ? MomLayout::OR : MomLayout::O1);
+    while (r >= 3 - q) r -= 3 - q++;
+    v = (mr ? 8 : 5) + r;
+  }
+}
+
+template <int L, int NW, int SEEDN, int STG>
 __global__ void __launch_bounds__(NW * 32, 1)
     moment_stream_kernel(const PassArgs* __restrict__ pa, FitState* __restrict__ st, cudaGraphConditionalHandle cond,
                          int use_cond, const PassArgs av) {
   using Model = ModelGauss2DRot;
-  constexpr int N = Model::N, KT = tri_count(N), KS2 = KT + 1;
-  constexpr int TPB = NW * 32;
-  constexpr int KS = MomLayout::KS, NV = MomLayout::NV, NF = MomLayout::OSR;
+  constexpr int KS = MomLayout::KS, NF = MomLayout::OSR;
   constexpr int CW = 32 * L;
   constexpr double D = 32.0;
-  const PassArgs& a = pa ? *pa : av;  // fits: device-resident args (graph replay); else by value
-  if (!pass_begin<true, false>(a, st)) {
-    qr2_dispatch<Model, COORD_GRID, false, NW * 32>(a, st, cond, use_cond);  // TSQR second pass
-    return;
-  }
-  const double* xs = (a.epilogue == EPI_FIT) ? st->x_eval : a.x;
+  constexpr int KC = (L - 1) / 2;
+  constexpr int NR = 11;  // row moments RP[0..4], RQ[0..2], RR[0..2]
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  // the arguments (fits: device-resident, graph replay; else by value) into
+  // shared memory once: every later field access is a shared-memory load
+  __shared__ __align__(16) PassArgs sargs;
+  __shared__ int fmap_claim;
+  {
+    constexpr int NA = sizeof(PassArgs) / 8;
+    static_assert(sizeof(PassArgs) % 8 == 0 && NA <= NW * 32, "PassArgs copy");
+    if (tid < NA)
+      reinterpret_cast<unsigned long long*>(&sargs)[tid] =
+          pa ? __ldg(reinterpret_cast<const unsigned long long*>(pa) + tid)
+             : reinterpret_cast<const unsigned long long*>(&av)[tid];
+    if (tid == 0) fmap_claim = 0;
+    __syncthreads();
+  }
+  const PassArgs& a = sargs;
   // development builds only (JF_DEV): per-warp globaltimer stamps (tools/stamps2.py)
   auto stamp = [&](int slot) {
     if (JF_DEV && a.dbg && lane == 0 && blockIdx.x * NW + wid < 8000) {
@@ -350,65 +353,133 @@ __global__ void __launch_bounds__(NW * 32, 1)
     }
   };
   stamp(1);
+  extern __shared__ __align__(128) double zring_all[];  // [NW][STG][CW]
+  __shared__ __align__(8) unsigned long long zbar_all[NW * STG];
+  __shared__ double wpart[NW][KS];
+  __shared__ PreGauss2D spre;
+  __shared__ double fmap_s[tri_count(7)][FMAP_COLS];  // finish map (built by the block's first idle warp)
+  double* zring = zring_all + wid * STG * CW;
+  unsigned long long* zbar = zbar_all + wid * STG;
 
-  extern __shared__ __align__(16) double dyn_stream[];  // [KS][TPB + 1]
-  auto col = [&](int i) -> double& { return dyn_stream[i * (TPB + 1) + tid]; };
-  __shared__ PreGauss2D spre;  // the pass's parameters incl. the chain-rule block
-
-  double A, off, ga, gb2, gc, x0, y0;
-  {
-    double xv[N];
-#pragma unroll
-    for (int j = 0; j < N; ++j) xv[j] = xs[j];
-    const auto pre = Model::template prologue<true>(xv);
-    A = pre.g.A, off = pre.off, ga = pre.g.a, gb2 = pre.g.b2, gc = pre.g.c, x0 = pre.g.x0, y0 = pre.g.y0;
-    if (tid == 0) spre = pre.g;
-  }
-  if (!moment_form_accurate(ga, gb2, gc)) {
-    pass_body_ool<Model, true, COORD_GRID, false, PassCfg<Model, true>::P, TPB, false>(a, st, cond, use_cond);
-    return;
-  }
-#pragma unroll
-  for (int i = 0; i < NF; ++i) col(i) = 0.0;
-  stamp(2);
-
-  // every thread reads the pass's parameters from spre below (row set-up,
-  // exp seeds): the hot loop keeps only A, off, rho and lane - x0 in registers
-  __syncthreads();
+  // ---- the warp's chunks: a function of (m, W, grid) only, so the first STG
+  // copies are issued before this kernel waits for the solver kernel that
+  // precedes it in a fit (PDL) and before the prologue
   const int W = (int)a.W;
-  const int H = (int)(a.m / a.W);
+  const int H = (int)((double)a.m / (double)W);  // (m = H W exactly)
   const int cpr = (W + CW - 1) / CW;
   const int64_t nch = (int64_t)H * cpr;
-  const int64_t nw = (int64_t)gridDim.x * NW;
-  const int64_t gw = (int64_t)blockIdx.x * NW + wid;
-  const int64_t c_begin = gw * nch / nw, c_end = (gw + 1) * nch / nw;
-  const int nmy = (int)(c_end - c_begin);  // this warp's chunks
-  const double rho = exp(-2.0 * ga * D * D);
+  // warp g owns chunks [f(g), f(g + 1)), f(g) = floor(g nch / nw) evaluated in
+  // double (exact for nch nw < 2^53; any monotone f with f(0) = 0, f(nw) = nch
+  // is a partition) — no 64-bit integer division on the start-up path
+  const double fnw = (double)nch / (double)(gridDim.x * NW);
+  const int gw = blockIdx.x * NW + wid;
+  const int64_t c_begin = (int64_t)((double)gw * fnw);
+  const int64_t c_end = (gw + 1 == (int)(gridDim.x * NW)) ? nch : (int64_t)((double)(gw + 1) * fnw);
+  const int nmy = (int)(c_end - c_begin);
+  int row_begin = (int)((double)c_begin / (double)cpr);  // exact quotient after the correction
+  if ((int64_t)row_begin * cpr > c_begin) --row_begin;
+  if ((int64_t)(row_begin + 1) * cpr <= c_begin) ++row_begin;
+  const int cc_begin = (int)(c_begin - (int64_t)row_begin * cpr);
+  const bool tma_ok = ((reinterpret_cast<uintptr_t>(a.z) & 15) == 0) && ((W & 1) == 0);
+  unsigned long long pol = 0;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  int irow = row_begin, icc = cc_begin;  // the next chunk to copy
+  auto issue = [&](int slot) {
+    if (lane == 0) {
+      const int c0 = icc * CW;
+      tma_load_1d(zring + slot * CW, a.z + (int64_t)irow * W + c0, (unsigned)(min(CW, W - c0) * 8), zbar + slot, pol);
+    }
+    if (++icc == cpr) {
+      icc = 0;
+      ++irow;
+    }
+  };
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < STG; ++q) mbar_init(zbar + q);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  if (tma_ok) {
+#pragma unroll
+    for (int q = 0; q < STG; ++q)
+      if (q < nmy) issue(q);
+  }
+  stamp(4);
+  // the copies issued so far complete before the block leaves this kernel
+  auto drain = [&]() {
+    if (tma_ok)
+      for (int q = 0; q < STG && q < nmy; ++q) mbar_wait(zbar + q, 0u);
+  };
+
+  if (!pass_begin<true, false>(a, st)) {
+    drain();
+    qr2_dispatch<Model, COORD_GRID, false, NW * 32>(a, st, cond, use_cond);  // TSQR second pass
+    return;
+  }
+  const double* xs = (a.epilogue == EPI_FIT) ? st->x_eval : a.x;
+  stamp(5);
+
+  // ---- prologue: precomputed by the caller (a.has_pre, fits: by the solver
+  // kernel, st->pre) or here (plain doubles; the expressions of
+  // Gauss2DComponent::prologue)
+  double A, off, ga, gb2, gc, x0, y0, rho;
+  if (a.epilogue == EPI_FIT ? st->has_pre : a.has_pre) {
+    const double* pr = (a.epilogue == EPI_FIT) ? st->pre : a.pre;
+    A = pr[0], x0 = pr[1], y0 = pr[2], ga = pr[3], gb2 = pr[4], gc = pr[5], off = pr[6], rho = pr[7];
+  } else {
+    double pr[8];
+    gauss2d_prologue(xs, pr);
+    A = pr[0], x0 = pr[1], y0 = pr[2], ga = pr[3], gb2 = pr[4], gc = pr[5], off = pr[6], rho = pr[7];
+  }
+  stamp(6);
+  if (!moment_form_accurate(ga, gb2, gc)) {
+    drain();
+    pass_body_ool<Model, true, COORD_GRID, false, PassCfg<Model, true>::P, NW * 32, false>(a, st, cond, use_cond);
+    return;
+  }
+  stamp(2);
   const double xl = (double)lane - x0;     // dx of the lane's pixel in column 0
   const double dyb = (double)a.row0 - y0;  // dy of the shard's row 0
 
   // Moments of the current chunk about the lane's chunk origin o_c (its
-  // pixel k = KC: t = D (k - KC), compile-time), and of the current row about
-  // dx = 0 (each chunk folded in by a Taylor shift when it ends).  Keeping the
-  // chunk moments local bounds the shift's cancellation by (|t| + |o_c|) / w
-  // over the chunk that holds the mass (w: the peak's width along the row):
-  // the origin never travels along the row with accumulated mass.
-  constexpr int KC = (L - 1) / 2;
-  constexpr int NR = 11;  // row moments: RP[0..4], RQ[0..2], RR[0..2] (shared-memory column, per thread)
+  // pixel k = KC: t = D (k - KC), compile-time), of the current row about
+  // dx = 0 (each chunk added by a Taylor shift when it ends), and of the
+  // warp's rows so far (lane i < NF holds entry i of the moment layout: the
+  // row totals over the warp times dy^q, added at each row change).  Keeping
+  // the chunk moments local bounds the shift's cancellation by
+  // (|t| + |o_c|) / w over the chunk that holds the mass (w: the peak's width
+  // along the row): the origin never travels along the row with accumulated mass.
   double P[5], Q[3], R[3];  // chunk, about o_c
+  double RM[NR];            // row, about dx = 0
 #pragma unroll
   for (int i = 0; i < 5; ++i) P[i] = 0.0;
 #pragma unroll
   for (int i = 0; i < 3; ++i) Q[i] = R[i] = 0.0;
-  auto rowm = [&](int i) -> double& { return dyn_stream[(KS + i) * (TPB + 1) + tid]; };
 #pragma unroll
-  for (int i = 0; i < NR; ++i) rowm(i) = 0.0;
-  double sr = 0.0, srr = 0.0;
+  for (int i = 0; i < NR; ++i) RM[i] = 0.0;
+  double sr = 0.0, srr = 0.0, wacc = 0.0;
   int bad = 0;
+  int fv = 0, fq = 0;
+  if (lane < NF) fold_index(lane, fv, fq);
 
-  // the chunk's moments about o_c -> about dx = 0 (Pascal scheme: t -> t + o_c),
-  // added to the row's; the chunk's moments restart from zero
-  auto chunk_fold = [&](double oc) {
+  // the row's moments summed over the warp (xor butterfly: every lane gets the
+  // same bits), times dy^q into the lane's entry; the row's restart from zero
+  auto fold = [&](double dyv) {
+#pragma unroll
+    for (int v = 0; v < NR; ++v)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) RM[v] += __shfl_xor_sync(FULL, RM[v], o);
+    double t = RM[0];
+#pragma unroll
+    for (int v = 1; v < NR; ++v) t = (fv == v) ? RM[v] : t;
+    const double d2 = dyv * dyv;
+    const double dq = (fq == 0) ? 1.0 : (fq == 1) ? dyv : (fq == 2) ? d2 : (fq == 3) ? d2 * dyv : d2 * d2;
+    if (lane < NF) wacc = fma(t, dq, wacc);
+#pragma unroll
+    for (int v = 0; v < NR; ++v) RM[v] = 0.0;
+  };
+  auto chunk_fold = [&](double oc) {  // chunk moments about o_c -> about dx = 0 (Pascal scheme), into the row's
 #pragma unroll
     for (int j = 1; j <= 4; ++j)
 #pragma unroll
@@ -422,82 +493,35 @@ __global__ void __launch_bounds__(NW * 32, 1)
       }
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
-      rowm(i) += P[i];
+      RM[i] += P[i];
       P[i] = 0.0;
     }
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-      rowm(5 + i) += Q[i];
-      rowm(8 + i) += R[i];
+      RM[5 + i] += Q[i];
+      RM[8 + i] += R[i];
       Q[i] = R[i] = 0.0;
     }
   };
-  auto fold = [&](double dyv) { stream_row_fold(dyn_stream + tid, TPB + 1, dyv); };
 
-  // position of the chunk being processed (advanced incrementally, 32-bit)
-  int row = (int)(c_begin / cpr);
-  int cc = (int)(c_begin - (int64_t)row * cpr) - 1;
-  int cur_row = -1, jc = 0;
+  int row = row_begin, cc = cc_begin;
+  int cur_row = -1;
   double dy = 0.0;
-  bool row_fast = false;   // the warp's chunks of this row are safe for the recurrence
-  bool carried = false;    // E, Rr continue from the previous chunk
+  bool row_fast = false;  // the warp's chunks of this row are safe for the recurrence
+  bool carried = false;   // E, Rr continue from the previous chunk
   int since_seed = 0;
   double E = 0.0, Rr = 0.0;
-
-  // Load the next chunk in order (lane's points) into zz; a partial (row-end)
-  // chunk is predicated.  (lp, lcc): the lane's first point and the column of
-  // the next chunk to load.
-  int lcc = cc + 1;
-  const double* lp = a.z + (int64_t)row * W + lcc * CW + lane;
-  const int row_step = W - (cpr - 1) * CW;  // last chunk of a row -> first chunk of the next
-  // L2 prefetch PF chunks beyond the one loaded into registers (one bulk
-  // prefetch per chunk by lane 0; the register loads then hit L2): rows must
-  // start 16-byte aligned for the bulk copy engine, else no prefetch
-  constexpr int PF = 2;
-  const bool pf_ok = ((reinterpret_cast<uintptr_t>(a.z) & 15) == 0) && ((W & 1) == 0);
-  int pcc = lcc, pleft = nmy;
-  const double* pp = a.z + (int64_t)row * W + pcc * CW;
-  auto prefetch_next = [&]() {  // the next chunk in the prefetch stream
-    if (pleft > 0) {
-      if (pf_ok && lane == 0) {
-        const int c0p = pcc * CW;
-        const unsigned bytes = (unsigned)(min(CW, W - c0p) * 8);
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pp), "r"(bytes) : "memory");
-      }
-      --pleft;
-      if (++pcc == cpr) {
-        pcc = 0;
-        pp += W - (cpr - 1) * CW;
-      } else {
-        pp += CW;
-      }
-    }
-  };
+  for (int j = 0; j < nmy; ++j) {
+    const int slot = j % STG;
+    double* zs = zring + slot * CW;
+    const int c0 = cc * CW;
+    if (tma_ok) {
+      mbar_wait(zbar + slot, (unsigned)(j / STG) & 1u);
+    } else {  // (odd W or unaligned z: no bulk copies) the lanes stage the chunk themselves
+      const double* zg = a.z + (int64_t)row * W + c0;
 #pragma unroll
-  for (int q = 0; q < PF; ++q) prefetch_next();
-  auto load = [&](double (&zz)[L]) {
-    prefetch_next();
-    const int c0l = lcc * CW;
-    if (c0l + CW <= W) {  // warp-uniform
-#pragma unroll
-      for (int k = 0; k < L; ++k) zz[k] = __ldcs(lp + 32 * k);
-    } else {
-#pragma unroll
-      for (int k = 0; k < L; ++k) zz[k] = (c0l + lane + 32 * k < W) ? __ldcs(lp + 32 * k) : 0.0;
-    }
-    if (++lcc == cpr) {
-      lcc = 0;
-      lp += row_step;
-    } else {
-      lp += CW;
-    }
-  };
-
-  // One chunk: zc holds its points.
-  auto process = [&](const double (&zc)[L]) {
-    if (++cc == cpr) {
-      cc = 0;
-      ++row;
+      for (int k = 0; k < L; ++k) zs[lane + 32 * k] = (c0 + lane + 32 * k < W) ? zg[lane + 32 * k] : 0.0;
+      __syncwarp();
     }
     if (row != cur_row) {  // warp-uniform: fold the previous row, set up this one
       if (cur_row >= 0) fold(dy);
@@ -505,27 +529,23 @@ __global__ void __launch_bounds__(NW * 32, 1)
       dy = (double)row + dyb;
       // the warp's chunks of this row: [cc, cl]; q is convex and argR linear
       // along the row, so the range ends bound them
-      const int cl = min(cpr - 1, cc + (nmy - jc) - 1);
-      const double sa = spre.a, sb2 = spre.b2, sc = spre.c;
+      const int cl = min(cpr - 1, cc + (nmy - j) - 1);
       const double dxa = (double)(cc * CW) + xl;
       const double dxb = (double)(cl * CW + 32 * (L - 1)) + xl;
-      const double qa = dxa * (sa * dxa + sb2 * dy) + sc * (dy * dy);
-      const double qb = dxb * (sa * dxb + sb2 * dy) + sc * (dy * dy);
-      const double ra = D * (2.0 * sa * dxa + sb2 * dy) + sa * D * D;
-      const double rb = D * (2.0 * sa * dxb + sb2 * dy) + sa * D * D;
+      const double qa = dxa * (ga * dxa + gb2 * dy) + gc * (dy * dy);
+      const double qb = dxb * (ga * dxb + gb2 * dy) + gc * (dy * dy);
+      const double ra = D * (2.0 * ga * dxa + gb2 * dy) + ga * D * D;
+      const double rb = D * (2.0 * ga * dxb + gb2 * dy) + ga * D * D;
       const bool ok = qa < 600.0 && qb < 600.0 && fabs(ra) < 300.0 && fabs(rb) < 300.0 &&
-                      2.0 * sa * D * D * L * SEEDN < 300.0;
+                      2.0 * ga * D * D * L * SEEDN < 300.0;
       row_fast = __all_sync(FULL, ok);
       carried = false;
     }
-    ++jc;
-    const int c0 = cc * CW;
     const double dx0 = (double)c0 + xl;
     if (row_fast && c0 + CW <= W) {  // warp-uniform
       if (!carried || ++since_seed >= SEEDN) {
-        const double sa = spre.a, sb2 = spre.b2, sc = spre.c;
-        const double q0 = dx0 * (sa * dx0 + sb2 * dy) + sc * (dy * dy);
-        const double argR = D * (2.0 * sa * dx0 + sb2 * dy) + sa * D * D;
+        const double q0 = dx0 * (ga * dx0 + gb2 * dy) + gc * (dy * dy);
+        const double argR = D * (2.0 * ga * dx0 + gb2 * dy) + ga * D * D;
         E = exp(-q0);
         Rr = exp(-argR);
         since_seed = 0;
@@ -533,10 +553,11 @@ __global__ void __launch_bounds__(NW * 32, 1)
       }
       double cs = 0.0;
       const double E_in = E, R_in = Rr;
+      const double* zl = zs + lane;
 #pragma unroll
       for (int k = 0; k < L; ++k) {
         const double u = E;
-        const double r = fma(A, u, off) - zc[k];  // Eq. 1: r = h - z
+        const double r = fma(A, u, off) - zl[32 * k];  // Eq. 1: r = h - z
         const double u2 = u * u;
         const double k1 = D * (k - KC), k2 = k1 * k1, k3 = k2 * k1, k4 = k2 * k2;
         const double ur = u * r;
@@ -563,7 +584,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
         double e = E_in, rr = R_in;
 #pragma unroll
         for (int k = 0; k < L; ++k) {
-          bad += isfinite(fma(A, e, off) - zc[k]) ? 0 : 1;
+          bad += isfinite(fma(A, e, off) - zl[32 * k]) ? 0 : 1;
           e *= rr;
           rr *= rho;
         }
@@ -579,8 +600,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
       acc.sr = sr;
       acc.srr = srr;
       acc.bad = bad;
-      stream_direct_chunk<L>(acc, a.z + (int64_t)row * W + c0 + lane, c0, lane, W, dx0, dy, spre.a, spre.b2,
-                             spre.c, A, off);
+      stream_direct_chunk<L>(acc, zs + lane, c0, lane, W, dx0, dy, ga, gb2, gc, A, off);
 #pragma unroll
       for (int q = 0; q < 5; ++q) P[q] = acc.P[q];
 #pragma unroll
@@ -590,28 +610,45 @@ __global__ void __launch_bounds__(NW * 32, 1)
       bad = acc.bad;
     }
     chunk_fold(dx0 + D * KC);
-  };
-
-  {
-    double za[L], zb[L];
-    if (nmy > 0) load(za);
-    for (int j = 0; j < nmy; j += 2) {
-      if (j + 1 < nmy) load(zb);
-      process(za);
-      if (j + 1 < nmy) {
-        if (j + 2 < nmy) load(za);
-        process(zb);
-      }
+    // the slot is free again: refill it with the chunk STG ahead
+    __syncwarp();
+    if (tma_ok && j + STG < nmy) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(slot);
+    }
+    if (++cc == cpr) {
+      cc = 0;
+      ++row;
     }
   }
   if (cur_row >= 0) fold(dy);
   stamp(3);
-  col(MomLayout::OSR) = sr;
-  col(MomLayout::OSRR) = srr;
-  col(NV) = (double)bad;
+  // the warp's moment vector: the folded entries (lanes < NF) and the lane sums
+  // of sum r, sum r^2 and the non-finite count (xor butterfly)
+  double bd = (double)bad;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sr += __shfl_xor_sync(FULL, sr, o);
+    srr += __shfl_xor_sync(FULL, srr, o);
+    bd += __shfl_xor_sync(FULL, bd, o);
+  }
+  if (lane < NF) wpart[wid][lane] = wacc;
+  if (lane == 0) {
+    wpart[wid][MomLayout::OSR] = sr;
+    wpart[wid][MomLayout::OSRR] = srr;
+    wpart[wid][MomLayout::NV] = bd;
+  }
+  // the first warp of the block to get here builds the finish map (the chain
+  // rule's T from the dual-number prologue) while the others still stream
+  int first = 0;
+  if (lane == 0) first = atomicAdd(&fmap_claim, 1);
+  if (__shfl_sync(FULL, first, 0) == 0) {
+    const PreGauss2D g = Model::template prologue<true>(xs).g;
+    if (lane == 0) spre = g;
+    for (int t = lane; t < tri_count(7); t += 32) finish_map_row(g, t, fmap_s[t]);
+  }
   __syncthreads();
-
-  moment_stream_tail<NW>(a, st, cond, use_cond, dyn_stream, spre, off);
+  moment_stream_tail<NW>(a, st, cond, use_cond, wpart, &fmap_s[0][0], spre);
 }
 
 }  // namespace jf

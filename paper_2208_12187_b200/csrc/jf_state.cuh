@@ -62,6 +62,30 @@ struct FitState {
   int32_t auto_mode;           // solver AUTO: Gram until the conditioning calls for TSQR (checked at x0 and at accepted steps)
   QRState* qr;                 // device TSQR working set
   double* prec;                // = qr->prec (read by the preconditioned pass kernel)
+  int32_t has_pre, pad_pre;    // pre: the n = 7 moment J-pass prologue at x_eval (gauss2d_prologue)
+  double pre[8];
 };
+
+// The parameter-only prologue of the n = 7 moment J-pass (the rotated 2D
+// Gaussian, SPEC S:463 form; the expressions of Gauss2DComponent::prologue):
+// pre = {A, x0, y0, a, 2b, c2, off, rho}, rho = exp(-2 a 32^2) the row
+// recurrence's step factor (lane stride 32).  Computed once per pass by the
+// caller — the host for a host x, the solver kernel for the next pass of a
+// fit — instead of by every thread of the pass.
+__host__ __device__ inline void gauss2d_prologue(const double* x, double* pre) {
+  const double sx = x[3], sy = x[4], th = x[5];
+  const double C = cos(th), S = sin(th);
+  const double ix = 0.5 / (sx * sx), iy = 0.5 / (sy * sy);
+  const double CC = C * C, SS = S * S;
+  const double a = CC * ix + SS * iy;
+  pre[0] = x[0];
+  pre[1] = x[1];
+  pre[2] = x[2];
+  pre[3] = a;
+  pre[4] = 2.0 * ((S * C) * (iy - ix));
+  pre[5] = SS * ix + CC * iy;
+  pre[6] = x[6];
+  pre[7] = exp(-2.0 * a * 32.0 * 32.0);
+}
 
 }  // namespace jf

@@ -115,8 +115,10 @@ def test_captured_passes_keep_their_own_arguments():
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=s):
-        jf.pass_device(pr.model, zd, x1, k1, grid=pr.grid, stream=s.cuda_stream)
-        jf.pass_device(pr.model, zd, x2, k2, grid=pr.grid, stream=s.cuda_stream)
+        # (x_host: the prologue jpass computes, so the costs compare bitwise; the
+        # precomputed prologue travels by value with each captured launch)
+        jf.pass_device(pr.model, zd, x1, k1, grid=pr.grid, stream=s.cuda_stream, x_host=pr.p0)
+        jf.pass_device(pr.model, zd, x2, k2, grid=pr.grid, stream=s.cuda_stream, x_host=pr.truth)
         jf.pass_device(pr.model, zd, x2, r1, grid=pr.grid, stream=s.cuda_stream, residual_only=True)
     k1.zero_()
     k2.zero_()
@@ -141,7 +143,8 @@ def test_calls_on_different_streams_are_ordered():
     streams = [torch.cuda.Stream() for _ in range(2)]
     torch.cuda.synchronize()
     for k in range(6):
-        jf.pass_device(pr.model, zd, xs[k], outs[k], grid=pr.grid, stream=streams[k % 2].cuda_stream)
+        jf.pass_device(pr.model, zd, xs[k], outs[k], grid=pr.grid, stream=streams[k % 2].cuda_stream,
+                       x_host=pr.p0 * (1 + 0.01 * k))  # (the prologue jpass computes: bitwise comparable)
     torch.cuda.synchronize()
     n = pr.n
     kk = (n + 1) * (n + 2) // 2

@@ -160,16 +160,26 @@ def test_pass_is_bitwise_deterministic():
 
 
 def test_pass_device_async_matches_sync():
+    """pass_device (device x) against jpass (host x).  With opts.x_host the
+    moment J-pass takes the same host-computed prologue as jpass: bitwise
+    equal; without it the kernel computes the prologue itself (device cos /
+    sin / exp, which may differ from the host's in the last bit): parity."""
     pr = dg.make_gauss2d(300)
     zd = torch.as_tensor(pr.z).cuda()
     xd = torch.as_tensor(pr.p0).cuda()
     kv = torch.zeros(37, dtype=torch.float64, device="cuda")
+    kv2 = torch.zeros(37, dtype=torch.float64, device="cuda")
     s = torch.cuda.current_stream()
-    jf.pass_device(pr.model, zd, xd, kv, grid=pr.grid, stream=s.cuda_stream)
+    jf.pass_device(pr.model, zd, xd, kv, grid=pr.grid, stream=s.cuda_stream, x_host=pr.p0)
+    jf.pass_device(pr.model, zd, xd, kv2, grid=pr.grid, stream=s.cuda_stream)
     torch.cuda.synchronize()
     c, g, G, bad = jf.jpass(pr.model, pr.z, pr.p0, grid=pr.grid)
     k = kv.cpu().numpy()
     assert k[-2] * 0.5 == c and k[-1] == bad
+    k2 = kv2.cpu().numpy()
+    assert abs(k2[-2] * 0.5 - c) <= TOL * c and k2[-1] == bad
+    ref = orp.jpass(pr.model, pr.coords(), pr.z, pr.p0)
+    check_pass((0.5 * k2[-2], g, G, int(k2[-1])), ref)
 
 
 @pytest.mark.slow

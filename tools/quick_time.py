@@ -15,13 +15,13 @@ s = torch.cuda.Stream()
 torch.cuda.set_stream(s)
 for ro in (False, True):
     for _ in range(3):
-        jf.pass_device(pr.model, z, x, kv, grid=pr.grid, stream=s.cuda_stream, residual_only=ro)
+        jf.pass_device(pr.model, z, x, kv, grid=pr.grid, stream=s.cuda_stream, residual_only=ro, x_host=pr.p0)
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
     N = 50
     e0.record()
     for _ in range(N):
-        jf.pass_device(pr.model, z, x, kv, grid=pr.grid, stream=s.cuda_stream, residual_only=ro)
+        jf.pass_device(pr.model, z, x, kv, grid=pr.grid, stream=s.cuda_stream, residual_only=ro, x_host=pr.p0)
     e1.record(); torch.cuda.synchronize()
     t = e0.elapsed_time(e1) / N
     print(f"{'r' if ro else 'J'}-pass W={W}: {t*1e3:.1f} us  {pr.m/t*1e3:.3e} pts/s")
@@ -29,7 +29,7 @@ for ro in (False, True):
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=s):
             for _ in range(N):
-                jf.pass_device(pr.model, z, x, kv, grid=pr.grid, stream=s.cuda_stream, residual_only=ro)
+                jf.pass_device(pr.model, z, x, kv, grid=pr.grid, stream=s.cuda_stream, residual_only=ro, x_host=pr.p0)
         g.replay(); torch.cuda.synchronize()
         e0.record(s); g.replay(); e1.record(s); torch.cuda.synchronize()
         t = e0.elapsed_time(e1) / N

@@ -18,7 +18,7 @@ print(f"warps {len(d)}")
 print("entry      ", q(en))
 print("prologue   ", q(pro), " (dur", q(pro - en), ")")
 print("loop end   ", q(lo), " (dur", q(lo - pro), ")")
-print("partial    ", q(pa))
+print("tail end   ", q(pa), " (tail dur", q(pa - lo), ")")
 tl = np.where(tail > 0, tail - tail[1], 0) / 1.9e3
 print("tail us from ticket [1]:", " ".join(f"[{i}] {tl[i]:.2f}" for i in (2, 5, 6, 7)))
 sm = d[:, 0]
