@@ -65,7 +65,9 @@ struct PassArgs {
   // the parameter-only prologue of the n = 7 moment J-pass, precomputed for
   // x by the caller (host x) — {A, x0, y0, a, 2b, c2, off, rho}; has_pre = 0: in-kernel
   double pre[8];
-  int32_t has_pre, pad_pre;
+  int32_t has_pre;
+  int32_t fused;        // fit of the n = 7 moment J-pass: the solver step runs in the pass's last block
+                        // (its dynamic shared memory as scratch) — no solver kernel between passes
   CommDev comm;
 };
 

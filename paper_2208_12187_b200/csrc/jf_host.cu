@@ -68,6 +68,15 @@ __global__ void inv_kernel(double* p, int64_t m) {
     p[i] = 1.0 / p[i];
 }
 
+// Wait for the stream by polling (a blocking cudaStreamSynchronize may sleep
+// and wake up tens of microseconds late: a fit is ~0.1-0.4 ms).
+cudaError_t stream_wait(cudaStream_t s) {
+  for (;;) {
+    const cudaError_t e = cudaStreamQuery(s);
+    if (e != cudaErrorNotReady) return e;
+  }
+}
+
 int model_n(int model) {
   switch (model) {
     case JF_LINEAR: return 2;
@@ -256,6 +265,7 @@ const PassArgs g_zero_args = {};  // the by-value args of launches that read dev
 struct PassPair {
   KernelFn j = nullptr, r = nullptr;
   int jtpb = 256, rtpb = 256, jgrid = 1, rgrid = 1, jsmem = 0;
+  bool fused = false;  // j runs the solver step in its last block (speculative fits)
 };
 
 PassPair select_pass(Ctx& c, const Kernels& k, bool weighted, int64_t m) {
@@ -265,6 +275,7 @@ PassPair select_pass(Ctx& c, const Kernels& k, bool weighted, int64_t m) {
   p.jtpb = (weighted && k.jwtpb > 0) ? k.jwtpb : k.jtpb;
   p.rtpb = k.rtpb;
   p.jsmem = weighted ? 0 : k.jsmem;
+  p.fused = !weighted && k.jfused;
   p.jgrid = grid_for(c, p.j, p.jtpb, m, p.jsmem);
   const bool jsplit = (weighted && k.jwsplit >= 0) ? (k.jwsplit != 0) : k.jsplit;
   if (jsplit) {  // two equal halves
@@ -470,7 +481,7 @@ struct StreamOrder {
   }
 };
 
-int build_graph(Ctx& c, const PassPair& k, int policy, bool qr, cudaGraphExec_t* out) {
+int build_graph(Ctx& c, const PassPair& k, int policy, bool qr, bool fused, cudaGraphExec_t* out) {
   (void)qr;
   cudaGraph_t g;
   CK(cudaGraphCreate(&g, 0));
@@ -535,9 +546,9 @@ int build_graph(Ctx& c, const PassPair& k, int policy, bool qr, cudaGraphExec_t*
   };
   kp.kernelParams = pargs;
   // U copies of the iteration per trip of the WHILE loop: the conditional
-  // node's per-trip overhead is paid once per U iterations; copies after the
-  // fit ended find nothing to do (phase DONE) and return at once.
-  constexpr int unroll = 2;
+  // node's per-trip overhead (~6 us) is paid once per U iterations; copies
+  // after the fit ended find nothing to do (phase DONE) and return at once.
+  constexpr int unroll = 3;
   for (int u = 0; u < unroll; ++u) {
     if (policy == JF_POLICY_CONSERVATIVE) {
       kp.func = (void*)k.r;
@@ -554,7 +565,8 @@ int build_graph(Ctx& c, const PassPair& k, int policy, bool qr, cudaGraphExec_t*
     kp.sharedMemBytes = k.jsmem;
     if (int e = add(kp, false)) return e;
     kp.sharedMemBytes = 0;
-    if (int e = add(sp, true)) return e;
+    if (!fused)  // (fused: the J-pass's last block runs the solver step)
+      if (int e = add(sp, true)) return e;
   }
   CK(cudaGraphInstantiate(out, g, 0));
   cudaGraphDestroy(g);
@@ -670,7 +682,7 @@ static int pass_common(int32_t model, const double* y, const double* z, int64_t 
   if (stamps) {
     static unsigned long long h_dbg[DBG_N];
     CK(cudaMemcpyAsync(h_dbg, d_dbg, sizeof(h_dbg), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    CK(stream_wait(s));
     if (FILE* f = fopen(stamps, "wb")) {
       fwrite(h_dbg, sizeof(h_dbg), 1, f);
       fclose(f);
@@ -682,12 +694,12 @@ static int pass_common(int32_t model, const double* y, const double* z, int64_t 
   if (sync) {
     int* herr = (int*)(c->h_pin + 256);
     CK(cudaMemcpyAsync(herr, a.err, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    CK(stream_wait(s));
     const int err = *herr;
     if (host_out) memcpy(host_out, c->h_pin, sizeof(double) * KSo);
     if (err) {
       CK(cudaMemsetAsync(a.err, 0, sizeof(int), s));
-      CK(cudaStreamSynchronize(s));
+      CK(stream_wait(s));
       return err;
     }
   }
@@ -801,7 +813,7 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
       if (launch_comm_sum(cd, o.comm->epoch, (double)m, d_m, d_err, s)) return fail(JF_ECUDA);
       CK(cudaMemcpyAsync(c->h_pin, d_m, sizeof(double), cudaMemcpyDeviceToHost, s));
       CK(cudaMemcpyAsync(c->h_pin + 1, d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
+      CK(stream_wait(s));
       if (*(int*)(c->h_pin + 1)) return fail(JF_ECOMM);
       m_global = (int64_t)c->h_pin[0];
     }
@@ -865,6 +877,12 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
     a.use_comm = 1;
     fill_comm(a.comm, o.comm);
   }
+  // speculative one-GPU fits of the n = 7 moment J-pass: the solver step runs
+  // in the pass kernel's last block (graph body: passes only).  Sharded fits
+  // keep the solver kernel: a pass's last block already waits on its peers in
+  // the cross-rank combine.
+  const bool fused = k.fused && o.policy == JF_POLICY_SPECULATIVE && !o.comm;
+  a.fused = fused ? 1 : 0;
   auto t0 = std::chrono::steady_clock::now();
   CK(cudaMemcpyAsync(c->d_state, &h, sizeof(h), cudaMemcpyHostToDevice, s));
   if (!c->h_args_valid || memcmp(c->h_args, &a, sizeof(a)) != 0) {  // a repeated fit skips the copy
@@ -883,13 +901,13 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
     f<<<1, 256, 0, s>>>(c->d_args, c->d_state);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(&h, c->d_state, sizeof(h), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    CK(stream_wait(s));
   } else if (o.use_graph) {
-    GraphKey key{(const void*)k.j, o.policy, k.jgrid, k.rgrid, qr ? 1 : 0};
+    GraphKey key{(const void*)k.j, o.policy, k.jgrid, k.rgrid, (qr ? 1 : 0) | (fused ? 2 : 0)};
     auto it = c->graphs.find(key);
     cudaGraphExec_t ge;
     if (it == c->graphs.end()) {
-      r = build_graph(*c, k, o.policy, qr, &ge);
+      r = build_graph(*c, k, o.policy, qr, fused, &ge);
       if (r) return fail(r);
       c->graphs[key] = ge;
     } else {
@@ -898,16 +916,16 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
     }
     CK(cudaGraphLaunch(ge, s));
     CK(cudaMemcpyAsync(&h, c->d_state, sizeof(h), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    CK(stream_wait(s));
   } else {
     const int cap = 4 * h.max_nfev + 8;
     for (int iter = 0; iter < cap; ++iter) {
       const bool jac = (o.policy == JF_POLICY_CONSERVATIVE) ? (h.phase != PH_TRIAL_R) : true;
       r = launch_pass(k, jac, s, c->d_args, c->d_state, g_zero_args);  // J kernels also run PH_QR2
       if (r) return fail(r);
-      if (launch_solver(c->d_state, c->d_out, s)) return fail(JF_ECUDA);
+      if (!fused && launch_solver(c->d_state, c->d_out, s)) return fail(JF_ECUDA);
       CK(cudaMemcpyAsync(&h, c->d_state, sizeof(h), cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
+      CK(stream_wait(s));
       if (!h.cont) break;
     }
   }
@@ -939,7 +957,7 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
   if (o.trace_cap > 0 && out->trace_len > 0)
   {
     CK(cudaMemcpyAsync(o.trace, c->d_trace, sizeof(double) * TRACE_FIELDS * out->trace_len, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    CK(stream_wait(s));
   }
   if (h.error) return fail(h.error);
   if (h.cont) return fail(JF_ECUDA);  // loop did not terminate

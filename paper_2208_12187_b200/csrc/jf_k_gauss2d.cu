@@ -42,6 +42,8 @@ Kernels kernels_gauss2d(int coord) {
     k.jk = JSTREAM;
     k.jtpb = JNW * 32;
     k.jsmem = moment_stream_smem_bytes(JNW, JL, JSTG);
+    static_assert(moment_stream_smem_bytes(JNW, JL, JSTG) >= (int)fused_solver_smem_bytes(), "solver scratch");
+    k.jfused = true;
 
   }
   return k;

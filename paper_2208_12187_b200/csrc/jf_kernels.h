@@ -20,6 +20,7 @@ struct Kernels {
   KernelFn rkw = nullptr;
   int jtpb = 256, rtpb = 256;  // threads per block of the J / r kernels
   int jsmem = 0;               // dynamic shared memory of the J kernel (bytes)
+  bool jfused = false;         // jk runs the solver step in its last block (PassArgs::fused)
   bool jsplit = false;         // J grid split in two halves (even grid >= 2)
   int jwtpb = 0;               // weighted J kernel's block size / split when jk is a moment kernel
   int jwsplit = -1;            //   (0 / -1: same as jtpb / jsplit)

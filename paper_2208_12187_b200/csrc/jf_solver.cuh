@@ -1353,6 +1353,9 @@ __device__ __forceinline__ void solver_step(FitState* st, SolverSmem& S, const d
 // written by the pass) into shared memory — every load issued before any is
 // consumed — run one solver step, write the state back, set the CUDA-graph
 // WHILE condition.  Used by the solver kernel and by the fused J-pass.
+#if JF_DEV
+constexpr bool getenv_dummy_twice = true;
+#endif
 template <int NC>
 __device__ __forceinline__ void solver_run(FitState* __restrict__ st, SolverSmem& S, FitState& sst, const double* kv,
                                            bool jac, cudaGraphConditionalHandle cond, int use_cond) {
@@ -1392,8 +1395,100 @@ __device__ __forceinline__ void solver_run(FitState* __restrict__ st, SolverSmem
     if (k < KMAX) S.kvs[k] = kvb[q];
   }
   __syncwarp();
+#if JF_DEV  // development: the same step run twice (state reloaded) — cold vs warm instruction cache
+  if (getenv_dummy_twice) {
+    const long long ca = clock64();
+    solver_step<NC>(&sst, S, S.kvs, jac);
+    __syncwarp();
+    const long long cb = clock64();
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int k = lane + 32 * q;
+      if (k < NW) dst[k] = buf[q];
+    }
+#pragma unroll
+    for (int q = 0; q < KPER; ++q) {
+      const int k = lane + 32 * q;
+      if (k < KMAX) S.kvs[k] = kvb[q];
+    }
+    __syncwarp();
+    solver_step<NC>(&sst, S, S.kvs, jac);
+    __syncwarp();
+    const long long cc = clock64();
+    if (lane == 0) {
+      sst.prof[0] = (long long)(cb - ca);  // (last call only)
+      sst.prof[2] = (long long)(cc - cb);
+    }
+  } else
+#endif
   solver_step<NC>(&sst, S, S.kvs, jac);
   if (lane == 0 && sst.n == 7) {  // the next n = 7 moment J-pass's prologue at x_eval
+    gauss2d_prologue(sst.x_eval, sst.pre);
+    sst.has_pre = 1;
+  }
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+  if (lane == 0) {
+    sst.pass_ready = 0;
+    sst.epi_ns += (t1 - t0);
+    const int k = sst.tl_n;
+    if (k < 64) sst.tl[k] = t1;
+    sst.tl_n = k + 1;
+  }
+  __syncwarp();
+  unsigned long long* back = reinterpret_cast<unsigned long long*>(st);
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int k = lane + 32 * q;
+    if (k < NW) back[k] = dst[k];
+  }
+  if (lane == 0 && use_cond) cudaGraphSetConditional(cond, sst.cont ? 1u : 0u);
+}
+
+// Scratch of the fused solver step (SolverSmem, then a FitState copy).
+__host__ __device__ constexpr size_t fused_solver_smem_bytes() {
+  return ((sizeof(SolverSmem) + 15) & ~(size_t)15) + sizeof(FitState);
+}
+
+// The solver step run by warp 0 of the last block of a fused J-pass (reading
+// PassArgs::fused): the same as the solver kernel's solver_run with the
+// pass's combined K-vector read from shared memory (vec) and the kernel's
+// dynamic shared memory (>= fused_solver_smem_bytes()) as scratch.  The next
+// pass kernel waits for this grid (PDL griddepcontrol.wait) and reads the
+// state it leaves.
+template <int NC>
+__device__ __noinline__ void fused_solver_step(FitState* __restrict__ st, const double* vec,
+                                               cudaGraphConditionalHandle cond, int use_cond) {
+  extern __shared__ __align__(16) unsigned char fused_dyn[];
+  SolverSmem& S = *reinterpret_cast<SolverSmem*>(fused_dyn);
+  FitState& sst = *reinterpret_cast<FitState*>(fused_dyn + ((sizeof(SolverSmem) + 15) & ~(size_t)15));
+  const int lane = threadIdx.x & 31;
+  unsigned long long t0, t1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  constexpr int NW = sizeof(FitState) / 8;
+  constexpr int PER = (NW + 31) / 32;
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(st);
+  unsigned long long* dst = reinterpret_cast<unsigned long long*>(&sst);
+  unsigned long long buf[PER];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int k = lane + 32 * q;
+    buf[q] = (k < NW) ? __ldcg(src + k) : 0ull;
+  }
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int k = lane + 32 * q;
+    if (k < NW) dst[k] = buf[q];
+  }
+  for (int k = lane; k < KMAX; k += 32) S.kvs[k] = vec[k];
+  __syncwarp();
+  if (lane == 0) {
+    const int k = sst.tl_n;
+    if (k < 64) sst.tl[k] = t0;
+    sst.tl_n = k + 1;
+  }
+  __syncwarp();
+  solver_step<NC>(&sst, S, S.kvs, true);
+  if (lane == 0 && sst.n == 7) {  // the next pass's prologue at x_eval
     gauss2d_prologue(sst.x_eval, sst.pre);
     sst.has_pre = 1;
   }

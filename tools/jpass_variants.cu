@@ -98,6 +98,19 @@ void run(const char* name, const double* dz, const double* dx, int W, int H, dou
     std::sort(last.begin(), last.end());
     printf("  per-block loop-end spread med %.2f max %.2f us; block last loop end min %.2f med %.2f max %.2f us\n",
            spread[grid / 2], spread.back(), last[0], last[grid / 2], last.back());
+    printf("  mean loop end by warp id:");
+    for (int w = 0; w < NW; ++w) {
+      double m = 0.0;
+      for (int b = 0; b < grid; ++b) m += ((double)hd[(b * NW + w) * 8 + 3] - (double)t0) / 1e3;
+      printf(" %.2f", m / grid);
+    }
+    printf("\n  mean loop dur by warp id:");
+    for (int w = 0; w < NW; ++w) {
+      double m = 0.0;
+      for (int b = 0; b < grid; ++b) m += ((double)hd[(b * NW + w) * 8 + 3] - (double)hd[(b * NW + w) * 8 + 2]) / 1e3;
+      printf(" %.2f", m / grid);
+    }
+    printf("\n");
     const unsigned long long* tl = hd.data() + 4 * 16384 - 16;  // last block's tail (clock64)
     printf("  tail from ticket (us at 1.965 GHz): loads+map %.2f, kvec %.2f, chain %.2f, hand-off %.2f\n",
            (double)(tl[2] - tl[1]) / 1965.0, (double)(tl[5] - tl[1]) / 1965.0, (double)(tl[6] - tl[1]) / 1965.0,
@@ -171,12 +184,9 @@ int main(int argc, char** argv) {
   int nsm;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
 #define RUN(L, NW, S, STG) run<L, NW, S, STG>(#L " " #NW " " #S " " #STG, dz, dx, W, H, dpart, dtick, dout, derr, nsm)
-  RUN(16, 12, 8, 3);
   double pre[8];
   gauss2d_prologue(p, pre);
   g_pre = pre;
-  have_ref = false;
   RUN(16, 12, 8, 3);
-  RUN(16, 12, 8, 2);
   return 0;
 }
