@@ -88,8 +88,11 @@ typedef enum { JF_XSCALE_JAC = 0, JF_XSCALE_ONES = 1, JF_XSCALE_ARRAY = 2 } jf_x
  *  GRAM: fp64 Gram G = J^T J; Cholesky Gauss-Newton trial, eigendecomposition
  *        of the scaled Gram when Alg. 2 needs alpha > 0
  *  TSQR: R factor of W = [J | r] by CholeskyQR2 (a Gram pass, then a pass
- *        accumulating (W R1^-1)^T (W R1^-1); R = chol(.) R1), SVD of the scaled
- *        R by one-sided Jacobi (two passes per accepted step)
+ *        accumulating (W R1^-1)^T (W R1^-1); R = chol(.) R1) while its
+ *        certificate bounds cond(W)^2 by 1e14, else by shifted CholeskyQR3
+ *        (R1 = chol(W^T W + s I), then CholeskyQR2 on W R1^-1: one pass
+ *        more; cond(W) up to ~1e16); SVD of the scaled R by one-sided Jacobi
+ *        (two or three passes per accepted step)
  *  AUTO: TSQR if cond(J D^-1)^2 estimated at x0 — or at an accepted step —
  *        exceeds 1e6, else GRAM (the default) */
 typedef enum { JF_SOLVE_AUTO = 0, JF_SOLVE_GRAM = 1, JF_SOLVE_TSQR = 2 } jf_solver;

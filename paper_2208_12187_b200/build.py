@@ -29,6 +29,8 @@ NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompil
               "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
 if os.environ.get("JF_DEV"):  # development build: per-warp timeline stamps, diagnostics (never shipped)
     NVCC_FLAGS += ["-DJF_DEV=1"]
+if os.environ.get("JF_CHECKED"):  # checked build: device bounds checks (JF_DCHECK), never shipped
+    NVCC_FLAGS += ["-DJF_CHECKED=1"]
 
 
 def nvcc() -> str:

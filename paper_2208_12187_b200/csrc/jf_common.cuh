@@ -1,6 +1,8 @@
 // jf_common.cuh — shared device-side definitions of the B200 hot path.
 #pragma once
 
+#include <cstdio>
+
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -11,6 +13,22 @@ constexpr int KMAX = (NMAX + 1) * (NMAX + 2) / 2 + 1;  // K-vector length for n 
 constexpr int BLOCK = 256;                             // threads per pass block
 constexpr int NWARP = BLOCK / 32;
 constexpr unsigned FULL = 0xffffffffu;
+
+// Checked builds (JF_CHECKED=1 python -m paper_2208_12187_b200.build; never
+// shipped): device-side bounds checks on every global read of the data and on
+// the bulk-copy ranges; a failed check prints where and traps the kernel.
+// The substitute for compute-sanitizer, which the GPU pool does not allow.
+#ifndef JF_CHECKED
+#define JF_CHECKED 0
+#endif
+#define JF_DCHECK(cond)                                                                                  \
+  do {                                                                                                   \
+    if (JF_CHECKED && !(cond)) {                                                                         \
+      printf("JF_DCHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__, __LINE__,          \
+             (int)blockIdx.x, (int)threadIdx.x);                                                         \
+      __trap();                                                                                          \
+    }                                                                                                    \
+  } while (0)
 
 // K-vector slot of W^T W entry (j, k), j <= k <= n, W = [J | r] (jf.h).
 __host__ __device__ constexpr int tri_slot(int n, int j, int k) {

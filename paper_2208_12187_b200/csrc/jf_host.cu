@@ -19,11 +19,25 @@
 #include <tuple>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/jf.h"
 #include "jf_kernels.h"
 #include "jf_state.cuh"
 
 using namespace jf;
+
+namespace {
+// NVTX ranges (SURVEY §5 tracing): per fit, per pass call, and in the host-
+// driven loop per pass / solver launch; visible in Nsight Systems, free when
+// no tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+}  // namespace
 
 namespace jf {  // jf_comm.cu
 int launch_comm_sum(const CommDev& cd, unsigned long long epoch, double v, double* d_out, int* d_err, cudaStream_t s);
@@ -620,6 +634,7 @@ const char* jf_version(void) { return "jfb200 0.1 sm_100a"; }
 static int pass_common(int32_t model, const double* y, const double* z, int64_t m, const double* x, int x_on_device,
                        int32_t n, const jf_opts* opts, int residual_only, double* out_dev_or_null,
                        double* host_out /* KMAX */, bool sync) {
+  NvtxRange nv(residual_only ? "jf_residual_pass" : "jf_pass");
   jf_opts o;
   if (opts) o = *opts;
   else jf_opts_default(&o);
@@ -742,6 +757,7 @@ int32_t jf_pass_device(int32_t model, const double* y, const double* z, int64_t 
 
 static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t m, const double* p0, int32_t n,
                         const double* lb, const double* ub, const jf_opts* opts, jf_result* out) {
+  NvtxRange nv("jf_curve_fit");
   auto fail = [&](int code) {
     out->status = code;
     return code;
@@ -794,7 +810,10 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
   if ((r = order.begin(c, s))) return fail(r);
   if (order.cap) return fail(JF_EINVAL);  // a fit synchronises: it cannot be captured
   Staged sg;
-  r = stage_inputs(*c, s, model, y, z, m, o, sg);
+  {
+    NvtxRange nv2("stage_inputs");
+    r = stage_inputs(*c, s, model, y, z, m, o, sg);
+  }
   if (r) return fail(r);
   out->t_upload_s = sg.upload_s;
   Kernels kk = get_kernels(model, sg.coord);
@@ -914,16 +933,25 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
       ge = it->second;
       out->graph_reused = 1;
     }
+    nvtxRangePushA("fit graph (passes + solver steps on the device)");
     CK(cudaGraphLaunch(ge, s));
     CK(cudaMemcpyAsync(&h, c->d_state, sizeof(h), cudaMemcpyDeviceToHost, s));
-    CK(stream_wait(s));
+    const cudaError_t we = stream_wait(s);
+    nvtxRangePop();
+    CK(we);
   } else {
     const int cap = 4 * h.max_nfev + 8;
     for (int iter = 0; iter < cap; ++iter) {
       const bool jac = (o.policy == JF_POLICY_CONSERVATIVE) ? (h.phase != PH_TRIAL_R) : true;
-      r = launch_pass(k, jac, s, c->d_args, c->d_state, g_zero_args);  // J kernels also run PH_QR2
+      {
+        NvtxRange nv3(jac ? "J-pass" : "r-pass");
+        r = launch_pass(k, jac, s, c->d_args, c->d_state, g_zero_args);  // J kernels also run PH_QR2
+      }
       if (r) return fail(r);
-      if (!fused && launch_solver(c->d_state, c->d_out, s)) return fail(JF_ECUDA);
+      if (!fused) {
+        NvtxRange nv3("solver step");
+        if (launch_solver(c->d_state, c->d_out, s)) return fail(JF_ECUDA);
+      }
       CK(cudaMemcpyAsync(&h, c->d_state, sizeof(h), cudaMemcpyDeviceToHost, s));
       CK(stream_wait(s));
       if (!h.cont) break;
@@ -979,6 +1007,7 @@ int32_t jf_curve_fit_batch(int32_t model, const double* y, const double* z, int6
                            const double* p0, int32_t n, const double* lb, const double* ub, const jf_opts* opts,
                            jf_batch_result* out) {
   static_assert(sizeof(jf_batch_result) == sizeof(BatchResult), "jf_batch_result layout");
+  NvtxRange nv("jf_curve_fit_batch");
   jf_opts o;
   if (opts) o = *opts;
   else jf_opts_default(&o);

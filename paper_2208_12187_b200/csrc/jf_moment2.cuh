@@ -251,6 +251,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
   auto load = [&](int64_t row, int cc) {
     const int c0l = cc * CW;
     const double* zp = z + row * (int64_t)W + c0l + lane;
+    JF_DCHECK(row >= 0 && row * (int64_t)W + min(c0l + CW, W) <= a.m);
     if (c0l + CW <= W) {  // warp-uniform
 #pragma unroll
       for (int k = 0; k < L; ++k) zn[k] = __ldcs(zp + 32 * k);

@@ -387,6 +387,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
   auto issue = [&](int slot) {
     if (lane == 0) {
       const int c0 = icc * CW;
+      JF_DCHECK(irow >= 0 && c0 < W && (int64_t)irow * W + min(CW, W - c0) + c0 <= a.m && slot < STG);
       tma_load_1d(zring + slot * CW, a.z + (int64_t)irow * W + c0, (unsigned)(min(CW, W - c0) * 8), zbar + slot, pol);
     }
     if (++icc == cpr) {
@@ -519,6 +520,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
       mbar_wait(zbar + slot, (unsigned)(j / STG) & 1u);
     } else {  // (odd W or unaligned z: no bulk copies) the lanes stage the chunk themselves
       const double* zg = a.z + (int64_t)row * W + c0;
+      JF_DCHECK(row >= 0 && (int64_t)row * W + min(c0 + CW, W) <= a.m);
 #pragma unroll
       for (int k = 0; k < L; ++k) zs[lane + 32 * k] = (c0 + lane + 32 * k < W) ? zg[lane + 32 * k] : 0.0;
       __syncwarp();

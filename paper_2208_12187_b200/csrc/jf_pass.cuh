@@ -510,6 +510,7 @@ __device__ __forceinline__ void grid_recur_loop(const PassArgs& a, const auto& p
 #pragma unroll
       for (int k = 0; k < L; ++k) {
         const bool v = col + 32 * k < W;
+        JF_DCHECK(!v || row * a.W + col + 32 * k < a.m);
         zn[k] = v ? __ldcs(zp + 32 * k) : 0.0;
         if constexpr (WGT) wn[k] = v ? __ldcs(ws + row * a.W + col + 32 * k) : 0.0;
       }
@@ -615,6 +616,7 @@ __device__ __forceinline__ void run_part(const PassArgs& a, const Pre& pre, int 
     for (int p = 0; p < P; ++p) {
       const int64_t idx = base + p * S;
       const bool v = idx < m;
+      JF_DCHECK(!v || idx >= 0);
       qz[p] = v ? __ldcs(z + idx) : 0.0;
       qw[p] = (v && weighted) ? __ldcs(ws + idx) : 1.0;
       if constexpr (EXPL) {

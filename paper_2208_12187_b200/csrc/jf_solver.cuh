@@ -364,10 +364,10 @@ static __device__ __noinline__ int warp_svd(SolverSmem& S, int n, int rows) {
 
 // upper Cholesky of the Gram packed in a K-vector; false if not SPD
 template <int n>
-__device__ __forceinline__ bool chol_kv(const double* kv, double* R) {
+__device__ __forceinline__ bool chol_kv(const double* kv, double* R, double shift = 0.0) {
   constexpr int N1 = n + 1;
   for (int i = 0; i < N1; ++i)
-    for (int j = 0; j < N1; ++j) R[i * N1 + j] = (j >= i) ? kv[tri_slot(n, i, j)] : 0.0;
+    for (int j = 0; j < N1; ++j) R[i * N1 + j] = (j >= i) ? kv[tri_slot(n, i, j)] + (i == j ? shift : 0.0) : 0.0;
   for (int k = 0; k < N1; ++k) {
     double d = R[k * N1 + k];
     for (int j = 0; j < k; ++j) d = fma(-R[j * N1 + k], R[j * N1 + k], d);
@@ -943,31 +943,63 @@ __device__ __noinline__ void st_outer_top(FitState* st, SolverSmem& S) {
   st_trial_begin<n>(st, S, true);
 }
 
-// TSQR: start the preconditioned second pass at the current x from the
-// first pass's Gram (kv).  Returns false if G1 is not numerically SPD
-// (cond(W) beyond ~1e8): the fit then continues in Gram mode.
+// TSQR (reading R31): the R factor of W = [J | r] from passes that reduce
+// (W P)^T (W P) for preconditioners P built from the earlier passes.
+//  - CholeskyQR2: R1 = chol(W^T W), R = chol((W R1^-1)^T (W R1^-1)) R1 — one
+//    preconditioned pass; accurate while cond(W) stays below ~u^-1/2, here
+//    while the certificate trace(G1) ||R1^-1||_F^2 >= cond(W)^2 is <= 1e14.
+//  - beyond that (or when chol(G1) fails): shifted CholeskyQR3 (Fukaya,
+//    Kannan, Nakatsukasa, Yamamoto, Yanagisawa 2020): R1 = chol(G1 + s I)
+//    with s = 11 (m (n+1) + (n+1)(n+2)) u ||W||_2^2 (||W||_2^2 <= trace G1),
+//    which exists for any cond(W); then CholeskyQR2 on W R1^-1 — two
+//    preconditioned passes, R accurate for cond(W) up to ~u^-1.
+constexpr double QR2_KAPPA2_MAX = 1.0e14;
+
+// Start TSQR at the current x from the first pass's Gram (kv): the first
+// preconditioner into the QR working set, phase PH_QR2.  Returns false only if
+// G1 is not finite or not even the shifted Gram factors (the fit then
+// continues in Gram mode).
 template <int n>
 __device__ __forceinline__ bool st_qr_begin(FitState* st, SolverSmem& S, const double* kv, int after) {
   constexpr int N1 = n + 1;
   double* R1 = &S.T[0][0];
   double* P = &S.M2[0][0];
-  if (!chol_kv<n>(kv, R1)) {
-    st->qr_mode = 0;
-    return false;
+  double tr = 0.0;
+  for (int i = 0; i < N1; ++i) tr += kv[tri_slot(n, i, i)];
+  bool ok = chol_kv<n>(kv, R1);
+  if (ok) {
+    tri_inv<n>(R1, P);
+    double fro = 0.0;
+    for (int i = 0; i < N1 * N1; ++i) fro = fma(P[i], P[i], fro);
+    ok = tr * fro <= QR2_KAPPA2_MAX;
   }
-  tri_inv<n>(R1, P);
+  int stage = 0;
+  if (!ok) {  // shifted CholeskyQR3
+    const double u = 0.5 * DBL_EPSILON;
+    const double shift = 11.0 * ((double)st->m_global * N1 + (double)(N1 * (N1 + 1))) * u * tr;
+    if (!(tr > 0.0 && tr < INFINITY) || !chol_kv<n>(kv, R1, shift)) {
+      st->qr_mode = 0;
+      return false;
+    }
+    tri_inv<n>(R1, P);
+    stage = 1;
+  }
   for (int i = 0; i < N1 * N1; ++i) {
     st->qr->R1[i] = R1[i];
     st->qr->prec[i] = P[i];
   }
+  st->qr_stage = stage;
   st->qr_after = after;
   st->phase = PH_QR2;
   return true;
 }
 
-// TSQR: after the preconditioned pass, R = chol(G2) R1 and (g, G) from R.
+// TSQR: after a preconditioned pass (Gram G2 of W P, P = R1^-1), R = chol(G2)
+// R1.  Shifted CholeskyQR3's first preconditioned pass: R becomes the next
+// R1 (another PH_QR2 pass follows; returns false).  Otherwise (g, G) from R
+// (g = R_J^T c, G = R_J^T R_J); returns true.
 template <int n>
-__device__ __forceinline__ void st_qr_finish(FitState* st, SolverSmem& S, const double* kv) {
+__device__ __forceinline__ bool st_qr_finish(FitState* st, SolverSmem& S, const double* kv) {
   constexpr int N1 = n + 1;
   double* R2 = &S.T[0][0];
   double* R = &S.M2[0][0];
@@ -981,6 +1013,16 @@ __device__ __forceinline__ void st_qr_finish(FitState* st, SolverSmem& S, const 
       for (int k = i; k <= j; ++k) t = fma(R2[i * N1 + k], R1[k * N1 + j], t);
       R[i * N1 + j] = (j >= i) ? t : 0.0;
     }
+  if (st->qr_stage == 1) {  // shifted CholeskyQR3: CholeskyQR2 on W R^-1 next
+    double* P = &S.T[0][0];
+    tri_inv<n>(R, P);
+    for (int i = 0; i < N1 * N1; ++i) {
+      st->qr->R1[i] = R[i];
+      st->qr->prec[i] = P[i];
+    }
+    st->qr_stage = 2;
+    return false;
+  }
   for (int i = 0; i < N1 * N1; ++i) st->qr->R[i] = R[i];
   for (int j = 0; j < n; ++j) {  // g = R_J^T c, G = R_J^T R_J
     double t = 0.0;
@@ -993,6 +1035,7 @@ __device__ __forceinline__ void st_qr_finish(FitState* st, SolverSmem& S, const 
       st->G[l * NMAX + j] = u;
     }
   }
+  return true;
 }
 
 // AUTO solver choice (jf.h jf_solver): an upper bound on cond(J D^-1)^2 for
@@ -1183,7 +1226,7 @@ __device__ __noinline__ void fit_after_pass(FitState* st, SolverSmem& S, const d
     st_outer_top<n>(st, S);
     st->prof[6] += clock64() - c1;
   } else if (phase == PH_QR2 && jac) {
-    st_qr_finish<n>(st, S, st->kv);
+    if (!st_qr_finish<n>(st, S, st->kv)) return;  // (shifted CholeskyQR3: one more preconditioned pass)
     if (st->qr_after == 0) {
       st_init_finish<n>(st, S);
     } else {
@@ -1353,9 +1396,6 @@ __device__ __forceinline__ void solver_step(FitState* st, SolverSmem& S, const d
 // written by the pass) into shared memory — every load issued before any is
 // consumed — run one solver step, write the state back, set the CUDA-graph
 // WHILE condition.  Used by the solver kernel and by the fused J-pass.
-#if JF_DEV
-constexpr bool getenv_dummy_twice = true;
-#endif
 template <int NC>
 __device__ __forceinline__ void solver_run(FitState* __restrict__ st, SolverSmem& S, FitState& sst, const double* kv,
                                            bool jac, cudaGraphConditionalHandle cond, int use_cond) {
@@ -1395,32 +1435,6 @@ __device__ __forceinline__ void solver_run(FitState* __restrict__ st, SolverSmem
     if (k < KMAX) S.kvs[k] = kvb[q];
   }
   __syncwarp();
-#if JF_DEV  // development: the same step run twice (state reloaded) — cold vs warm instruction cache
-  if (getenv_dummy_twice) {
-    const long long ca = clock64();
-    solver_step<NC>(&sst, S, S.kvs, jac);
-    __syncwarp();
-    const long long cb = clock64();
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const int k = lane + 32 * q;
-      if (k < NW) dst[k] = buf[q];
-    }
-#pragma unroll
-    for (int q = 0; q < KPER; ++q) {
-      const int k = lane + 32 * q;
-      if (k < KMAX) S.kvs[k] = kvb[q];
-    }
-    __syncwarp();
-    solver_step<NC>(&sst, S, S.kvs, jac);
-    __syncwarp();
-    const long long cc = clock64();
-    if (lane == 0) {
-      sst.prof[0] = (long long)(cb - ca);  // (last call only)
-      sst.prof[2] = (long long)(cc - cb);
-    }
-  } else
-#endif
   solver_step<NC>(&sst, S, S.kvs, jac);
   if (lane == 0 && sst.n == 7) {  // the next n = 7 moment J-pass's prologue at x_eval
     gauss2d_prologue(sst.x_eval, sst.pre);

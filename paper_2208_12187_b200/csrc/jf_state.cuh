@@ -59,6 +59,9 @@ struct FitState {
   double pcov[NMAX * NMAX];  // parameter covariance at the final x (curve_fit's pcov)
   int32_t pcov_done, qr_mode;  // qr_mode: TSQR (CholeskyQR2 + SVD of R) instead of the Gram eigensolver
   int32_t qr_after;            // what follows the PH_QR2 pass: 0 initialisation, 1 an accepted step
+  int32_t qr_stage;            // 0: CholeskyQR2's second pass pending; 1, 2: shifted CholeskyQR3's
+                               // first / second preconditioned pass pending (reading R31)
+  int32_t pad_qr;
   int32_t auto_mode;           // solver AUTO: Gram until the conditioning calls for TSQR (checked at x0 and at accepted steps)
   QRState* qr;                 // device TSQR working set
   double* prec;                // = qr->prec (read by the preconditioned pass kernel)

@@ -211,6 +211,21 @@ def test_tsqr_ill_conditioned_matches_oracle(sig):
     check_fit(res, ref, res.trace, tr, trace_rtol=1e-7)
 
 
+@pytest.mark.parametrize("sig", [20.0, 40.0])
+def test_tsqr_near_rank_deficient_matches_oracle(sig):
+    """kappa(J D^-1) ~ 8.5e8 / 1.4e10: beyond CholeskyQR2 (its certificate
+    trace(G1) ||R1^-1||_F^2 exceeds 1e14, or chol(G1) fails), so the TSQR path
+    runs shifted CholeskyQR3 (reading R31) and keeps the oracle's App. B SVD
+    trajectory: same counts, x to 1e-6; Delta and alpha carry R's relative
+    error ~EPS kappa amplified by s_max / s_min (reading R28): 1e-4."""
+    t, z, p0 = _ill_conditioned(sig)
+    tr = []
+    ref = otrf.fit("gauss1d", t, z, p0, trace=tr)
+    for solver in ("tsqr", "auto"):
+        res = jf.curve_fit("gauss1d", z, y=t, p0=p0, solver=solver, trace_cap=256)
+        check_fit(res, ref, res.trace, tr, trace_rtol=1e-4)
+
+
 def test_auto_solver_picks_tsqr_only_when_ill_conditioned():
     """AUTO: the ill-conditioned case follows the oracle like TSQR; the
     well-conditioned case runs the Gram path (one pass per trial)."""

@@ -20,7 +20,9 @@ EXTRA=sm__sass_thread_inst_executed_op_dfma_pred_on.sum,sm__sass_thread_inst_exe
 timeout 600 ncu --set full --metrics $EXTRA --clock-control none --import-source on -k regex:moment_stream -s 3 -c 1 \
     -o gpurun_out/jpass_${TAG} -f python tools/quick_time.py 4096 passonly > /dev/null 2>&1
 if [ "$WHAT" = all ]; then
-timeout 600 ncu --set full --metrics $EXTRA --clock-control none --import-source on -k regex:solver_kernel -s 20 -c 1 \
-    -o gpurun_out/solver_${TAG} -f python tools/quick_time.py 4096 > /dev/null 2>&1
+# (T fits run the solver step inside the J-pass's last block; the solver kernel
+# still serves the n = 13 C5 fit)
+timeout 900 ncu --set full --metrics $EXTRA --clock-control none --import-source on -k regex:solver_kernel -s 4 -c 1 \
+    -o gpurun_out/solver_${TAG} -f python bench.py --steps 1 --warmup 3 --no-batch --no-cpu-baseline > /dev/null 2>&1
 fi
 ls -la gpurun_out
