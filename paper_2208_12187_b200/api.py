@@ -133,27 +133,49 @@ def make_opts(*, grid=None, t0=0.0, dt=1.0, index0=0, sigma_ptr=None, on_device=
     return o, keep
 
 
-@dataclass
 class FitResult:
-    x: np.ndarray
-    cost: float
-    optimality: float
-    grad: np.ndarray
-    gram: np.ndarray
-    pcov: np.ndarray
-    status: int
-    nfev: int
-    njev: int
-    nit: int
-    active_mask: np.ndarray
-    kernel_launches: int
-    graph_reused: int
-    t_upload_s: float
-    t_solve_s: float
-    t_epilogue_s: float
-    epilogue_cycles: np.ndarray = field(default_factory=lambda: np.zeros(8))
-    timeline_ns: np.ndarray = field(default_factory=lambda: np.zeros(0))
-    trace: np.ndarray = field(default_factory=lambda: np.zeros((0, L.JF_TRACE_FIELDS)))
+    """jf_result as Python values.  The arrays are built from the C struct on
+    first access (marshalling only; a fit's wall time then does not pay for
+    arrays the caller never reads)."""
+
+    _ARRAYS = {"x": 1, "grad": 1, "gram": 2, "pcov": 2}
+    _SCALARS = ("cost", "optimality", "status", "nfev", "njev", "nit", "kernel_launches", "graph_reused",
+                "t_upload_s", "t_solve_s", "t_epilogue_s")
+
+    def __init__(self, res, n, trace=None):
+        self._res = res
+        self._n = n
+        self._cache = {}
+        self.trace = trace if trace is not None else np.zeros((0, L.JF_TRACE_FIELDS))
+
+    def __getattr__(self, name):
+        if name.startswith("_"):
+            raise AttributeError(name)
+        cache = self._cache
+        if name in cache:
+            return cache[name]
+        res, n = self._res, self._n
+        if name in self._SCALARS:
+            v = getattr(res, name)
+        elif name in self._ARRAYS:
+            k = n if self._ARRAYS[name] == 1 else n * n
+            v = np.frombuffer(getattr(res, name), dtype=np.float64, count=k).copy()
+            if self._ARRAYS[name] == 2:
+                v = v.reshape(n, n)
+        elif name == "active_mask":
+            v = np.frombuffer(res.active_mask, dtype=np.int8, count=n).astype(np.int64)
+        elif name == "epilogue_cycles":
+            v = np.frombuffer(res.epilogue_cycles, dtype=np.float64, count=8).copy()
+        elif name == "timeline_ns":
+            v = np.frombuffer(res.timeline_ns, dtype=np.float64, count=res.timeline_len).copy()
+        else:
+            raise AttributeError(name)
+        cache[name] = v
+        return v
+
+    def __repr__(self):
+        return (f"FitResult(status={self.status}, nfev={self.nfev}, njev={self.njev}, nit={self.nit}, "
+                f"cost={self.cost!r}, x={self.x!r})")
 
 
 def curve_fit(model, z, y=None, *, grid=None, p0=None, lb=None, ub=None, sigma=None, trace_cap=0,
@@ -178,17 +200,7 @@ def curve_fit(model, z, y=None, *, grid=None, p0=None, lb=None, ub=None, sigma=N
                           C.byref(opts), C.byref(res))
     if rc < 0:
         raise JFError(rc, "jf_curve_fit")
-    # numpy views of the ctypes arrays, copied (no per-element Python lists)
-    def arr(field_, k):
-        return np.frombuffer(field_, dtype=np.float64, count=k).copy()
-    out = FitResult(
-        x=arr(res.x, n), cost=res.cost, optimality=res.optimality, grad=arr(res.grad, n),
-        gram=arr(res.gram, n * n).reshape(n, n), pcov=arr(res.pcov, n * n).reshape(n, n),
-        status=res.status, nfev=res.nfev, njev=res.njev,
-        nit=res.nit, active_mask=np.frombuffer(res.active_mask, dtype=np.int8, count=n).astype(np.int64),
-        kernel_launches=res.kernel_launches, graph_reused=res.graph_reused, t_upload_s=res.t_upload_s, t_solve_s=res.t_solve_s,
-        t_epilogue_s=res.t_epilogue_s, epilogue_cycles=arr(res.epilogue_cycles, 8),
-        timeline_ns=arr(res.timeline_ns, res.timeline_len))
+    out = FitResult(res, n)
     if tr is not None:
         out.trace = tr[: res.trace_len].copy()
     return out

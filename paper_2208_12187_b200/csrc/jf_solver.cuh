@@ -1436,9 +1436,10 @@ __device__ __forceinline__ void solver_run(FitState* __restrict__ st, SolverSmem
   }
   __syncwarp();
   solver_step<NC>(&sst, S, S.kvs, jac);
-  if (lane == 0 && sst.n == 7) {  // the next n = 7 moment J-pass's prologue at x_eval
-    gauss2d_prologue(sst.x_eval, sst.pre);
-    sst.has_pre = 1;
+  __syncwarp();
+  if (sst.n == 7) {  // the next n = 7 moment J-pass's prologue at x_eval
+    gauss2d_prologue_warp(sst.x_eval, sst.pre);
+    if (lane == 0) sst.has_pre = 1;
   }
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
   if (lane == 0) {
@@ -1502,9 +1503,10 @@ __device__ __noinline__ void fused_solver_step(FitState* __restrict__ st, const 
   }
   __syncwarp();
   solver_step<NC>(&sst, S, S.kvs, true);
-  if (lane == 0 && sst.n == 7) {  // the next pass's prologue at x_eval
-    gauss2d_prologue(sst.x_eval, sst.pre);
-    sst.has_pre = 1;
+  __syncwarp();
+  if (sst.n == 7) {  // the next pass's prologue at x_eval
+    gauss2d_prologue_warp(sst.x_eval, sst.pre);
+    if (lane == 0) sst.has_pre = 1;
   }
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
   if (lane == 0) {

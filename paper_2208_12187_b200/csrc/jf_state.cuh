@@ -90,5 +90,33 @@ __host__ __device__ inline void gauss2d_prologue(const double* x, double* pre) {
   pre[6] = x[6];
   pre[7] = exp(-2.0 * a * 32.0 * 32.0);
 }
+#ifdef __CUDACC__
+// The same on a whole warp (lane values equal on entry): cos, sin and the two
+// reciprocals on four lanes at once, the rest on every lane (identical bits);
+// lane 0 writes pre.
+__device__ __forceinline__ void gauss2d_prologue_warp(const double* x, double* pre) {
+  const int lane = threadIdx.x & 31;
+  const double sx = x[3], sy = x[4], th = x[5];
+  double v = 0.0;
+  if (lane == 0) v = cos(th);
+  else if (lane == 1) v = sin(th);
+  else if (lane == 2) v = 0.5 / (sx * sx);
+  else if (lane == 3) v = 0.5 / (sy * sy);
+  const double C = __shfl_sync(0xffffffffu, v, 0), S = __shfl_sync(0xffffffffu, v, 1);
+  const double ix = __shfl_sync(0xffffffffu, v, 2), iy = __shfl_sync(0xffffffffu, v, 3);
+  const double CC = C * C, SS = S * S;
+  const double a = CC * ix + SS * iy;
+  if (lane == 0) {
+    pre[0] = x[0];
+    pre[1] = x[1];
+    pre[2] = x[2];
+    pre[3] = a;
+    pre[4] = 2.0 * ((S * C) * (iy - ix));
+    pre[5] = SS * ix + CC * iy;
+    pre[6] = x[6];
+    pre[7] = exp(-2.0 * a * 32.0 * 32.0);
+  }
+}
+#endif
 
 }  // namespace jf
