@@ -1327,10 +1327,210 @@ __device__ __noinline__ void st_pcov(FitState* st, SolverSmem& S) {
   __syncwarp();
 }
 
+// Warp fast path of the most common solver step: in a speculative,
+// unbounded, Gram-mode fit, the J-pass at the trial point is accepted
+// without a termination test firing and the next trial is a certified
+// Gauss-Newton step inside the new radius (every step of every BASELINE fit
+// after the first).  Bitwise the same arithmetic, in the same order, as the
+// general path fit_after_pass -> st_after_trial -> st_end_inner ->
+// st_outer_top -> gn_fastpath -> st_trial_finish, with the independent parts
+// on the warp's lanes (lane i: row i of B_hat, of the Cholesky factor, the
+// forward substitution; lane c: column c of L^-1) and over shared memory
+// rather than lane 0's long serial chain.  Everything is decided before the
+// state is written: any other case (rejection, termination, AUTO re-check,
+// no certified Gauss-Newton step) returns false and the general path runs
+// from the untouched state.  All lanes call it.
+template <int n>
+__device__ __noinline__ bool warp_gn_step(FitState* st, SolverSmem& S, const double* kv) {
+  const int lane = threadIdx.x & 31;
+  if (st->phase != PH_TRIAL_J || st->bounded || st->qr_mode || st->policy != 0 || st->trace_cap > 0 ||
+      st->status != STATUS_NONE)
+    return false;
+  if (kv[tri_count(n)] != 0.0) return false;  // R17 path
+  // ---- st_after_trial (read-only)
+  const double cost_new = 0.5 * kv[tri_slot(n, n, n)];
+  const double cost = st->cost;
+  const double actual = cost - cost_new;
+  const double pred_old = st->pred;
+  double ratio;
+  if (pred_old > 0.0) ratio = actual / pred_old;
+  else if (pred_old == 0.0 && actual == 0.0) ratio = 1.0;
+  else ratio = 0.0;
+  const double Delta = st->Delta, hn_old = st->hn;
+  double Delta_new = Delta;
+  if (ratio < 0.25) Delta_new = 0.25 * hn_old;
+  else if (ratio > 0.75 && hn_old > 0.95 * Delta) Delta_new = 2.0 * Delta;
+  const double xnorm = vnorm<n>(st->x);
+  const bool ft = actual < st->ftol * cost && ratio > 0.25;
+  const bool xt = st->step_norm < st->xtol * (st->xtol + xnorm);
+  if (ft || xt || !(actual > 0.0)) return false;
+  const int nfev = st->nfev + 1;
+  if (nfev == st->max_nfev) return false;
+  if (st->auto_mode && !(st->kappa2_gn <= 1.0e6)) return false;  // AUTO re-check: general path
+  // ---- the accepted point: g, G from the K-vector, scale, gnorm (lane j: entry j)
+  double gj = 0.0, si = 1.0, dd = 0.0;
+  if (lane < n) {
+    gj = kv[tri_slot(n, lane, n)];
+    const double sq = sqrt(kv[tri_slot(n, lane, lane)]);
+    si = st->jacmode ? fmax(sq, st->scale_inv[lane]) : st->scale_inv[lane];
+    dd = 1.0 / si;
+    S.w1[lane] = gj;
+  }
+  __syncwarp();
+  double gnorm = 0.0;
+  for (int j = 0; j < n; ++j) gnorm = fmax(gnorm, fabs(S.w1[j] * 1.0));
+  if (gnorm < st->gtol) return false;  // gtol termination: general path
+  // B_hat = d G d (+ diag_h = 0 on the diagonal; row i on lane i), g_hat
+  if (lane < n) S.w2[lane] = dd;
+  __syncwarp();
+  if (lane < n) {
+    for (int j = 0; j < n; ++j) {
+      const int a = lane < j ? lane : j, b = lane < j ? j : lane;
+      double bij = dd * kv[tri_slot(n, a, b)] * S.w2[j];
+      if (lane == j) bij += 0.0;
+      S.M[lane][j] = bij;
+    }
+    S.w3[lane] = dd * gj;  // g_hat
+  }
+  __syncwarp();
+  // ---- gn_fastpath: Cholesky (left-looking, column k: lane i >= k forms its
+  // entry with the same j order as chol_reg), L in S.T (lower)
+  double tr = 0.0;
+  for (int i = 0; i < n; ++i) tr += S.M[i][i];
+  double* cinv = S.w4;
+  bool spd = true;
+  for (int k = 0; k < n; ++k) {
+    double t = 0.0;
+    if (lane >= k && lane < n) {
+      t = S.M[lane][k];
+      for (int j = 0; j < k; ++j) t = fma(-S.T[lane][j], S.T[k][j], t);
+    }
+    const double d = __shfl_sync(FULL, t, k);
+    if (!(d > 0.0)) {
+      spd = false;
+      break;
+    }
+    const double r = rsqrt(d);
+    if (lane == k) {
+      S.T[k][k] = d * r;
+      cinv[k] = r;
+    } else if (lane > k && lane < n) {
+      S.T[lane][k] = t * r;
+    }
+    __syncwarp();
+  }
+  if (!spd) return false;
+  // Y = L^-1 (column c on lane c), ||Y||_F^2 summed in inv_fro2's order
+  if (lane < n) {
+    const int c = lane;
+    for (int i = c; i < n; ++i) {
+      double t = (i == c) ? 1.0 : 0.0;
+      for (int k = c; k < i; ++k) t = fma(-S.T[i][k], S.M2[k][c], t);
+      S.M2[i][c] = t * cinv[i];
+    }
+  }
+  __syncwarp();
+  double fro = 0.0;
+  for (int c = 0; c < n; ++c)
+    for (int i = c; i < n; ++i) fro = fma(S.M2[i][c], S.M2[i][c], fro);
+  const int64_t m = st->m_global;
+  if (!(m >= n && rsqrt(fro) > 2.0 * DBL_EPSILON * (double)m * sqrt(tr))) return false;
+  // L w = -g_hat (lane i accumulates row i as w_k become known, k increasing)
+  double t = (lane < n) ? -S.w3[lane] : 0.0;
+  for (int k = 0; k < n; ++k) {
+    const double wk = __shfl_sync(FULL, t * cinv[k], k);
+    if (lane > k && lane < n) t = fma(-S.T[lane][k], wk, t);
+    if (lane == k) S.w5[k] = wk;
+  }
+  __syncwarp();
+  // L^T p = w (gn_fastpath's order: k increasing from i + 1), serial
+  double* pr = S.A[0];  // (scratch row)
+  double pn = 0.0;
+  if (lane == 0) {
+    for (int i = n - 1; i >= 0; --i) {
+      double u = S.w5[i];
+      for (int k = i + 1; k < n; ++k) u = fma(-S.T[k][i], pr[k], u);
+      pr[i] = u * cinv[i];
+    }
+    for (int i = 0; i < n; ++i) pn = fma(pr[i], pr[i], pn);
+  }
+  pn = __shfl_sync(FULL, pn, 0);
+  __syncwarp();
+  if (!(sqrt(pn) <= Delta_new)) return false;
+  // pred = -(0.5 p^T B p + p^T g_hat): rows of B p on the lanes, sums in vquad's order
+  if (lane < n) {
+    double r = 0.0;
+    for (int k = 0; k < n; ++k) r = fma(S.M[lane][k], pr[k], r);
+    S.V[0][lane] = r;
+  }
+  __syncwarp();
+  // ---- commit (the general path's state, field by field)
+  if (lane == 0) {
+    double q = 0.0;
+    for (int i = 0; i < n; ++i) q = fma(pr[i], S.V[0][i], q);
+    double gp = 0.0;
+    for (int j = 0; j < n; ++j) gp = fma(pr[j], S.w3[j], gp);
+    const double pred = -(0.5 * q + gp);
+    const int KS = tri_count(n) + 1;
+    for (int k = 0; k < KS; ++k) st->kv[k] = kv[k];
+    st->launches = st->launches + 1;
+    st->nfev = nfev;
+    st->cost_new = cost_new;
+    st->ratio = ratio;
+    st->alpha = st->alpha * (Delta / Delta_new);
+    st->Delta = Delta_new;
+    st->cost = cost_new;
+    st->njev = st->njev + 1;
+    st->nit = st->nit + 1;
+    st->gnorm = gnorm;
+    st->theta = fmax(0.995, 1.0 - gnorm);
+    st->actual = -1.0;
+    st->have_eig = 0;
+    st->kappa2_gn = tr * fro;
+    st->alpha = 0.0;
+    st->pred = pred;
+    double h2 = 0.0, s2 = 0.0;
+    for (int j = 0; j < n; ++j) {
+      const double dj = S.w2[j];
+      const double stp = dj * pr[j];
+      st->step_h[j] = pr[j];
+      st->step[j] = stp;
+      st->x[j] = st->x_eval[j];
+      st->x_eval[j] = st->x[j] + stp;
+      h2 = fma(pr[j], pr[j], h2);
+      s2 = fma(stp, stp, s2);
+    }
+    st->hn = sqrt(h2);
+    st->step_norm = sqrt(s2);
+    st->Delta_used = Delta_new;
+    st->branch = -1;
+    st->phase = PH_TRIAL_J;
+  }
+  if (lane < n) {
+    st->g[lane] = gj;
+    st->scale_inv[lane] = si;
+    st->d[lane] = dd;
+    st->diag_h[lane] = 0.0;
+    st->gh[lane] = S.w3[lane];
+    for (int j = 0; j < n; ++j) {
+      const int a = lane < j ? lane : j, b = lane < j ? j : lane;
+      st->G[lane * NMAX + j] = kv[tri_slot(n, a, b)];
+      st->Gh[lane * NMAX + j] = S.M[lane][j];
+    }
+  }
+  __syncwarp();
+  return true;
+}
+
 template <int n>
 __device__ __forceinline__ void solver_step_n(FitState* st, SolverSmem& S, const double* kv, bool jac) {
   const int lane = threadIdx.x & 31;
   const long long c0 = clock64();
+  if (jac && warp_gn_step<n>(st, S, kv)) {  // (the common step, on the whole warp)
+    if (lane == 0) st->prof[3] += clock64() - c0;
+    __syncwarp();
+    return;
+  }
   if (lane == 0) fit_after_pass<n>(st, S, kv, jac);
   __syncwarp();
   if (S.need_trial && S.need_eig && st->qr_mode) {
@@ -1477,6 +1677,9 @@ __device__ __noinline__ void fused_solver_step(FitState* __restrict__ st, const 
   SolverSmem& S = *reinterpret_cast<SolverSmem*>(fused_dyn);
   FitState& sst = *reinterpret_cast<FitState*>(fused_dyn + ((sizeof(SolverSmem) + 15) & ~(size_t)15));
   const int lane = threadIdx.x & 31;
+#if JF_DEV
+  const long long dvs = clock64();
+#endif
   unsigned long long t0, t1;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   constexpr int NW = sizeof(FitState) / 8;
@@ -1496,6 +1699,9 @@ __device__ __noinline__ void fused_solver_step(FitState* __restrict__ st, const 
   }
   for (int k = lane; k < KMAX; k += 32) S.kvs[k] = vec[k];
   __syncwarp();
+#if JF_DEV
+  const long long dv0 = clock64();
+#endif
   if (lane == 0) {
     const int k = sst.tl_n;
     if (k < 64) sst.tl[k] = t0;
@@ -1504,10 +1710,19 @@ __device__ __noinline__ void fused_solver_step(FitState* __restrict__ st, const 
   __syncwarp();
   solver_step<NC>(&sst, S, S.kvs, true);
   __syncwarp();
+#if JF_DEV
+  const long long dv1 = clock64();
+#endif
   if (sst.n == 7) {  // the next pass's prologue at x_eval
     gauss2d_prologue_warp(sst.x_eval, sst.pre);
     if (lane == 0) sst.has_pre = 1;
   }
+#if JF_DEV  // development: cycles of the state load (prof[0]) and of the prologue (prof[2])
+  if (lane == 0) {
+    sst.prof[0] += dv0 - dvs;
+    sst.prof[2] += clock64() - dv1;
+  }
+#endif
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
   if (lane == 0) {
     sst.pass_ready = 0;
