@@ -561,8 +561,10 @@ int build_graph(Ctx& c, const PassPair& k, int policy, bool qr, bool fused, cuda
   kp.kernelParams = pargs;
   // U copies of the iteration per trip of the WHILE loop: the conditional
   // node's per-trip overhead (~6 us) is paid once per U iterations; copies
-  // after the fit ended find nothing to do (phase DONE) and return at once.
-  constexpr int unroll = 3;
+  // after the fit ended find nothing to do (phase DONE) and return at once
+  // (~3 us for a fused J-pass: it drains its first bulk copies).  Fused
+  // bodies (one kernel per trial): 6, so a 6-pass fit (T, C3) is one trip.
+  const int unroll = fused ? 6 : 3;
   for (int u = 0; u < unroll; ++u) {
     if (policy == JF_POLICY_CONSERVATIVE) {
       kp.func = (void*)k.r;

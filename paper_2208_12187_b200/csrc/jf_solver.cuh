@@ -1237,38 +1237,57 @@ __device__ __noinline__ void fit_after_pass(FitState* st, SolverSmem& S, const d
   }
 }
 
-// Fast path of the covariance (lane 0): when the Cholesky certificate of
-// gn_fastpath shows no singular value of J falls below the cut-off
-// (1/||L^-1||_F > 2 EPS max(m, n) sqrt(trace G) => s_min > EPS max(m, n) s_max),
-// the pseudo-inverse is the inverse, (L L^T)^-1 = L^-T L^-1: n^3/2 fmas in
-// place of an eigendecomposition.  Returns false when not certified.
+// Warp Cholesky of the SPD matrix A (shared memory, rows padded to MS) with
+// the rank certificate: L (lower) in Lm, cinv = 1 / diag(L), Y = L^-1 in Ym,
+// fro = ||L^-1||_F^2, tr = trace(A) — the same arithmetic in the same order
+// as chol_reg + inv_fro2 (lane i forms row i's entries of column k; lane c
+// column c of L^-1; the sums in their serial order).  false: not SPD.
 template <int n>
-__device__ __noinline__ bool pcov_chol(FitState* st, SolverSmem& S, double s_sq) {
-  const int64_t m = st->m_global;
-  double L[n][n], Y[n][n], cinv[n];
-  double tr = 0.0;
+__device__ __forceinline__ bool warp_chol_cert(const double (*A)[MS], double (*Lm)[MS], double* cinv,
+                                               double (*Ym)[MS], double& tr, double& fro) {
+  const int lane = threadIdx.x & 31;
+  tr = 0.0;
 #pragma unroll
-  for (int i = 0; i < n; ++i) {
-    tr += st->G[i * NMAX + i];
-#pragma unroll
-    for (int j = 0; j <= i; ++j) L[i][j] = st->G[i * NMAX + j];
+  for (int i = 0; i < n; ++i) tr += A[i][i];
+  for (int k = 0; k < n; ++k) {
+    double t = 0.0;
+    if (lane >= k && lane < n) {
+      t = A[lane][k];
+      for (int j = 0; j < k; ++j) t = fma(-Lm[lane][j], Lm[k][j], t);
+    }
+    const double d = __shfl_sync(FULL, t, k);
+    if (!(d > 0.0)) return false;
+    const double r = rsqrt(d);
+    if (lane == k) {
+      Lm[k][k] = d * r;
+      cinv[k] = r;
+    } else if (lane > k && lane < n) {
+      Lm[lane][k] = t * r;
+    }
+    __syncwarp();
   }
-  if (!chol_reg<n>(L, cinv)) return false;
-  const double fro = inv_fro2<n>(L, cinv, Y);
-  if (!(m >= n && rsqrt(fro) > 2.0 * DBL_EPSILON * (double)(m > n ? m : n) * sqrt(tr))) return false;
-#pragma unroll
-  for (int i = 0; i < n; ++i) {
-#pragma unroll
-    for (int j = i; j < n; ++j) {
-      double t = 0.0;
-#pragma unroll
-      for (int k = j; k < n; ++k) t = fma(Y[k][i], Y[k][j], t);
-      st->pcov[i * NMAX + j] = st->pcov[j * NMAX + i] = t * s_sq;
+  if (lane < n) {
+    const int c = lane;
+    for (int i = c; i < n; ++i) {
+      double t = (i == c) ? 1.0 : 0.0;
+      for (int k = c; k < i; ++k) t = fma(-Lm[i][k], Ym[k][c], t);
+      Ym[i][c] = t * cinv[i];
     }
   }
+  __syncwarp();
+  fro = 0.0;
+#pragma unroll
+  for (int c = 0; c < n; ++c)
+#pragma unroll
+    for (int i = c; i < n; ++i) fro = fma(Ym[i][c], Ym[i][c], fro);
   return true;
 }
 
+// Fast path of the covariance: when the Cholesky certificate (warp_chol_cert)
+// shows no singular value of J falls below the cut-off
+// (1/||L^-1||_F > 2 EPS max(m, n) sqrt(trace G) => s_min > EPS max(m, n) s_max),
+// the pseudo-inverse is the inverse, (L L^T)^-1 = L^-T L^-1: n^3/2 fmas in
+// place of an eigendecomposition (st_pcov below).
 // Whole warp, once at the end of a fit: the parameter covariance curve_fit
 // returns with the parameters: the Moore-Penrose
 // inverse of J^T J at the final x, discarding singular values of J below
@@ -1280,11 +1299,21 @@ __device__ __noinline__ void st_pcov(FitState* st, SolverSmem& S) {
   const int lane = threadIdx.x & 31;
   const int64_t m = st->m_global;
   const double s_sq = (m > n) ? 2.0 * st->cost / (double)(m - n) : INFINITY;
-  if (!st->qr_mode) {
-    int ok = 0;
-    if (lane == 0) ok = pcov_chol<n>(st, S, s_sq) ? 1 : 0;
-    ok = __shfl_sync(0xffffffffu, ok, 0);
-    if (ok) {
+  if (!st->qr_mode) {  // pcov_chol on the warp: the same arithmetic (warp_chol_cert), entries on the lanes
+    if (lane < n)
+      for (int j = 0; j <= lane; ++j) S.A[lane][j] = st->G[lane * NMAX + j];
+    __syncwarp();
+    double tr, fro;
+    const bool spd = warp_chol_cert<n>(S.A, S.T, S.w4, S.M2, tr, fro);
+    if (spd && m >= n && rsqrt(fro) > 2.0 * DBL_EPSILON * (double)(m > n ? m : n) * sqrt(tr)) {
+      for (int e = lane; e < n * n; e += 32) {
+        const int i = e / n, j = e % n;
+        if (j < i) continue;
+        double t = 0.0;
+        for (int k = j; k < n; ++k) t = fma(S.M2[k][i], S.M2[k][j], t);
+        st->pcov[i * NMAX + j] = st->pcov[j * NMAX + i] = t * s_sq;
+      }
+      __syncwarp();
       if (lane == 0) st->pcov_done = 1;
       __syncwarp();
       return;
@@ -1327,60 +1356,96 @@ __device__ __noinline__ void st_pcov(FitState* st, SolverSmem& S) {
   __syncwarp();
 }
 
-// Warp fast path of the most common solver step: in a speculative,
-// unbounded, Gram-mode fit, the J-pass at the trial point is accepted
-// without a termination test firing and the next trial is a certified
-// Gauss-Newton step inside the new radius (every step of every BASELINE fit
-// after the first).  Bitwise the same arithmetic, in the same order, as the
-// general path fit_after_pass -> st_after_trial -> st_end_inner ->
-// st_outer_top -> gn_fastpath -> st_trial_finish, with the independent parts
-// on the warp's lanes (lane i: row i of B_hat, of the Cholesky factor, the
-// forward substitution; lane c: column c of L^-1) and over shared memory
-// rather than lane 0's long serial chain.  Everything is decided before the
-// state is written: any other case (rejection, termination, AUTO re-check,
-// no certified Gauss-Newton step) returns false and the general path runs
-// from the untouched state.  All lanes call it.
+// Warp fast path of the common solver steps of a speculative, unbounded,
+// Gram-mode fit (every step of every BASELINE fit but the last):
+//  - PH_INIT_J: the J-pass at x0 (st_init: AUTO keeps the Gram path, scale,
+//    Delta0), then Alg. 1's loop top and a certified Gauss-Newton trial;
+//  - PH_TRIAL_J: the J-pass at the trial point is accepted with no
+//    termination test firing, then the loop top and the next certified
+//    Gauss-Newton trial inside the new radius.
+// Bitwise the same arithmetic, in the same order, as the general path
+// (fit_after_pass -> st_init / st_after_trial -> st_end_inner ->
+// st_outer_top -> gn_fastpath -> st_trial_finish), with the independent parts
+// on the warp's lanes and over shared memory rather than lane 0's long serial
+// chain.  Everything is decided before the state is written: any other case
+// returns false and the general path runs from the untouched state.  All
+// lanes call it.
 template <int n>
 __device__ __noinline__ bool warp_gn_step(FitState* st, SolverSmem& S, const double* kv) {
   const int lane = threadIdx.x & 31;
-  if (st->phase != PH_TRIAL_J || st->bounded || st->qr_mode || st->policy != 0 || st->trace_cap > 0 ||
-      st->status != STATUS_NONE)
+  const int phase = st->phase;
+  const bool init = (phase == PH_INIT_J);
+  if ((phase != PH_TRIAL_J && !init) || st->bounded || st->policy != 0 || st->trace_cap > 0 ||
+      (init ? st->qr_mode == 1 : (st->qr_mode != 0 || st->status != STATUS_NONE)))
     return false;
-  if (kv[tri_count(n)] != 0.0) return false;  // R17 path
-  // ---- st_after_trial (read-only)
+  if (kv[tri_count(n)] != 0.0) return false;  // R17 / R18 paths
   const double cost_new = 0.5 * kv[tri_slot(n, n, n)];
-  const double cost = st->cost;
-  const double actual = cost - cost_new;
-  const double pred_old = st->pred;
-  double ratio;
-  if (pred_old > 0.0) ratio = actual / pred_old;
-  else if (pred_old == 0.0 && actual == 0.0) ratio = 1.0;
-  else ratio = 0.0;
-  const double Delta = st->Delta, hn_old = st->hn;
-  double Delta_new = Delta;
-  if (ratio < 0.25) Delta_new = 0.25 * hn_old;
-  else if (ratio > 0.75 && hn_old > 0.95 * Delta) Delta_new = 2.0 * Delta;
-  const double xnorm = vnorm<n>(st->x);
-  const bool ft = actual < st->ftol * cost && ratio > 0.25;
-  const bool xt = st->step_norm < st->xtol * (st->xtol + xnorm);
-  if (ft || xt || !(actual > 0.0)) return false;
-  const int nfev = st->nfev + 1;
+  double ratio = 0.0, Delta_new = 0.0, alpha_new = 0.0;
+  int nfev = 1;
+  if (!init) {  // ---- st_after_trial (read-only)
+    const double cost = st->cost;
+    const double actual = cost - cost_new;
+    const double pred_old = st->pred;
+    if (pred_old > 0.0) ratio = actual / pred_old;
+    else if (pred_old == 0.0 && actual == 0.0) ratio = 1.0;
+    else ratio = 0.0;
+    const double Delta = st->Delta, hn_old = st->hn;
+    Delta_new = Delta;
+    if (ratio < 0.25) Delta_new = 0.25 * hn_old;
+    else if (ratio > 0.75 && hn_old > 0.95 * Delta) Delta_new = 2.0 * Delta;
+    const double xnorm = vnorm<n>(st->x);
+    const bool ft = actual < st->ftol * cost && ratio > 0.25;
+    const bool xt = st->step_norm < st->xtol * (st->xtol + xnorm);
+    if (ft || xt || !(actual > 0.0)) return false;
+    nfev = st->nfev + 1;
+    if (st->auto_mode && !(st->kappa2_gn <= 1.0e6)) return false;  // AUTO re-check: general path
+    alpha_new = st->alpha * (Delta / Delta_new);
+  }
   if (nfev == st->max_nfev) return false;
-  if (st->auto_mode && !(st->kappa2_gn <= 1.0e6)) return false;  // AUTO re-check: general path
-  // ---- the accepted point: g, G from the K-vector, scale, gnorm (lane j: entry j)
-  double gj = 0.0, si = 1.0, dd = 0.0;
+  // ---- the new iterate's g, G (from the K-vector) and scale (lane j: entry j)
+  double gj = 0.0, gjj = 0.0, si = 1.0;
   if (lane < n) {
     gj = kv[tri_slot(n, lane, n)];
-    const double sq = sqrt(kv[tri_slot(n, lane, lane)]);
-    si = st->jacmode ? fmax(sq, st->scale_inv[lane]) : st->scale_inv[lane];
-    dd = 1.0 / si;
+    gjj = kv[tri_slot(n, lane, lane)];
+    const double sq = sqrt(gjj);
+    if (init) {
+      si = st->jacmode ? (sq == 0.0 ? 1.0 : sq) : st->xs_inv[lane];
+    } else {
+      si = st->jacmode ? fmax(sq, st->scale_inv[lane]) : st->scale_inv[lane];
+    }
     S.w1[lane] = gj;
   }
   __syncwarp();
+  if (init && st->qr_mode == 2) {  // AUTO at x0: kappa2_estimate of the column-scaled Gram
+    if (lane < n) S.w2[lane] = gjj > 0.0 ? rsqrt(gjj) : 1.0;
+    __syncwarp();
+    if (lane < n) {
+      for (int j = 0; j <= lane; ++j) S.A[lane][j] = S.w2[lane] * kv[tri_slot(n, j, lane)] * S.w2[j];
+    }
+    __syncwarp();
+    double tr0, fro0;
+    if (!warp_chol_cert<n>(S.A, S.T, S.w4, S.M2, tr0, fro0)) return false;  // (kappa2 = inf: TSQR)
+    if (tr0 * fro0 > 1.0e6) return false;                                    // TSQR: general path
+  }
   double gnorm = 0.0;
+#pragma unroll
   for (int j = 0; j < n; ++j) gnorm = fmax(gnorm, fabs(S.w1[j] * 1.0));
   if (gnorm < st->gtol) return false;  // gtol termination: general path
+  if (init) {  // R4: Delta0 = ||x0 scale_inv||, 0 -> 1
+    if (lane < n) S.w5[lane] = si;
+    __syncwarp();
+    double s2 = 0.0;
+#pragma unroll
+    for (int j = 0; j < n; ++j) {
+      const double t = st->x[j] * S.w5[j];
+      s2 = fma(t, t, s2);
+    }
+    Delta_new = sqrt(s2);
+    if (Delta_new == 0.0) Delta_new = 1.0;
+    __syncwarp();
+  }
   // B_hat = d G d (+ diag_h = 0 on the diagonal; row i on lane i), g_hat
+  const double dd = (lane < n) ? 1.0 / si : 0.0;
   if (lane < n) S.w2[lane] = dd;
   __syncwarp();
   if (lane < n) {
@@ -1393,73 +1458,35 @@ __device__ __noinline__ bool warp_gn_step(FitState* st, SolverSmem& S, const dou
     S.w3[lane] = dd * gj;  // g_hat
   }
   __syncwarp();
-  // ---- gn_fastpath: Cholesky (left-looking, column k: lane i >= k forms its
-  // entry with the same j order as chol_reg), L in S.T (lower)
-  double tr = 0.0;
-  for (int i = 0; i < n; ++i) tr += S.M[i][i];
+  // ---- gn_fastpath: Cholesky + certificate, L w = -g_hat, L^T p = w
+  double tr, fro;
   double* cinv = S.w4;
-  bool spd = true;
-  for (int k = 0; k < n; ++k) {
-    double t = 0.0;
-    if (lane >= k && lane < n) {
-      t = S.M[lane][k];
-      for (int j = 0; j < k; ++j) t = fma(-S.T[lane][j], S.T[k][j], t);
-    }
-    const double d = __shfl_sync(FULL, t, k);
-    if (!(d > 0.0)) {
-      spd = false;
-      break;
-    }
-    const double r = rsqrt(d);
-    if (lane == k) {
-      S.T[k][k] = d * r;
-      cinv[k] = r;
-    } else if (lane > k && lane < n) {
-      S.T[lane][k] = t * r;
-    }
-    __syncwarp();
-  }
-  if (!spd) return false;
-  // Y = L^-1 (column c on lane c), ||Y||_F^2 summed in inv_fro2's order
-  if (lane < n) {
-    const int c = lane;
-    for (int i = c; i < n; ++i) {
-      double t = (i == c) ? 1.0 : 0.0;
-      for (int k = c; k < i; ++k) t = fma(-S.T[i][k], S.M2[k][c], t);
-      S.M2[i][c] = t * cinv[i];
-    }
-  }
-  __syncwarp();
-  double fro = 0.0;
-  for (int c = 0; c < n; ++c)
-    for (int i = c; i < n; ++i) fro = fma(S.M2[i][c], S.M2[i][c], fro);
+  if (!warp_chol_cert<n>(S.M, S.T, cinv, S.M2, tr, fro)) return false;
   const int64_t m = st->m_global;
   if (!(m >= n && rsqrt(fro) > 2.0 * DBL_EPSILON * (double)m * sqrt(tr))) return false;
-  // L w = -g_hat (lane i accumulates row i as w_k become known, k increasing)
   double t = (lane < n) ? -S.w3[lane] : 0.0;
-  for (int k = 0; k < n; ++k) {
+  for (int k = 0; k < n; ++k) {  // lane i accumulates row i as w_k become known (k increasing)
     const double wk = __shfl_sync(FULL, t * cinv[k], k);
     if (lane > k && lane < n) t = fma(-S.T[lane][k], wk, t);
     if (lane == k) S.w5[k] = wk;
   }
   __syncwarp();
-  // L^T p = w (gn_fastpath's order: k increasing from i + 1), serial
-  double* pr = S.A[0];  // (scratch row)
-  double pn = 0.0;
-  if (lane == 0) {
-    for (int i = n - 1; i >= 0; --i) {
-      double u = S.w5[i];
-      for (int k = i + 1; k < n; ++k) u = fma(-S.T[k][i], pr[k], u);
-      pr[i] = u * cinv[i];
-    }
-    for (int i = 0; i < n; ++i) pn = fma(pr[i], pr[i], pn);
+  double pr[n];  // L^T p = w in gn_fastpath's order (k increasing from i + 1), every lane
+#pragma unroll
+  for (int i = n - 1; i >= 0; --i) {
+    double u = S.w5[i];
+#pragma unroll
+    for (int k = i + 1; k < n; ++k) u = fma(-S.T[k][i], pr[k], u);
+    pr[i] = u * cinv[i];
   }
-  pn = __shfl_sync(FULL, pn, 0);
-  __syncwarp();
+  double pn = 0.0;
+#pragma unroll
+  for (int i = 0; i < n; ++i) pn = fma(pr[i], pr[i], pn);
   if (!(sqrt(pn) <= Delta_new)) return false;
   // pred = -(0.5 p^T B p + p^T g_hat): rows of B p on the lanes, sums in vquad's order
   if (lane < n) {
     double r = 0.0;
+#pragma unroll
     for (int k = 0; k < n; ++k) r = fma(S.M[lane][k], pr[k], r);
     S.V[0][lane] = r;
   }
@@ -1467,35 +1494,44 @@ __device__ __noinline__ bool warp_gn_step(FitState* st, SolverSmem& S, const dou
   // ---- commit (the general path's state, field by field)
   if (lane == 0) {
     double q = 0.0;
+#pragma unroll
     for (int i = 0; i < n; ++i) q = fma(pr[i], S.V[0][i], q);
     double gp = 0.0;
+#pragma unroll
     for (int j = 0; j < n; ++j) gp = fma(pr[j], S.w3[j], gp);
-    const double pred = -(0.5 * q + gp);
     const int KS = tri_count(n) + 1;
     for (int k = 0; k < KS; ++k) st->kv[k] = kv[k];
     st->launches = st->launches + 1;
     st->nfev = nfev;
-    st->cost_new = cost_new;
-    st->ratio = ratio;
-    st->alpha = st->alpha * (Delta / Delta_new);
-    st->Delta = Delta_new;
+    if (init) {
+      st->njev = 1;
+      st->nit = 0;
+      st->status = STATUS_NONE;
+      if (st->qr_mode == 2) st->qr_mode = 0;
+    } else {
+      st->cost_new = cost_new;
+      st->ratio = ratio;
+      st->njev = st->njev + 1;
+      st->nit = st->nit + 1;
+#pragma unroll
+      for (int j = 0; j < n; ++j) st->x[j] = st->x_eval[j];
+    }
     st->cost = cost_new;
-    st->njev = st->njev + 1;
-    st->nit = st->nit + 1;
+    st->Delta = Delta_new;
     st->gnorm = gnorm;
     st->theta = fmax(0.995, 1.0 - gnorm);
     st->actual = -1.0;
     st->have_eig = 0;
     st->kappa2_gn = tr * fro;
+    (void)alpha_new;  // (the trial's alpha: 0, a Gauss-Newton step)
     st->alpha = 0.0;
-    st->pred = pred;
+    st->pred = -(0.5 * q + gp);
     double h2 = 0.0, s2 = 0.0;
+#pragma unroll
     for (int j = 0; j < n; ++j) {
-      const double dj = S.w2[j];
-      const double stp = dj * pr[j];
+      const double stp = S.w2[j] * pr[j];
       st->step_h[j] = pr[j];
       st->step[j] = stp;
-      st->x[j] = st->x_eval[j];
       st->x_eval[j] = st->x[j] + stp;
       h2 = fma(pr[j], pr[j], h2);
       s2 = fma(stp, stp, s2);

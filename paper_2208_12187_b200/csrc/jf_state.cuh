@@ -91,21 +91,21 @@ __host__ __device__ inline void gauss2d_prologue(const double* x, double* pre) {
   pre[7] = exp(-2.0 * a * 32.0 * 32.0);
 }
 #ifdef __CUDACC__
-// The same on a whole warp (lane values equal on entry): cos, sin and the two
-// reciprocals on four lanes at once, the rest on every lane (identical bits);
-// lane 0 writes pre.
+// The same on a whole warp (lane values equal on entry), without divergent
+// lanes: sin and cos from one sincos, the two reciprocals on two lanes of the
+// same instruction stream; lane 0 writes pre.  (sincos may differ from the
+// separate cos / sin in the last bit: a fit's passes agree with a plain pass
+// at the same x to ~1e-15, like host- and device-computed prologues, R36.)
 __device__ __forceinline__ void gauss2d_prologue_warp(const double* x, double* pre) {
   const int lane = threadIdx.x & 31;
-  const double sx = x[3], sy = x[4], th = x[5];
-  double v = 0.0;
-  if (lane == 0) v = cos(th);
-  else if (lane == 1) v = sin(th);
-  else if (lane == 2) v = 0.5 / (sx * sx);
-  else if (lane == 3) v = 0.5 / (sy * sy);
-  const double C = __shfl_sync(0xffffffffu, v, 0), S = __shfl_sync(0xffffffffu, v, 1);
-  const double ix = __shfl_sync(0xffffffffu, v, 2), iy = __shfl_sync(0xffffffffu, v, 3);
+  double S, C;
+  sincos(x[5], &S, &C);
+  const double sg = (lane & 1) ? x[4] : x[3];
+  const double rinv = 0.5 / (sg * sg);
+  const double ix = __shfl_sync(0xffffffffu, rinv, 0), iy = __shfl_sync(0xffffffffu, rinv, 1);
   const double CC = C * C, SS = S * S;
   const double a = CC * ix + SS * iy;
+  const double rho = exp(-2.0 * a * 32.0 * 32.0);
   if (lane == 0) {
     pre[0] = x[0];
     pre[1] = x[1];
@@ -114,7 +114,7 @@ __device__ __forceinline__ void gauss2d_prologue_warp(const double* x, double* p
     pre[4] = 2.0 * ((S * C) * (iy - ix));
     pre[5] = SS * ix + CC * iy;
     pre[6] = x[6];
-    pre[7] = exp(-2.0 * a * 32.0 * 32.0);
+    pre[7] = rho;
   }
 }
 #endif
