@@ -25,6 +25,10 @@
 #include "jf_kernels.h"
 #include "jf_state.cuh"
 
+#ifndef JF_DEV
+#define JF_DEV 0
+#endif
+
 using namespace jf;
 
 namespace {
@@ -506,8 +510,12 @@ int build_graph(Ctx& c, const PassPair& k, int policy, bool qr, bool fused, cuda
   cp.conditional.handle = h;
   cp.conditional.type = cudaGraphCondTypeWhile;
   cp.conditional.size = 1;
-  cudaGraphNode_t cn;
-  CK(cudaGraphAddNode(&cn, g, nullptr, 0, &cp));
+  // the fit's initial state in (the host-written prefix) and the final state
+  // out are nodes of the graph too: one launch per fit
+  cudaGraphNode_t up, cn, down;
+  CK(cudaGraphAddMemcpyNode1D(&up, g, nullptr, 0, c.d_state, c.h_state, FITSTATE_UPLOAD, cudaMemcpyHostToDevice));
+  CK(cudaGraphAddNode(&cn, g, &up, 1, &cp));
+  CK(cudaGraphAddMemcpyNode1D(&down, g, &cn, 1, c.h_state, c.d_state, sizeof(FitState), cudaMemcpyDeviceToHost));
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   int use = 1;
   PassArgs* pa = c.d_args;
@@ -760,6 +768,14 @@ int32_t jf_pass_device(int32_t model, const double* y, const double* z, int64_t 
 static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t m, const double* p0, int32_t n,
                         const double* lb, const double* ub, const jf_opts* opts, jf_result* out) {
   NvtxRange nv("jf_curve_fit");
+#if JF_DEV  // development: host-side phase times of a fit (stderr)
+  const auto hd0 = std::chrono::steady_clock::now();
+  auto hdt = [&]() { return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - hd0).count(); };
+  double hd[8] = {0};
+#define JF_HSTAMP(i) hd[i] = hdt()
+#else
+#define JF_HSTAMP(i) (void)0
+#endif
   auto fail = [&](int code) {
     out->status = code;
     return code;
@@ -904,8 +920,15 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
   // the cross-rank combine.
   const bool fused = k.fused && o.policy == JF_POLICY_SPECULATIVE && !o.comm;
   a.fused = fused ? 1 : 0;
+  JF_HSTAMP(0);
   auto t0 = std::chrono::steady_clock::now();
-  CK(cudaMemcpyAsync(c->d_state, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+  const int n64_est = 10 + 8 * n + (n + 1) * (n + 2) / 2;
+  constexpr double small_budget = 1.0e6;  // fp64 operations of one pass that one block absorbs
+  const bool small = !o.comm && o.policy == JF_POLICY_SPECULATIVE && kk.small &&
+                     (double)mg * n64_est <= small_budget;
+  if (small || !o.use_graph)  // (the fit graph copies the state in and out itself)
+    CK(cudaMemcpyAsync(c->d_state, &h, FITSTATE_UPLOAD, cudaMemcpyHostToDevice, s));  // (not the device-written bulk)
+  JF_HSTAMP(1);
   if (!c->h_args_valid || memcmp(c->h_args, &a, sizeof(a)) != 0) {  // a repeated fit skips the copy
     *c->h_args = a;
     c->h_args_valid = true;
@@ -913,10 +936,6 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
   }
   int launches = 0;
   // small m: the whole fit in one single-block kernel (state in shared memory)
-  const int n64_est = 10 + 8 * n + (n + 1) * (n + 2) / 2;
-  constexpr double small_budget = 1.0e6;  // fp64 operations of one pass that one block absorbs
-  const bool small = !o.comm && o.policy == JF_POLICY_SPECULATIVE && kk.small &&
-                     (double)mg * n64_est <= small_budget;
   if (small) {
     SmallFitFn f = sg.wsig ? kk.smallw : kk.small;
     f<<<1, 256, 0, s>>>(c->d_args, c->d_state);
@@ -936,9 +955,12 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
       out->graph_reused = 1;
     }
     nvtxRangePushA("fit graph (passes + solver steps on the device)");
-    CK(cudaGraphLaunch(ge, s));
-    CK(cudaMemcpyAsync(&h, c->d_state, sizeof(h), cudaMemcpyDeviceToHost, s));
+    JF_HSTAMP(2);
+    CK(cudaGraphLaunch(ge, s));  // (state in, passes + solver steps, state out)
+    JF_HSTAMP(3);
+    JF_HSTAMP(4);
     const cudaError_t we = stream_wait(s);
+    JF_HSTAMP(5);
     nvtxRangePop();
     CK(we);
   } else {
@@ -992,6 +1014,11 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
   if (h.error) return fail(h.error);
   if (h.cont) return fail(JF_ECUDA);  // loop did not terminate
   out->status = h.status;
+#if JF_DEV
+  JF_HSTAMP(6);
+  fprintf(stderr, "fit host us: setup %.1f h2d %.1f ->launch %.1f launch %.1f d2h-enq %.1f wait %.1f results %.1f\n", hd[0],
+          hd[1] - hd[0], hd[2] - hd[1], hd[3] - hd[2], hd[4] - hd[3], hd[5] - hd[4], hd[6] - hd[5]);
+#endif
   return h.status;
 }
 

@@ -3,6 +3,8 @@
 // (which read the phase and the point to evaluate) and the solver kernel.
 #pragma once
 
+#include <cstddef>
+
 #include "jf_common.cuh"
 
 namespace jf {
@@ -40,7 +42,6 @@ struct FitState {
   int32_t full_rank, branch, launches, have_V;
   int32_t kernels;     // kernel launches of this fit (pass kernels incl. predicated-out ones + solver kernels)
   int32_t tl_n;        // timeline entries written
-  unsigned long long tl[64];  // device timeline (globaltimer ns): pass start/end, solver start/end
   int32_t pass_ready;  // set by a pass kernel's last block: 1 J-pass, 2 r-pass result in kv_in
   int32_t have_eig;    // eigendecomposition of the current B_hat computed (lazy, per iteration)
   unsigned long long comm_epoch;
@@ -51,12 +52,10 @@ struct FitState {
   double pred, hn, step_norm, Delta_used, ratio;
   double kappa2_gn;  // cond(B_hat)^2 bound from the last Gauss-Newton Cholesky (tr B_hat ||L^-1||_F^2; +inf if none)
   double x[NMAX], x_eval[NMAX];
-  double g[NMAX], G[NMAX * NMAX], scale_inv[NMAX];
+  double g[NMAX], scale_inv[NMAX];
   // hat space of the current iterate (reused by rejected trials, R15)
-  double d[NMAX], diag_h[NMAX], gh[NMAX], Gh[NMAX * NMAX], lam[NMAX], V[NMAX * NMAX], suf[NMAX];
+  double d[NMAX], diag_h[NMAX], gh[NMAX], suf[NMAX];
   double step[NMAX], step_h[NMAX];
-  double kv[KMAX];  // K-vector of the last pass
-  double pcov[NMAX * NMAX];  // parameter covariance at the final x (curve_fit's pcov)
   int32_t pcov_done, qr_mode;  // qr_mode: TSQR (CholeskyQR2 + SVD of R) instead of the Gram eigensolver
   int32_t qr_after;            // what follows the PH_QR2 pass: 0 initialisation, 1 an accepted step
   int32_t qr_stage;            // 0: CholeskyQR2's second pass pending; 1, 2: shifted CholeskyQR3's
@@ -67,7 +66,16 @@ struct FitState {
   double* prec;                // = qr->prec (read by the preconditioned pass kernel)
   int32_t has_pre, pad_pre;    // pre: the n = 7 moment J-pass prologue at x_eval (gauss2d_prologue)
   double pre[8];
+  // ---- bulk: every entry is written on the device before it is read (the
+  // host uploads only the fields above, FITSTATE_UPLOAD bytes, per fit)
+  unsigned long long tl[64];  // device timeline (globaltimer ns): pass start/end, solver start/end
+  double G[NMAX * NMAX];      // J^T J at the current iterate
+  double Gh[NMAX * NMAX];     // B_hat of the current iterate
+  double lam[NMAX], V[NMAX * NMAX];  // its eigendecomposition (valid while have_eig / have_V)
+  double kv[KMAX];            // K-vector of the last pass
+  double pcov[NMAX * NMAX];   // parameter covariance at the final x (curve_fit's pcov)
 };
+constexpr size_t FITSTATE_UPLOAD = offsetof(FitState, tl);
 
 // The parameter-only prologue of the n = 7 moment J-pass (the rotated 2D
 // Gaussian, SPEC S:463 form; the expressions of Gauss2DComponent::prologue):
