@@ -295,3 +295,22 @@ def test_device_select_step_matches_oracle_all_branches():
         assert pred == pytest.approx(a[2], rel=1e-10, abs=1e-14)
         seen.add(br)
     assert seen == {0, 1, 2, 3}
+
+
+@pytest.mark.parametrize("name,make", [("C3 W=256", lambda: dg.make_gauss2d(256)),
+                                       ("C2 m=100000", lambda: dg.make_gauss1d(100_000)),
+                                       ("C1", lambda: dg.make_exp_decay()),
+                                       ("C5 W=128", lambda: dg.make_gauss2d_x2(128))])
+def test_warp_fast_path_equals_general_path(name, make):
+    """The solver's warp fast path (warp_gn_step: the initial step and every
+    accepted Gauss-Newton step of an unbounded Gram-mode fit) performs the
+    general path's arithmetic in the same order: a fit with a trace (which
+    keeps every step on the general path) equals the same fit without one
+    bitwise — x, cost, gradient, covariance and counts."""
+    pr = make()
+    kw = _kw(pr)
+    a = jf.curve_fit(pr.model, pr.z, p0=pr.p0, **kw)
+    b = jf.curve_fit(pr.model, pr.z, p0=pr.p0, trace_cap=256, **kw)
+    assert (a.status, a.nfev, a.njev, a.nit) == (b.status, b.nfev, b.njev, b.nit)
+    assert np.array_equal(a.x, b.x) and a.cost == b.cost
+    assert np.array_equal(a.grad, b.grad) and np.array_equal(a.pcov, b.pcov)
