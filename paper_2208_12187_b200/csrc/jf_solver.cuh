@@ -1373,6 +1373,9 @@ __device__ __noinline__ void st_pcov(FitState* st, SolverSmem& S) {
 template <int n>
 __device__ __noinline__ bool warp_gn_step(FitState* st, SolverSmem& S, const double* kv) {
   const int lane = threadIdx.x & 31;
+#if JF_DEV  // development: cycles of the phases (prof[1] decide + g/G, [4] B_hat + Cholesky, [6] solves, [7] pred + commit)
+  long long dq0 = clock64(), dq1 = 0, dq2 = 0, dq3 = 0;
+#endif
   const int phase = st->phase;
   const bool init = (phase == PH_INIT_J);
   if ((phase != PH_TRIAL_J && !init) || st->bounded || st->policy != 0 || st->trace_cap > 0 ||
@@ -1444,6 +1447,9 @@ __device__ __noinline__ bool warp_gn_step(FitState* st, SolverSmem& S, const dou
     if (Delta_new == 0.0) Delta_new = 1.0;
     __syncwarp();
   }
+#if JF_DEV
+  dq1 = clock64();
+#endif
   // B_hat = d G d (+ diag_h = 0 on the diagonal; row i on lane i), g_hat
   const double dd = (lane < n) ? 1.0 / si : 0.0;
   if (lane < n) S.w2[lane] = dd;
@@ -1464,6 +1470,9 @@ __device__ __noinline__ bool warp_gn_step(FitState* st, SolverSmem& S, const dou
   if (!warp_chol_cert<n>(S.M, S.T, cinv, S.M2, tr, fro)) return false;
   const int64_t m = st->m_global;
   if (!(m >= n && rsqrt(fro) > 2.0 * DBL_EPSILON * (double)m * sqrt(tr))) return false;
+#if JF_DEV
+  dq2 = clock64();
+#endif
   double t = (lane < n) ? -S.w3[lane] : 0.0;
   for (int k = 0; k < n; ++k) {  // lane i accumulates row i as w_k become known (k increasing)
     const double wk = __shfl_sync(FULL, t * cinv[k], k);
@@ -1483,6 +1492,9 @@ __device__ __noinline__ bool warp_gn_step(FitState* st, SolverSmem& S, const dou
 #pragma unroll
   for (int i = 0; i < n; ++i) pn = fma(pr[i], pr[i], pn);
   if (!(sqrt(pn) <= Delta_new)) return false;
+#if JF_DEV
+  dq3 = clock64();
+#endif
   // pred = -(0.5 p^T B p + p^T g_hat): rows of B p on the lanes, sums in vquad's order
   if (lane < n) {
     double r = 0.0;
@@ -1555,6 +1567,14 @@ __device__ __noinline__ bool warp_gn_step(FitState* st, SolverSmem& S, const dou
     }
   }
   __syncwarp();
+#if JF_DEV
+  if (lane == 0) {
+    st->prof[1] += dq1 - dq0;
+    st->prof[4] += dq2 - dq1;
+    st->prof[6] += dq3 - dq2;
+    st->prof[7] += clock64() - dq3;
+  }
+#endif
   return true;
 }
 
@@ -1769,11 +1789,19 @@ __device__ __noinline__ void fused_solver_step(FitState* __restrict__ st, const 
   }
   __syncwarp();
   unsigned long long* back = reinterpret_cast<unsigned long long*>(st);
+#if JF_DEV  // development: cycles of the state write-back (prof[5], accumulated in the global state)
+  const long long dvw = clock64();
+#endif
 #pragma unroll
   for (int q = 0; q < PER; ++q) {
     const int k = lane + 32 * q;
     if (k < NW) back[k] = dst[k];
   }
+#if JF_DEV
+  __syncwarp();
+  __threadfence();
+  if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&st->prof[5]), (unsigned long long)(clock64() - dvw));
+#endif
   if (lane == 0 && use_cond) cudaGraphSetConditional(cond, sst.cont ? 1u : 0u);
 }
 
