@@ -17,8 +17,10 @@
 // 41 fp64 operations against ~300 for the dual-number rank-1 form of the
 // n = 13 triangle (computed twice over, once per grid half).
 //
-// Scheduling, determinism and the per-task lane sums follow
-// moment_task_kernel (jf_moment.cuh).  The last block maps the summed moment
+// Scheduling: tasks of TC chunks of one row, taken by the block's warps from
+// a shared-memory counter; every task's lane sums land in the task's own slot
+// and the block partial adds the slots in task order (bitwise reproducible
+// whichever warp ran which task).  The last block maps the summed moment
 // vector to the alt-coordinate K-vector (kalt2_slot), applies the two
 // chain-rule blocks (apply_chain_kvec) and hands off.
 #pragma once

@@ -1,37 +1,44 @@
 // jf_moment_stream.cuh — the production J-pass for the rotated 2D Gaussian
 // (n = 7) on an implicit pixel grid, unweighted: the moment form of R34
-// (jf_moment.cuh) with a static, contiguous split of the image over warps.
+// (jf_moment.cuh) with a static, contiguous split of the image over warps and
+// the image staged into shared memory by TMA bulk copies.
 //
 // Same output as every other J-pass — the upper triangle of [J | r]^T [J | r]
 // (Eq. 2, Eq. 4, Eq. 5) plus the non-finite count —
 // from the 29 moments of jf_moment.cuh's MomLayout, mapped once per pass.
 //
 // Work split.  The image is a sequence of warp-chunks (32 L consecutive
-// pixels of one row; a row's last chunk may be partial).  Warp w of the grid
-// owns the contiguous chunk range [w nch / nw, (w+1) nch / nw): every warp
-// streams the same number of pixels (to one chunk) with no scheduling work,
-// so the warps of an SM finish together (measured: tools/jpass_probe.cu,
-// profiles/r2_jpass_probe.txt).  Lane l owns pixels l + 32 k of a chunk, so
-// every load of the warp reads 256 contiguous bytes; the next chunk is
-// prefetched into registers (two buffers, the loop unrolled by two chunks:
-// no register copies).
+// pixels of one row; a row's last chunk may be partial).  Warp g of the grid
+// owns the contiguous chunk range [f(g), f(g + 1)), f(g) = floor(g nch / nw)
+// in fp64 (a monotone partition, no 64-bit division at start-up): every warp
+// streams the same number of pixels to one chunk with no scheduling work.
+// Lane 0 of each warp streams its chunks into a STG-slot shared-memory ring
+// with 1D bulk copies (cp.async.bulk, mbarrier completion, L2 evict-first):
+// the first STG copies are issued at kernel entry, before the PDL wait on the
+// preceding kernel of a fit and before the prologue; a slot is refilled as
+// soon as the warp has consumed it.  Lane l reads pixels l + 32 k of a chunk
+// from shared memory.  (Inputs that are not 16-byte aligned or have odd W are
+// staged by the lanes.)
 //
 // Per point (the whole hot loop): u = E from the row recurrence
 // E_{k+1} = E_k R_k, R_{k+1} = R_k rho (2 DMUL), r = A u + off - z (2),
 // u^2, u r (2), the eleven step-index moments (11), sum r, sum r^2 (2):
 // 19 FP64 operations.  A chunk's moments are taken about the lane's pixel
 // k = (L-1)/2 of the chunk (compile-time powers of the step index), moved to
-// dx = 0 by a Taylor shift when the chunk ends and added to the row's; the
-// row's are folded with dy^q into the thread's column of a shared-memory
-// table at each row change (reading R34).  A row segment whose exponent range
-// is unsafe for the recurrence (q >= 600 or a step factor beyond e^300
-// anywhere on it) is evaluated with exp per point instead, and a pass whose
-// peak is narrower than MOMENT_MIN_WIDTH runs the dual-number body.
+// dx = 0 by a Taylor shift when the chunk ends and added to the row's (all
+// in registers); at a row change the row's moments are summed over the warp
+// and lane i adds entry i of the folded moment vector (x dy^q).  A row
+// segment whose exponent range is unsafe for the recurrence (q >= 600 or a
+// step factor beyond e^300 anywhere on it) is evaluated with exp per point,
+// and a pass whose peak is narrower than MOMENT_MIN_WIDTH or too elongated
+// runs the dual-number body.  The parameter-only prologue comes precomputed
+// (reading R36) or is computed here.
 //
 // Determinism: the chunk -> (warp, lane) map is a function of (m, W, grid),
-// every per-thread sum runs in chunk order, the block partial sums the
-// thread columns in thread order and the grid combine sums the block
-// partials in block order — a pass is bitwise reproducible.
+// every per-lane sum runs in chunk order, the warp sums use a fixed xor
+// butterfly, the block partial sums the warps in warp order and the grid
+// combine sums the block partials in block order — a pass is bitwise
+// reproducible.
 #pragma once
 
 #include "jf_moment.cuh"
