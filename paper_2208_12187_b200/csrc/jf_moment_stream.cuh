@@ -147,13 +147,13 @@ struct StreamAcc {
   int bad;
 };
 // A chunk by exp per point (row end, or an exponent range unsafe for the
-// recurrence): points c0 + lane + 32 k < W, z read from global memory,
-// moments about the chunk origin t = D (k - KC).
+// recurrence): points c0 + lane + 32 k < W, z from zp[32 k], moments about
+// dx = 0 directly (t = dx: no Taylor shift, so a chunk that holds only a few
+// pixels — a row narrower than the chunk — keeps full accuracy).
 template <int L>
 __device__ __noinline__ void stream_direct_chunk(StreamAcc& acc, const double* __restrict__ zp, int c0, int lane,
                                                  int W, double dx0, double dy, double ga, double gb2, double gc,
                                                  double A, double off) {
-  constexpr int KC = (L - 1) / 2;
   constexpr double D = 32.0;
   for (int k = 0; k < L; ++k) {
     if (c0 + lane + 32 * k < W) {
@@ -161,7 +161,7 @@ __device__ __noinline__ void stream_direct_chunk(StreamAcc& acc, const double* _
       const double u = exp(-(dx * (ga * dx + gb2 * dy) + gc * (dy * dy)));
       const double r = fma(A, u, off) - zp[32 * k];
       acc.bad += isfinite(r) ? 0 : 1;
-      const double u2 = u * u, t = D * (k - KC), t2 = t * t, ur = u * r;
+      const double u2 = u * u, t = dx, t2 = t * t, ur = u * r;
       acc.P[0] += u2;
       acc.P[1] = fma(u2, t, acc.P[1]);
       acc.P[2] = fma(u2, t2, acc.P[2]);
@@ -551,7 +551,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
       carried = false;
     }
     const double dx0 = (double)c0 + xl;
-    if (row_fast && c0 + CW <= W) {  // warp-uniform
+    const bool fast = row_fast && c0 + CW <= W;  // warp-uniform
+    if (fast) {
       if (!carried || ++since_seed >= SEEDN) {
         const double q0 = dx0 * (ga * dx0 + gb2 * dy) + gc * (dy * dy);
         const double argR = D * (2.0 * ga * dx0 + gb2 * dy) + ga * D * D;
@@ -618,7 +619,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
       srr = acc.srr;
       bad = acc.bad;
     }
-    chunk_fold(dx0 + D * KC);
+    chunk_fold(fast ? dx0 + D * KC : 0.0);  // (direct chunks are already about dx = 0)
     // the slot is free again: refill it with the chunk STG ahead
     __syncwarp();
     if (tma_ok && j + STG < nmy) {

@@ -291,3 +291,29 @@ def test_jpass_two_gaussians_edge_shapes(comp2):
     z = dg.render("gauss2d_rot_x2", (X, Y), truth) + 0.1 * np.random.default_rng(8).standard_normal(W * H)
     ref = orp.jpass("gauss2d_rot_x2", (X, Y), z, truth)
     check_pass(jf.jpass("gauss2d_rot_x2", z, truth, grid=(W, H, 0)), ref)
+
+
+@pytest.mark.parametrize("W", [1, 2, 31, 33, 511, 512, 513, 1000, 2049])
+@pytest.mark.parametrize("H", [1, 3, 17])
+def test_moment_pass_odd_shapes(W, H):
+    """The n = 7 moment J-pass (bulk-copy ring, chunk-granular warp split) on
+    shapes around its chunk (512 px) and lane (32 px) granularity: fewer
+    chunks than warps, one-row images, partial row-end chunks, widths below
+    one lane group.  A wide peak keeps the moment form (not the dual-number
+    fallback); pixel centres off the peak test the exp-per-point row ends."""
+    truth = np.array([1.3, 0.37 * W, 0.61 * H, 80.0, 55.0, 0.4, 0.25])
+    pr = dg.make_gauss2d_at(W, H, truth)
+    ref = orp.jpass(pr.model, pr.coords(), pr.z, pr.p0)
+    check_pass(jf.jpass(pr.model, pr.z, pr.p0, grid=pr.grid), ref)
+    zd = torch.as_tensor(pr.z).cuda()  # device input (16-byte aligned: bulk copies when W is even)
+    check_pass(jf.jpass(pr.model, zd, pr.p0, grid=pr.grid), ref)
+
+
+@pytest.mark.parametrize("W,H", [(1, 1), (2, 3), (33, 17), (257, 1), (1000, 3)])
+def test_moment2_pass_odd_shapes(W, H):
+    """The n = 13 moment J-pass on images narrower than a task / a chunk."""
+    truth = np.array([1.3, 0.37 * W, 0.61 * H, 80.0, 55.0, 0.4, 0.9, 0.55 * W, 0.3 * H, 60.0, 90.0, 1.1, 0.25])
+    X, Y = dg.grid_coords(W, H)
+    z = dg.render("gauss2d_rot_x2", (X, Y), truth) + 0.1 * np.random.default_rng(3).standard_normal(W * H)
+    ref = orp.jpass("gauss2d_rot_x2", (X, Y), z, truth)
+    check_pass(jf.jpass("gauss2d_rot_x2", z, truth, grid=(W, H, 0)), ref)
