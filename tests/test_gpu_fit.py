@@ -46,6 +46,15 @@ def check_fit(res, ref, trace=None, ref_trace=None, trace_rtol=1e-9):
             assert np.all(rel <= trace_rtol), (col, float(rel.max()))
 
 
+def _ragged():
+    """A well-conditioned fit on a 2049 x 150 image (row ends in partial
+    chunks): the peak fits the image, p0 perturbed from the truth."""
+    truth = [1.3, 900.0, 75.0, 400.0, 60.0, 0.3, 0.2]
+    pr = dg.make_gauss2d_at(2049, 150, truth)
+    pr.p0 = np.array(truth) * np.array([1.1, 1.02, 0.97, 1.15, 0.9, 1.0, 1.3]) + np.array([0, 0, 0, 0, 0, 0.1, 0])
+    return pr
+
+
 FITS = [
     ("C1", lambda: dg.make_exp_decay()),
     ("C2 m=1000", lambda: dg.make_gauss1d(1000)),
@@ -56,6 +65,8 @@ FITS = [
     ("C4b W=256", lambda: dg.make_gauss2d_bounded(256, "b")),
     ("C4c W=256", lambda: dg.make_gauss2d_bounded(256, "c")),
     ("C5 W=128", lambda: dg.make_gauss2d_x2(128)),
+    ("C3 301x97 (odd W: lane-staged chunks)", lambda: dg.make_gauss2d(301, H=97)),
+    ("C3 2049x150 (ragged row ends)", lambda: _ragged()),
 ]
 
 
@@ -300,7 +311,9 @@ def test_device_select_step_matches_oracle_all_branches():
 @pytest.mark.parametrize("name,make", [("C3 W=256", lambda: dg.make_gauss2d(256)),
                                        ("C2 m=100000", lambda: dg.make_gauss1d(100_000)),
                                        ("C1", lambda: dg.make_exp_decay()),
-                                       ("C5 W=128", lambda: dg.make_gauss2d_x2(128))])
+                                       ("C5 W=128", lambda: dg.make_gauss2d_x2(128)),
+                                       ("C3 301x97", lambda: dg.make_gauss2d(301, H=97)),
+                                       ("C3 2049x150", lambda: _ragged())])
 def test_warp_fast_path_equals_general_path(name, make):
     """The solver's warp fast path (warp_gn_step: the initial step and every
     accepted Gauss-Newton step of an unbounded Gram-mode fit) performs the
