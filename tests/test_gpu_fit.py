@@ -327,3 +327,14 @@ def test_warp_fast_path_equals_general_path(name, make):
     assert (a.status, a.nfev, a.njev, a.nit) == (b.status, b.nfev, b.njev, b.nit)
     assert np.array_equal(a.x, b.x) and a.cost == b.cost
     assert np.array_equal(a.grad, b.grad) and np.array_equal(a.pcov, b.pcov)
+
+
+@pytest.mark.slow
+def test_C2_fit_at_large_m_matches_oracle():
+    """BASELINE config 2 in the paper's large-data regime (m = 2,682,696, a
+    point of the length sweep): the complete fit against the
+    oracle's TRF (same counts, x to 1e-6)."""
+    pr = dg.make_gauss1d(2_682_696)
+    ref = otrf.fit(pr.model, pr.t, pr.z, pr.p0)
+    res = jf.curve_fit(pr.model, torch.as_tensor(pr.z).cuda(), y=torch.as_tensor(pr.t).cuda(), p0=pr.p0)
+    check_fit(res, ref)

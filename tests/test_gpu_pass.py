@@ -317,3 +317,15 @@ def test_moment2_pass_odd_shapes(W, H):
     z = dg.render("gauss2d_rot_x2", (X, Y), truth) + 0.1 * np.random.default_rng(3).standard_normal(W * H)
     ref = orp.jpass("gauss2d_rot_x2", (X, Y), z, truth)
     check_pass(jf.jpass("gauss2d_rot_x2", z, truth, grid=(W, H, 0)), ref)
+
+
+@pytest.mark.slow
+def test_full_size_C2_pass_matches_oracle():
+    """BASELINE config 2 at the top of its length sweep (1D Gaussian, m = 1e7,
+    explicit t): the dual-number J-pass and the r-pass at p0 against the oracle."""
+    pr = dg.make_gauss1d(10_000_000)
+    ref = orp.jpass(pr.model, pr.t, pr.z, pr.p0)
+    check_pass(jf.jpass(pr.model, pr.z, pr.p0, y=pr.t), ref)
+    cr, _ = orp.residual_pass(pr.model, pr.t, pr.z, pr.p0)
+    c, _ = jf.residual_pass(pr.model, pr.z, pr.p0, y=pr.t)
+    assert abs(c - cr) <= TOL * cr
