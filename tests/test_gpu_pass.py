@@ -329,3 +329,20 @@ def test_full_size_C2_pass_matches_oracle():
     cr, _ = orp.residual_pass(pr.model, pr.t, pr.z, pr.p0)
     c, _ = jf.residual_pass(pr.model, pr.z, pr.p0, y=pr.t)
     assert abs(c - cr) <= TOL * cr
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("W,H", [(2600, 7200), (8192, 8192)])
+def test_moment2_sub_runs_equal_dual_number_pass(W, H):
+    """Blocks with more tasks than the n = 13 moment kernel's slots run them
+    as sub-runs (W = 2600, H = 7200: two; the full C5 image: more) — sizes the
+    oracle cannot reduce in test time.  The property that holds at any size:
+    the moment form equals the dual-number rank-1 pass (the weighted kernel
+    with sigma = 1, pinned to the oracle in the weighted-pass tests) to the
+    parity tolerance, on the same device data."""
+    pr = dg.make_gauss2d_x2(W, seed=5, H=H)
+    zd = torch.as_tensor(pr.z).cuda()
+    ones = torch.ones(pr.m, dtype=torch.float64, device="cuda")
+    a = jf.jpass(pr.model, zd, pr.p0, grid=pr.grid)
+    b = jf.jpass(pr.model, zd, pr.p0, grid=pr.grid, sigma=ones)
+    check_pass(a, b)
