@@ -29,7 +29,10 @@ static void use_moment2(Kernels& k) {
   k.jk = moment2_task_kernel<L, TC, NW, ROLLED>;
   k.jtpb = NW * 32;
   k.jsmem = moment2_task_smem_bytes(NW);
-  k.jsplit = false;
+  // (the moment kernel itself runs on any grid, but its fallback to the
+  // dual-number body — narrow or elongated peaks — splits the n = 13 triangle
+  // across two halves of the grid: at least two blocks)
+  k.jsplit = true;
 }
 void kernel_attrs_init_x2() {
   cudaFuncSetAttribute((const void*)moment2_task_kernel<8, 8, 12, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
