@@ -116,3 +116,31 @@ def test_random_fit_matches_oracle(k):
     assert (res.status, res.nfev, res.njev, res.nit) == (ref["status"], ref["nfev"], ref["njev"], ref["nit"]), what
     x = ref["x"]
     assert np.all(np.abs(res.x - x) <= 1e-6 * np.maximum(np.abs(x), 1e-3 * np.max(np.abs(x)))), what
+
+
+@pytest.mark.parametrize("mode", ["tsqr", "conservative", "hostloop", "capacity", "weighted"])
+@pytest.mark.parametrize("k", range(8))
+def test_random_fit_modes_match_oracle(k, mode):
+    """The same seeded fits through the other fit paths: TSQR solver,
+    conservative policy (r-pass per trial), host-driven loop, a capacity-sized
+    graph (App. A masking without dummy data) and per-point weights."""
+    pr = _fit_case(100 + k)
+    kw = dict(grid=pr.grid) if pr.grid is not None else dict(y=pr.t)
+    sigma = None
+    if mode == "weighted":
+        sigma = np.random.default_rng([7, k]).uniform(0.05, 0.2, pr.m)
+        kw["sigma"] = sigma
+    elif mode == "tsqr":
+        kw["solver"] = "tsqr"
+    elif mode == "conservative":
+        kw["policy"] = "conservative"
+    elif mode == "hostloop":
+        kw["use_graph"] = False
+    elif mode == "capacity":
+        kw["capacity"] = pr.m + 12345
+    ref = otrf.fit(pr.model, pr.coords(), pr.z, pr.p0, pr.lb, pr.ub, sigma=sigma)
+    res = jf.curve_fit(pr.model, pr.z, p0=pr.p0, lb=pr.lb, ub=pr.ub, **kw)
+    what = f"case {k} {mode}: {pr.name}"
+    assert (res.status, res.nfev, res.njev, res.nit) == (ref["status"], ref["nfev"], ref["njev"], ref["nit"]), what
+    x = ref["x"]
+    assert np.all(np.abs(res.x - x) <= 1e-6 * np.maximum(np.abs(x), 1e-3 * np.max(np.abs(x)))), what
