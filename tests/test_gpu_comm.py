@@ -96,3 +96,45 @@ def test_sharded_fit_matches_single_rank(R):
         assert np.allclose(o.x, ref.x, rtol=1e-6)
     for o in outs[1:]:
         assert np.array_equal(o.x, outs[0].x) and o.cost == outs[0].cost
+
+
+@pytest.mark.parametrize("case", range(6))
+def test_sharded_random_fits_match_single_rank(case):
+    """Seeded sharded fits of every model family (1D models sharded by index
+    ranges with explicit t, images by row bands; 2-3 ranks): each rank returns
+    the single-rank fit's counts and x, all ranks bitwise equal."""
+    rng = np.random.default_rng([31, case])
+    R = 2 + case % 2
+    kind = case % 3
+    if kind == 0:
+        pr = dg.make_gauss1d(int(rng.integers(20_000, 90_000)), k=case)
+    elif kind == 1:
+        pr = dg.make_exp_decay(m=int(rng.integers(20_000, 60_000)), k=case)
+    else:
+        pr = dg.make_gauss2d_x2(int(rng.integers(96, 160)), k=case)
+    kw0 = dict(grid=pr.grid) if pr.grid is not None else dict(y=pr.t)
+    ref = jf.curve_fit(pr.model, pr.z, p0=pr.p0, **kw0)
+    comms = jf.Comm.create_local(R, 0)
+    if pr.grid is not None:
+        W, H = pr.grid[0], pr.grid[1]
+        bands = [dg.shard_rows(H, R, r) for r in range(R)]
+        zs = [torch.as_tensor(pr.z[r0 * W:r1 * W]).cuda() for r0, r1 in bands]
+        kws = [dict(grid=(W, r1 - r0, r0)) for r0, r1 in bands]
+    else:
+        rngs = [dg.shard_range(pr.m, R, r) for r in range(R)]
+        zs = [torch.as_tensor(pr.z[a:b]).cuda() for a, b in rngs]
+        kws = [dict(y=torch.as_tensor(pr.t[a:b]).cuda()) for a, b in rngs]
+    torch.cuda.synchronize()
+    try:
+        def fn(r, s):
+            return jf.curve_fit(pr.model, zs[r], p0=pr.p0, comm=comms[r], m_global=pr.m, stream=s.cuda_stream,
+                                **kws[r])
+        outs = _run_ranks(R, fn)
+    finally:
+        for c in comms:
+            c.destroy()
+    for o in outs:
+        assert (o.status, o.nfev, o.njev, o.nit) == (ref.status, ref.nfev, ref.njev, ref.nit), pr.name
+        assert np.allclose(o.x, ref.x, rtol=1e-6), pr.name
+    for o in outs[1:]:
+        assert np.array_equal(o.x, outs[0].x) and o.cost == outs[0].cost
