@@ -81,8 +81,9 @@ struct PassArgs {
   int32_t no_chain;     // debug (JF_DEBUG_NOCHAIN): return the Gram in the alt coordinates (a, 2b, c2)
   unsigned long long* dbg; // debug (JF_DEBUG_STAMPS): per-warp [smid, t_start, t_loop_end, t_exit] (moment kernel)
   // the parameter-only prologue of the n = 7 moment J-pass, precomputed for
-  // x by the caller (host x) — {A, x0, y0, a, 2b, c2, off, rho}; has_pre = 0: in-kernel
-  double pre[8];
+  // x by the caller (host x) — n = 7: {A, x0, y0, a, 2b, c2, off, rho}; n = 13:
+  // {A, x0, y0, a, 2b, c2} of each component, off, rho1, rho2; has_pre = 0: in-kernel
+  double pre[16];
   int32_t has_pre;
   int32_t fused;        // fit of the n = 7 moment J-pass: the solver step runs in the pass's last block
                         // (its dynamic shared memory as scratch) — no solver kernel between passes

@@ -679,10 +679,16 @@ static int pass_common(int32_t model, const double* y, const double* z, int64_t 
     if (o.x_host && model == JF_GAUSS2D_ROT) {  // (the caller's host copy of x_dev)
       gauss2d_prologue(o.x_host, a.pre);
       a.has_pre = 1;
+    } else if (o.x_host && model == JF_GAUSS2D_ROT_X2) {
+      gauss2d_x2_prologue(o.x_host, a.pre);
+      a.has_pre = 1;
     }
   } else {
     if (model == JF_GAUSS2D_ROT) {  // the moment J-pass's prologue, once, here
       gauss2d_prologue(x, a.pre);
+      a.has_pre = 1;
+    } else if (model == JF_GAUSS2D_ROT_X2) {
+      gauss2d_x2_prologue(x, a.pre);
       a.has_pre = 1;
     }
     double* hx = c->h_pin + 512;  // (the previous call's copy finished: calls are stream-ordered)
@@ -893,8 +899,11 @@ static int32_t fit_impl(int32_t model, const double* y, const double* z, int64_t
   h.kappa2_gn = 0.0;
   h.qr = c->d_qr;
   h.prec = c->d_qr->prec;
-  if (n == 7) {  // the first J-pass's prologue (the solver kernel writes the later ones)
+  if (n == 7) {  // the first J-pass's prologue (the solver step writes the later ones)
     gauss2d_prologue(h.x_eval, h.pre);
+    h.has_pre = 1;
+  } else if (n == 13) {
+    gauss2d_x2_prologue(h.x_eval, h.pre);
     h.has_pre = 1;
   }
   h.phase = PH_INIT_J;
@@ -1135,8 +1144,11 @@ int32_t jf_curve_fit_batch(int32_t model, const double* y, const double* z, int6
   }
   h.qr_mode = (o.solver == JF_SOLVE_TSQR) ? 1 : (o.solver == JF_SOLVE_AUTO ? 2 : 0);
   h.auto_mode = (o.solver == JF_SOLVE_AUTO) ? 1 : 0;
-  if (n == 7) {  // the first J-pass's prologue (the solver kernel writes the later ones)
+  if (n == 7) {  // the first J-pass's prologue (the solver step writes the later ones)
     gauss2d_prologue(h.x_eval, h.pre);
+    h.has_pre = 1;
+  } else if (n == 13) {
+    gauss2d_x2_prologue(h.x_eval, h.pre);
     h.has_pre = 1;
   }
   h.phase = PH_INIT_J;

@@ -132,13 +132,38 @@ __global__ void __launch_bounds__(NW * 32, 1)
   constexpr int CW = 32 * L;
   constexpr int MAXT = MOMENT2_MAXT;
   constexpr double D = 32.0;
-  const PassArgs& a = pa ? *pa : av;  // fits: device-resident args (graph replay); else by value
-  if (!pass_begin<true, false>(a, st)) {
-    qr2_dispatch<ModelGauss2DRotX2, COORD_GRID, false, NW * 32>(a, st, cond, use_cond);  // TSQR second pass
-    return;
-  }
-  const double* xs = (a.epilogue == EPI_FIT) ? st->x_eval : a.x;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  // the arguments (fits: device-resident, graph replay; else by value) into
+  // shared memory once: every later field access is a shared-memory load
+  __shared__ __align__(16) PassArgs sargs;
+  {
+    constexpr int NA = sizeof(PassArgs) / 8;
+    static_assert(sizeof(PassArgs) % 8 == 0 && NA <= NW * 32, "PassArgs copy");
+    if (tid < NA)
+      reinterpret_cast<unsigned long long*>(&sargs)[tid] =
+          pa ? __ldg(reinterpret_cast<const unsigned long long*>(pa) + tid)
+             : reinterpret_cast<const unsigned long long*>(&av)[tid];
+    __syncthreads();
+  }
+  const PassArgs& a = sargs;
+  // in a fit: the state's phase and the precomputed prologue (reading R36)
+  // in one batch of loads after the PDL wait
+  double pf[15];
+  int pf_has = 0;
+  if (a.epilogue == EPI_FIT) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int ph = __ldcg(&st->phase);
+    pf_has = __ldcg(&st->has_pre);
+#pragma unroll
+    for (int i = 0; i < 15; ++i) pf[i] = __ldcg(&st->pre[i]);
+    if (!(ph == PH_INIT_J || ph == PH_TRIAL_J || ph == PH_ACCEPT_J)) {
+      pass_begin<true, false>(a, st);  // (the launch count and timeline; returns false)
+      qr2_dispatch<ModelGauss2DRotX2, COORD_GRID, false, NW * 32>(a, st, cond, use_cond);  // TSQR second pass
+      return;
+    }
+  }
+  pass_begin<true, false>(a, st);
+  const double* xs = (a.epilogue == EPI_FIT) ? st->x_eval : a.x;
 
   extern __shared__ __align__(16) double dyn_task2[];
   double (*tslot)[KS] = reinterpret_cast<double (*)[KS]>(dyn_task2);                 // [MAXT][KS]
@@ -150,15 +175,21 @@ __global__ void __launch_bounds__(NW * 32, 1)
   __shared__ int next_task;
   __shared__ double binom[5][5];
 
-  double A1, A2, off, a1, b1, c1, a2, b2, c2, x01, y01, x02, y02;
+  double A1, A2, off, a1, b1, c1, a2, b2, c2, x01, y01, x02, y02, rho1, rho2;
   {
-    double xv[N];
+    double pr[15];
+    const double* p = pr;
+    if (a.epilogue == EPI_FIT ? pf_has : a.has_pre) {  // precomputed once per pass (R36)
+      p = (a.epilogue == EPI_FIT) ? pf : a.pre;
+    } else {
+      double xv[N];
 #pragma unroll
-    for (int j = 0; j < N; ++j) xv[j] = xs[j];
-    const auto pre = Model::template prologue<false>(xv);
-    A1 = pre.g1.A, a1 = pre.g1.a, b1 = pre.g1.b2, c1 = pre.g1.c, x01 = pre.g1.x0, y01 = pre.g1.y0;
-    A2 = pre.g2.A, a2 = pre.g2.a, b2 = pre.g2.b2, c2 = pre.g2.c, x02 = pre.g2.x0, y02 = pre.g2.y0;
-    off = pre.off;
+      for (int j = 0; j < N; ++j) xv[j] = xs[j];
+      gauss2d_x2_prologue(xv, pr);
+    }
+    A1 = p[0], x01 = p[1], y01 = p[2], a1 = p[3], b1 = p[4], c1 = p[5];
+    A2 = p[6], x02 = p[7], y02 = p[8], a2 = p[9], b2 = p[10], c2 = p[11];
+    off = p[12], rho1 = p[13], rho2 = p[14];
   }
   if (!moment_form_accurate(a1, b1, c1) || !moment_form_accurate(a2, b2, c2)) {  // (jf_moment_stream.cuh)
     pass_body_ool<Model, true, COORD_GRID, false, PassCfg<Model, true>::P, TPB, false>(a, st, cond, use_cond);
@@ -208,7 +239,6 @@ __global__ void __launch_bounds__(NW * 32, 1)
     if (lane == 0) t = atomicAdd(&next_task, 1);
     return __shfl_sync(FULL, t, 0);
   };
-  const double rho1 = exp(-2.0 * a1 * D * D), rho2 = exp(-2.0 * a2 * D * D);
   const double* __restrict__ z = a.z;
 
   double P11[5], P22[5], P12[5], Q1[3], Q2[3], R1[3], R2[3], sr, srr;

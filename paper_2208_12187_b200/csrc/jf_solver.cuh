@@ -1696,6 +1696,9 @@ __device__ __forceinline__ void solver_run(FitState* __restrict__ st, SolverSmem
   if (sst.n == 7) {  // the next n = 7 moment J-pass's prologue at x_eval
     gauss2d_prologue_warp(sst.x_eval, sst.pre);
     if (lane == 0) sst.has_pre = 1;
+  } else if (sst.n == 13) {  // (the two-Gaussian moment J-pass's)
+    gauss2d_x2_prologue_warp(sst.x_eval, sst.pre);
+    if (lane == 0) sst.has_pre = 1;
   }
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
   if (lane == 0) {
@@ -1771,6 +1774,9 @@ __device__ __noinline__ void fused_solver_step(FitState* __restrict__ st, const 
 #endif
   if (sst.n == 7) {  // the next pass's prologue at x_eval
     gauss2d_prologue_warp(sst.x_eval, sst.pre);
+    if (lane == 0) sst.has_pre = 1;
+  } else if (sst.n == 13) {  // (the two-Gaussian moment J-pass's)
+    gauss2d_x2_prologue_warp(sst.x_eval, sst.pre);
     if (lane == 0) sst.has_pre = 1;
   }
 #if JF_DEV  // development: cycles of the state load (prof[0]) and of the prologue (prof[2])

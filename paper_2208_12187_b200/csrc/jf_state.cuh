@@ -64,8 +64,8 @@ struct FitState {
   int32_t auto_mode;           // solver AUTO: Gram until the conditioning calls for TSQR (checked at x0 and at accepted steps)
   QRState* qr;                 // device TSQR working set
   double* prec;                // = qr->prec (read by the preconditioned pass kernel)
-  int32_t has_pre, pad_pre;    // pre: the n = 7 moment J-pass prologue at x_eval (gauss2d_prologue)
-  double pre[8];
+  int32_t has_pre, pad_pre;    // pre: the moment J-pass prologue at x_eval (gauss2d_prologue, _x2)
+  double pre[16];
   // ---- bulk: every entry is written on the device before it is read (the
   // host uploads only the fields above, FITSTATE_UPLOAD bytes, per fit)
   unsigned long long tl[64];  // device timeline (globaltimer ns): pass start/end, solver start/end
@@ -98,6 +98,28 @@ __host__ __device__ inline void gauss2d_prologue(const double* x, double* pre) {
   pre[6] = x[6];
   pre[7] = exp(-2.0 * a * 32.0 * 32.0);
 }
+// The two-Gaussian model (n = 13): pre = {A1, x01, y01, a1, 2b1, c21, A2,
+// x02, y02, a2, 2b2, c22, off, rho1, rho2} (the expressions of
+// ModelGauss2DRotX2::prologue, rho_c = exp(-2 a_c 32^2)).
+__host__ __device__ inline void gauss2d_x2_prologue(const double* x, double* pre) {
+  for (int c = 0; c < 2; ++c) {
+    const double* xc = x + 6 * c;
+    const double sx = xc[3], sy = xc[4], th = xc[5];
+    const double C = cos(th), S = sin(th);
+    const double ix = 0.5 / (sx * sx), iy = 0.5 / (sy * sy);
+    const double CC = C * C, SS = S * S;
+    const double a = CC * ix + SS * iy;
+    double* pc = pre + 6 * c;
+    pc[0] = xc[0];
+    pc[1] = xc[1];
+    pc[2] = xc[2];
+    pc[3] = a;
+    pc[4] = 2.0 * ((S * C) * (iy - ix));
+    pc[5] = SS * ix + CC * iy;
+    pre[13 + c] = exp(-2.0 * a * 32.0 * 32.0);
+  }
+  pre[12] = x[12];
+}
 #ifdef __CUDACC__
 // The same on a whole warp (lane values equal on entry), without divergent
 // lanes: sin and cos from one sincos, the two reciprocals on two lanes of the
@@ -123,6 +145,38 @@ __device__ __forceinline__ void gauss2d_prologue_warp(const double* x, double* p
     pre[5] = SS * ix + CC * iy;
     pre[6] = x[6];
     pre[7] = rho;
+  }
+}
+// n = 13 on a whole warp: lanes 0-1 the two components' sincos... each lane
+// of a pair (lane & 1) one component, the rest on every lane; lane 0 writes.
+__device__ __forceinline__ void gauss2d_x2_prologue_warp(const double* x, double* pre) {
+  const int lane = threadIdx.x & 31;
+  const double* xc = x + 6 * (lane & 1);
+  double S, C;
+  sincos(xc[5], &S, &C);
+  const double ix = 0.5 / (xc[3] * xc[3]), iy = 0.5 / (xc[4] * xc[4]);
+  const double CC = C * C, SS = S * S;
+  const double a = CC * ix + SS * iy;
+  const double b2 = 2.0 * ((S * C) * (iy - ix));
+  const double c2 = SS * ix + CC * iy;
+  const double rho = exp(-2.0 * a * 32.0 * 32.0);
+  const double a_1 = __shfl_sync(0xffffffffu, a, 1), b_1 = __shfl_sync(0xffffffffu, b2, 1);
+  const double c_1 = __shfl_sync(0xffffffffu, c2, 1), r_1 = __shfl_sync(0xffffffffu, rho, 1);
+  if (lane == 0) {
+    for (int c = 0; c < 2; ++c) {
+      pre[6 * c + 0] = x[6 * c + 0];
+      pre[6 * c + 1] = x[6 * c + 1];
+      pre[6 * c + 2] = x[6 * c + 2];
+    }
+    pre[3] = a;
+    pre[4] = b2;
+    pre[5] = c2;
+    pre[9] = a_1;
+    pre[10] = b_1;
+    pre[11] = c_1;
+    pre[12] = x[12];
+    pre[13] = rho;
+    pre[14] = r_1;
   }
 }
 #endif
