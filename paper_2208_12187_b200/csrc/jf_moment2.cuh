@@ -164,6 +164,15 @@ __global__ void __launch_bounds__(NW * 32, 1)
   }
   pass_begin<true, false>(a, st);
   const double* xs = (a.epilogue == EPI_FIT) ? st->x_eval : a.x;
+  // development builds only (JF_DEV): per-warp globaltimer stamps
+  auto stamp = [&](int slot) {
+    if (JF_DEV && a.dbg && lane == 0 && blockIdx.x * NW + wid < 8000) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.dbg[(blockIdx.x * NW + wid) * 8 + slot] = t;
+    }
+  };
+  stamp(1);
 
   extern __shared__ __align__(16) double dyn_task2[];
   double (*tslot)[KS] = reinterpret_cast<double (*)[KS]>(dyn_task2);                 // [MAXT][KS]
@@ -293,6 +302,16 @@ __global__ void __launch_bounds__(NW * 32, 1)
     }
   };
 
+  // the components' chain-rule blocks for the last block's tail (dual-number
+  // prologue), by one thread of every block at its start: its warp takes
+  // fewer tasks (the block's warps grab tasks dynamically)
+  __shared__ Pre spre2;
+  if (tid == 4 * 32) {
+    double xv[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) xv[j] = xs[j];
+    spre2 = Model::template prologue<true>(xv);
+  }
   constexpr int NSEG = TPB / KS > 0 ? (TPB / KS < NW ? TPB / KS : NW) : 1;
   double bsum = 0.0;  // this thread's (entry, segment) share of the block partial, over the rounds
   for (int rd = 0; rd < nround; ++rd) {
@@ -302,6 +321,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
     if (tid == 0) next_task = 0;
     __syncthreads();
   }
+  stamp(2);
   int task = grab();
   int64_t trow = 0;
   int tcc0 = 0, tncc = 0;
@@ -503,6 +523,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
   }
   __syncthreads();  // the slots are reused by the next round
   }  // rounds
+  stamp(3);
 
   // ---- block partial: the task slots summed in task order (round by round)
   {
@@ -520,25 +541,45 @@ __global__ void __launch_bounds__(NW * 32, 1)
     }
   }
   if (!grid_reduce1<KS, TPB>(a, mom, scratch)) return;
-  // ---- last block: moments -> alt-coordinate K-vector -> chain rule -> hand-off
-  Pre pre;
-  {
-    double xv[N];
-#pragma unroll
-    for (int j = 0; j < N; ++j) xv[j] = xs[j];
-    pre = Model::template prologue<true>(xv);
-  }
-  for (int t = tid; t < KT; t += TPB) {
-    int j = 0, rem = t;
-    while (rem >= N + 1 - j) {
-      rem -= N + 1 - j;
-      ++j;
+  // ---- last block: moments -> alt-coordinate K-vector -> chain rule -> hand-off.
+  // The 105 slots by warps 0-3 in an order that groups slots of one kind
+  // (cross-component, own-frame, offset / residual column) so a warp's threads
+  // take the same branches; the components' chain-rule blocks (dual-number
+  // prologue) were computed at the block's start (spre2).
+  dbg_tail(a, 5);
+  if (tid < KT) {
+    PreGauss2D g1, g2;
+    g1.A = A1, g1.x0 = x01, g1.y0 = y01, g1.a = a1, g1.b2 = b1, g1.c = c1;
+    g2.A = A2, g2.x0 = x02, g2.y0 = y02, g2.a = a2, g2.b2 = b2, g2.c = c2;
+    int j, k, o = tid;
+    if (o < 36) {  // cross-component (F12)
+      j = o / 6;
+      k = 6 + o % 6;
+    } else if (o < 78) {  // own frame (F11 / F22): j <= k within one component
+      const int c = (o < 57) ? 0 : 1;
+      int r = o - (c == 0 ? 36 : 57);
+      j = 0;
+      while (r >= 6 - j) {
+        r -= 6 - j;
+        ++j;
+      }
+      k = j + r;
+      j += 6 * c;
+      k += 6 * c;
+    } else if (o < 102) {  // offset / residual columns
+      j = (o - 78) / 2;
+      k = 12 + (o - 78) % 2;
+    } else {
+      j = (o == 104) ? 13 : 12;
+      k = (o == 102) ? 12 : 13;
     }
-    vec[t] = kalt2_slot(pre.g1, pre.g2, (double)a.m, mom, j, j + rem);
+    vec[tri_slot(N, j, k)] = kalt2_slot(g1, g2, (double)a.m, mom, j, k);
   }
   if (tid == 0) vec[KT] = mom[Mom2::NV];
   __syncthreads();
-  if (!a.no_chain) apply_chain_kvec<Model, TPB>(pre, vec, scratch);
+  dbg_tail(a, 6);
+  if (!a.no_chain) apply_chain_kvec<Model, TPB>(spre2, vec, scratch);
+  dbg_tail(a, 7);
   pass_tail<KS2, TPB, true>(a, st, vec, cond, use_cond);
 }
 
