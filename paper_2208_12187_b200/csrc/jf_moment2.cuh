@@ -115,9 +115,69 @@ __device__ __forceinline__ double kalt2_slot(const PreGauss2D& g1, const PreGaus
   return v * f;
 }
 
+// The same slot as a short list of (coefficient, moment index) terms —
+// kalt2_slot's products expanded (the map is linear in the moments; the
+// point count is index M2_COUNT) — so the last block applies a precomputed
+// map instead of evaluating kalt2_slot.  At most M2_TERMS terms per slot:
+// psi has <= 2 monomials, a shifted monomial of degree <= 2 <= 4 terms, and a
+// column's monomials shift to <= 4 terms in all.
+constexpr int M2_TERMS = 8, M2_COUNT = 255;
+__device__ __forceinline__ int kalt2_terms(const PreGauss2D& g1, const PreGauss2D& g2, int j, int k, double* coef,
+                                           unsigned char* idx) {
+  constexpr int OFF = 12, RES = 13;
+  int n = 0;
+  auto add = [&](double c, int i) {
+    coef[n] = c;
+    idx[n] = (unsigned char)i;
+    ++n;
+  };
+  if (j == OFF) {
+    add(1.0, k == OFF ? M2_COUNT : Mom2::OSR);
+    return n;
+  }
+  if (j == RES) {
+    add(1.0, Mom2::OSRR);
+    return n;
+  }
+  const int cj = j / 6, jj = j % 6;
+  const PreGauss2D& gj = cj == 0 ? g1 : g2;
+  const Poly2 a = psi(gj, jj);
+  const double fa = (jj == 0 ? 1.0 : gj.A);
+  if (k == OFF || k == RES) {
+    const int base = (k == OFF) ? (cj == 0 ? Mom2::G1 : Mom2::G2) : (cj == 0 ? Mom2::H1 : Mom2::H2);
+    for (int s = 0; s < 2; ++s)
+      if (a.c[s] != 0.0) add(fa * a.c[s], base + mono(2, a.p[s], a.q[s]));
+    return n;
+  }
+  const int ck = k / 6, kk = k % 6;
+  const PreGauss2D& gk = ck == 0 ? g1 : g2;
+  const Poly2 b = psi(gk, kk);
+  const double f = fa * (kk == 0 ? 1.0 : gk.A);
+  if (cj == ck) {  // F11 / F22 in the component's own frame
+    const int base = cj == 0 ? Mom2::F11 : Mom2::F22;
+    for (int s = 0; s < 2; ++s)
+      for (int u = 0; u < 2; ++u)
+        if (a.c[s] != 0.0 && b.c[u] != 0.0)
+          add(f * (a.c[s] * b.c[u]), base + mono(4, a.p[s] + b.p[u], a.q[s] + b.q[u]));
+  } else {  // F12 in component 1's frame: component 2's monomials shifted
+    const double sx = g1.x0 - g2.x0, sy = g1.y0 - g2.y0;
+    for (int s = 0; s < 2; ++s) {
+      if (a.c[s] == 0.0) continue;
+      for (int u = 0; u < 2; ++u) {
+        if (b.c[u] == 0.0) continue;
+        const ShiftTerms t = shift_mono(b.p[u], b.q[u], sx, sy);
+        for (int e = 0; e < t.n; ++e)
+          add(f * (a.c[s] * b.c[u]) * t.c[e], Mom2::F12 + mono(4, a.p[s] + t.p[e], a.q[s] + t.q[e]));
+      }
+    }
+  }
+  return n;
+}
+
 constexpr int MOMENT2_MAXT = 96;  // task slots per block
 __host__ __device__ constexpr int moment2_task_smem_bytes(int NW) {
-  return (MOMENT2_MAXT * Mom2::KS + NW * Mom2::NRUN * 33) * 8;
+  // task slots, per-warp lane-sum rows, the moments -> K-vector term lists
+  return (MOMENT2_MAXT * Mom2::KS + NW * Mom2::NRUN * 33) * 8 + 105 * M2_TERMS * 8 + 105 * M2_TERMS + 105 * 4 + 16;
 }
 
 template <int L, int TC, int NW, bool ROLLED = false>
@@ -311,6 +371,26 @@ __global__ void __launch_bounds__(NW * 32, 1)
 #pragma unroll
     for (int j = 0; j < N; ++j) xv[j] = xs[j];
     spre2 = Model::template prologue<true>(xv);
+  }
+  // ... and the moments -> alt-coordinate K-vector map as term lists, by
+  // the block's last four warps (likewise absorbed by the dynamic task grab)
+  static_assert(KT == 105, "term-list layout");
+  double (*m2coef)[M2_TERMS] = reinterpret_cast<double (*)[M2_TERMS]>(dyn_task2 + MAXT * KS + NW * NR * 33);
+  unsigned char (*m2idx)[M2_TERMS] = reinterpret_cast<unsigned char (*)[M2_TERMS]>(m2coef + KT);
+  int* m2n = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(m2idx + KT) + 8 - (KT * M2_TERMS) % 8);
+  static_assert(NW >= 4, "four builder warps");
+  if (wid >= NW - 4) {
+    PreGauss2D g1, g2;
+    g1.A = A1, g1.x0 = x01, g1.y0 = y01, g1.a = a1, g1.b2 = b1, g1.c = c1;
+    g2.A = A2, g2.x0 = x02, g2.y0 = y02, g2.a = a2, g2.b2 = b2, g2.c = c2;
+    for (int t = lane + 32 * (wid - (NW - 4)); t < KT; t += 128) {
+      int j = 0, rem = t;
+      while (rem >= N + 1 - j) {
+        rem -= N + 1 - j;
+        ++j;
+      }
+      m2n[t] = kalt2_terms(g1, g2, j, j + rem, m2coef[t], m2idx[t]);
+    }
   }
   constexpr int NSEG = TPB / KS > 0 ? (TPB / KS < NW ? TPB / KS : NW) : 1;
   double bsum = 0.0;  // this thread's (entry, segment) share of the block partial, over the rounds
@@ -541,39 +621,17 @@ __global__ void __launch_bounds__(NW * 32, 1)
     }
   }
   if (!grid_reduce1<KS, TPB>(a, mom, scratch)) return;
-  // ---- last block: moments -> alt-coordinate K-vector -> chain rule -> hand-off.
-  // The 105 slots by warps 0-3 in an order that groups slots of one kind
-  // (cross-component, own-frame, offset / residual column) so a warp's threads
-  // take the same branches; the components' chain-rule blocks (dual-number
-  // prologue) were computed at the block's start (spre2).
+  // ---- last block: moments -> alt-coordinate K-vector (the term lists built
+  // at the block's start) -> chain rule (the blocks of spre2) -> hand-off
   dbg_tail(a, 5);
   if (tid < KT) {
-    PreGauss2D g1, g2;
-    g1.A = A1, g1.x0 = x01, g1.y0 = y01, g1.a = a1, g1.b2 = b1, g1.c = c1;
-    g2.A = A2, g2.x0 = x02, g2.y0 = y02, g2.a = a2, g2.b2 = b2, g2.c = c2;
-    int j, k, o = tid;
-    if (o < 36) {  // cross-component (F12)
-      j = o / 6;
-      k = 6 + o % 6;
-    } else if (o < 78) {  // own frame (F11 / F22): j <= k within one component
-      const int c = (o < 57) ? 0 : 1;
-      int r = o - (c == 0 ? 36 : 57);
-      j = 0;
-      while (r >= 6 - j) {
-        r -= 6 - j;
-        ++j;
-      }
-      k = j + r;
-      j += 6 * c;
-      k += 6 * c;
-    } else if (o < 102) {  // offset / residual columns
-      j = (o - 78) / 2;
-      k = 12 + (o - 78) % 2;
-    } else {
-      j = (o == 104) ? 13 : 12;
-      k = (o == 102) ? 12 : 13;
+    const double m_pts = (double)a.m;
+    double v = 0.0;
+    for (int e = 0; e < m2n[tid]; ++e) {
+      const int i = m2idx[tid][e];
+      v = fma(m2coef[tid][e], i == M2_COUNT ? m_pts : mom[i], v);
     }
-    vec[tri_slot(N, j, k)] = kalt2_slot(g1, g2, (double)a.m, mom, j, k);
+    vec[tid] = v;
   }
   if (tid == 0) vec[KT] = mom[Mom2::NV];
   __syncthreads();
