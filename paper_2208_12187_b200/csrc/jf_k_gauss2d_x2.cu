@@ -33,6 +33,8 @@ static void use_moment2(Kernels& k) {
   // dual-number body — narrow or elongated peaks — splits the n = 13 triangle
   // across two halves of the grid: at least two blocks)
   k.jsplit = true;
+  static_assert(moment2_task_smem_bytes(12) >= (int)fused_solver_smem_bytes(), "solver scratch");
+  k.jfused = true;  // speculative one-GPU fits: the solver step in the pass's last block
 }
 void kernel_attrs_init_x2() {
   cudaFuncSetAttribute((const void*)moment2_task_kernel<8, 8, 12, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,

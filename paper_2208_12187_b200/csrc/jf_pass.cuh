@@ -745,10 +745,10 @@ __device__ __forceinline__ void pass_tail(const PassArgs& a, FitState* __restric
 
   // ---- fit: hand the combined K-vector to the solver kernel (jf_solver.cu)
   for (int k = threadIdx.x; k < KS; k += TPB) a.out[k] = vec[k];
-  if constexpr (JAC && KS == tri_count(7) + 1) {
+  if constexpr (JAC && (KS == tri_count(7) + 1 || KS == tri_count(13) + 1)) {
     if (a.fused) {  // the solver step here, by warp 0 (the kernel's dynamic shared memory as scratch)
       __syncthreads();
-      if (threadIdx.x < 32) fused_solver_step<7>(st, vec, cond, use_cond);
+      if (threadIdx.x < 32) fused_solver_step<(KS == tri_count(7) + 1) ? 7 : 13>(st, vec, cond, use_cond);
       return;
     }
   }
