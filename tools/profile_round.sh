@@ -19,10 +19,6 @@ fi
 EXTRA=sm__sass_thread_inst_executed_op_dfma_pred_on.sum,sm__sass_thread_inst_executed_op_dadd_pred_on.sum,sm__sass_thread_inst_executed_op_dmul_pred_on.sum,sm__inst_executed_pipe_fp64.sum,sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active,sm__inst_executed_pipe_xu.sum,sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active,sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active,sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active
 timeout 600 ncu --set full --metrics $EXTRA --clock-control none --import-source on -k regex:moment_stream -s 3 -c 1 \
     -o gpurun_out/jpass_${TAG} -f python tools/quick_time.py 4096 passonly > /dev/null 2>&1
-if [ "$WHAT" = all ]; then
-# (T fits run the solver step inside the J-pass's last block; the solver kernel
-# still serves the n = 13 C5 fit)
-timeout 900 ncu --set full --metrics $EXTRA --clock-control none --import-source on -k regex:solver_kernel -s 4 -c 1 \
-    -o gpurun_out/solver_${TAG} -f python bench.py --steps 1 --warmup 3 --no-batch --no-cpu-baseline > /dev/null 2>&1
-fi
+# (fits of the moment J-passes run the solver step in the pass's last block,
+# R37: the bench launches no solver kernel to capture)
 ls -la gpurun_out
