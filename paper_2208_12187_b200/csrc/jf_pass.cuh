@@ -837,7 +837,20 @@ template <class Model, bool JAC, int COORD, bool WGT, int P = PassCfg<Model, JAC
 __global__ void __launch_bounds__(TPB, MINB)
     pass_kernel(const PassArgs* __restrict__ pa, FitState* __restrict__ st, cudaGraphConditionalHandle cond,
                 int use_cond, const PassArgs av) {
-  const PassArgs& a = pa ? *pa : av;  // fits: device-resident args (graph replay); else by value
+  // the arguments (fits: device-resident, graph replay; else by value) into
+  // shared memory once: a reference that may name either the kernel's
+  // parameters or global memory makes every field access a generic load
+  __shared__ __align__(16) PassArgs sargs;
+  {
+    constexpr int NA = sizeof(PassArgs) / 8;
+    static_assert(sizeof(PassArgs) % 8 == 0 && NA <= TPB, "PassArgs copy");
+    if ((int)threadIdx.x < NA)
+      reinterpret_cast<unsigned long long*>(&sargs)[threadIdx.x] =
+          pa ? __ldg(reinterpret_cast<const unsigned long long*>(pa) + threadIdx.x)
+             : reinterpret_cast<const unsigned long long*>(&av)[threadIdx.x];
+    __syncthreads();
+  }
+  const PassArgs& a = sargs;
   if (!pass_begin<JAC, PREC>(a, st)) {
     if constexpr (JAC && !PREC) qr2_dispatch<Model, COORD, WGT, TPB>(a, st, cond, use_cond);
     return;
