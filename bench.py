@@ -48,9 +48,9 @@ N_PARAMS = 7
 # implicit grid) and, in the moment form (jf_moment.cuh), execute 19 fp64
 # operations (row recurrence 2, residual 2, u^2 1, u r 1, the eleven
 # step-index moments 11, sum r and sum r^2 2; per-chunk/per-task overheads
-# are the implementation's, not the algorithm's).  HBM: 8 B / 6467 GB/s per
-# point; FP64: 19 / (148 SMs x 64 lanes x 1.965 GHz) per point -> at 4096^2
-# 20.8 us vs 17.1 us: the pass is HBM-bound and is reported against the
+# are the implementation's, not the algorithm's).  HBM: 8 B per
+# point at the measured HBM peak; FP64: 19 / (148 SMs x 64 lanes x 1.965 GHz)
+# per point -> at 4096^2 20.5 us vs 17.1 us: the pass is HBM-bound and is reported against the
 # measured HBM peak (MEASURED_PEAKS.json hbm_gbs), with the FP64-pipe
 # fraction alongside.  (The dual-number rank-1 form needs 85 fp64 per point,
 # SURVEY §8(d) d.3, and would be FP64-bound.)
@@ -173,10 +173,18 @@ def run_reference(args):
     if rank != 0:
         return
     from oracle import trf as otrf
-    pr = dg.make_gauss2d(W_IMG, seed=SEED)
-    rows = 256
-    z = pr.z[: rows * W_IMG]
-    X, Y = dg.grid_coords(W_IMG, rows, 0)
+    if world == 1:  # T: a 256-row band of the 4096^2 image
+        pr = dg.make_gauss2d(W_IMG, seed=SEED)
+        W, rows = W_IMG, 256
+        metric = "data points/s per J-pass (complete TRF fits, 2D Gaussian n=7)"
+        desc, scaling = f"gauss2d_rot n=7, rows 0..{rows} of the {W}x{W} seed-{SEED} image (bounded sample of T)", "weak"
+    else:  # N > 1: our arm's C5 metric; a 64-row band of the 8192^2 two-Gaussian image (n = 13)
+        W, rows = 8192, 64
+        pr = dg.make_gauss2d_x2(W, seed=5, H=rows)
+        metric = "data points/s per J-pass (complete TRF fits, two 2D Gaussians n=13, C5 row bands)"
+        desc, scaling = f"gauss2d_rot_x2 n=13, rows 0..{rows} of the {W}x{W} seed-5 image (bounded sample of C5)", "strong"
+    z = pr.z[: rows * W]
+    X, Y = dg.grid_coords(W, rows, 0)
     times, pts = [], []
     for s in range(args.warmup + args.steps):
         t0 = time.perf_counter()
@@ -188,14 +196,13 @@ def run_reference(args):
     tot = sum(times)
     value = sum(pts) / tot
     line = {
-        "impl": "reference", "metric": "data points/s per J-pass (complete TRF fits, 2D Gaussian n=7)",
-        "value": value, "unit": "points/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "weak",
+        "impl": "reference", "metric": metric,
+        "value": value, "unit": "points/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"gauss2d_rot n=7, rows 0..{rows} of the {W_IMG}x{W_IMG} seed-{SEED} image "
-                               f"(bounded sample of T)", "m": int(z.size)},
+        "config": {"workload": desc, "m": int(z.size), "parallelism": "oracle on rank 0's host cores"},
         "cpu_baseline": {"value": value, "unit": "points/s", "cores": 1, "kind": "oracle",
-                         "sample": f"oracle/trf.py fit of a {rows}x{W_IMG} band per step"},
+                         "sample": f"oracle/trf.py fit of a {rows}x{W} band per step"},
         "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
