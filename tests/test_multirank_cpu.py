@@ -68,3 +68,30 @@ def test_shard_helpers_cover_exactly():
             bands = [dg.shard_rows(H, R, k) for k in range(R)]
             assert bands[0][0] == 0 and bands[-1][1] == H
             assert all(bands[k][1] == bands[k + 1][0] for k in range(R - 1))
+
+
+def _run_ref(env_extra):
+    import subprocess
+    import sys
+    import json
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, **env_extra)
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--steps", "1",
+                        "--warmup", "0"], capture_output=True, text=True, env=env, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    return [json.loads(ln) for ln in lines]
+
+
+def test_reference_arm_rank_nonzero_is_silent():
+    """bench.py --impl reference under torchrun: ranks other than 0 exit 0 without work or output."""
+    assert _run_ref({"WORLD_SIZE": "2", "RANK": "1", "LOCAL_RANK": "1"}) == []
+
+
+def test_reference_arm_line_at_n2_carries_the_c5_metric():
+    """At N > 1 the reference arm reports our arm's metric (C5 row bands, n = 13) with the contract keys."""
+    (d,) = _run_ref({"WORLD_SIZE": "2", "RANK": "0", "LOCAL_RANK": "0"})
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["scaling"] == "strong"
+    assert "n=13, C5 row bands" in d["metric"] and d["unit"] == "points/s" and d["higher_is_better"] is True
+    assert d["value"] > 0 and d["e2e"]["value"] == d["value"] and d["e2e"]["h2d_bytes_per_step"] == 0
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
