@@ -1249,15 +1249,21 @@ __device__ __forceinline__ bool warp_chol_cert(const double (*A)[MS], double (*L
   tr = 0.0;
 #pragma unroll
   for (int i = 0; i < n; ++i) tr += A[i][i];
+  // (loops fully unrolled, the lane's own row of L in registers: the loads
+  // are issued together instead of one shared-memory round trip per fma)
+  double lrow[n];
+#pragma unroll
   for (int k = 0; k < n; ++k) {
     double t = 0.0;
     if (lane >= k && lane < n) {
       t = A[lane][k];
-      for (int j = 0; j < k; ++j) t = fma(-Lm[lane][j], Lm[k][j], t);
+#pragma unroll
+      for (int j = 0; j < k; ++j) t = fma(-lrow[j], Lm[k][j], t);
     }
     const double d = __shfl_sync(FULL, t, k);
     if (!(d > 0.0)) return false;
     const double r = rsqrt(d);
+    lrow[k] = (lane == k) ? d * r : t * r;
     if (lane == k) {
       Lm[k][k] = d * r;
       cinv[k] = r;
@@ -1266,12 +1272,17 @@ __device__ __forceinline__ bool warp_chol_cert(const double (*A)[MS], double (*L
     }
     __syncwarp();
   }
-  if (lane < n) {
+  if (lane < n) {  // lane c: column c of L^-1, rows i >= c (k increasing from c, as before)
     const int c = lane;
-    for (int i = c; i < n; ++i) {
+    double y[n];
+#pragma unroll
+    for (int i = 0; i < n; ++i) {
       double t = (i == c) ? 1.0 : 0.0;
-      for (int k = c; k < i; ++k) t = fma(-Lm[i][k], Ym[k][c], t);
-      Ym[i][c] = t * cinv[i];
+#pragma unroll
+      for (int k = 0; k < i; ++k)
+        if (k >= c) t = fma(-Lm[i][k], y[k], t);
+      y[i] = t * cinv[i];
+      if (i >= c) Ym[i][c] = y[i];
     }
   }
   __syncwarp();
@@ -1455,6 +1466,7 @@ __device__ __noinline__ bool warp_gn_step(FitState* st, SolverSmem& S, const dou
   if (lane < n) S.w2[lane] = dd;
   __syncwarp();
   if (lane < n) {
+#pragma unroll
     for (int j = 0; j < n; ++j) {
       const int a = lane < j ? lane : j, b = lane < j ? j : lane;
       double bij = dd * kv[tri_slot(n, a, b)] * S.w2[j];
@@ -1474,6 +1486,7 @@ __device__ __noinline__ bool warp_gn_step(FitState* st, SolverSmem& S, const dou
   dq2 = clock64();
 #endif
   double t = (lane < n) ? -S.w3[lane] : 0.0;
+#pragma unroll
   for (int k = 0; k < n; ++k) {  // lane i accumulates row i as w_k become known (k increasing)
     const double wk = __shfl_sync(FULL, t * cinv[k], k);
     if (lane > k && lane < n) t = fma(-S.T[lane][k], wk, t);
