@@ -54,6 +54,7 @@ struct SolverSmem {
 template <int n>
 __device__ __forceinline__ double vdot(const double* a, const double* b) {
   double s = 0.0;
+#pragma unroll
   for (int j = 0; j < n; ++j) s = fma(a[j], b[j], s);
   return s;
 }
@@ -1524,8 +1525,6 @@ __device__ __noinline__ bool warp_gn_step(FitState* st, SolverSmem& S, const dou
     double gp = 0.0;
 #pragma unroll
     for (int j = 0; j < n; ++j) gp = fma(pr[j], S.w3[j], gp);
-    const int KS = tri_count(n) + 1;
-    for (int k = 0; k < KS; ++k) st->kv[k] = kv[k];
     st->launches = st->launches + 1;
     st->nfev = nfev;
     if (init) {
@@ -1567,12 +1566,14 @@ __device__ __noinline__ bool warp_gn_step(FitState* st, SolverSmem& S, const dou
     st->branch = -1;
     st->phase = PH_TRIAL_J;
   }
+  for (int k = lane; k < tri_count(n) + 1; k += 32) st->kv[k] = kv[k];  // (the K-vector, lane-parallel)
   if (lane < n) {
     st->g[lane] = gj;
     st->scale_inv[lane] = si;
     st->d[lane] = dd;
     st->diag_h[lane] = 0.0;
     st->gh[lane] = S.w3[lane];
+#pragma unroll
     for (int j = 0; j < n; ++j) {
       const int a = lane < j ? lane : j, b = lane < j ? j : lane;
       st->G[lane * NMAX + j] = kv[tri_slot(n, a, b)];
