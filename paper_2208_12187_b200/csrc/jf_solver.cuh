@@ -1388,35 +1388,38 @@ __device__ __noinline__ bool warp_gn_step(FitState* st, SolverSmem& S, const dou
 #if JF_DEV  // development: cycles of the phases (prof[1] decide + g/G, [4] B_hat + Cholesky, [6] solves, [7] pred + commit)
   long long dq0 = clock64(), dq1 = 0, dq2 = 0, dq3 = 0;
 #endif
-  const int phase = st->phase;
+  // (the gating fields read together, ahead of the first branch)
+  const int phase = st->phase, bounded = st->bounded, policy = st->policy, trace_cap = st->trace_cap;
+  const int qr_mode = st->qr_mode, status0 = st->status, nfev0 = st->nfev, max_nfev = st->max_nfev;
+  const int auto_mode = st->auto_mode;
+  const double cost = st->cost, pred_old = st->pred, Delta = st->Delta, hn_old = st->hn, ftol = st->ftol,
+               xtol = st->xtol, step_norm = st->step_norm, kappa2_gn = st->kappa2_gn, alpha0 = st->alpha;
+  const double kv_flag = kv[tri_count(n)], kv_rr = kv[tri_slot(n, n, n)];
   const bool init = (phase == PH_INIT_J);
-  if ((phase != PH_TRIAL_J && !init) || st->bounded || st->policy != 0 || st->trace_cap > 0 ||
-      (init ? st->qr_mode == 1 : (st->qr_mode != 0 || st->status != STATUS_NONE)))
+  if ((phase != PH_TRIAL_J && !init) || bounded || policy != 0 || trace_cap > 0 ||
+      (init ? qr_mode == 1 : (qr_mode != 0 || status0 != STATUS_NONE)))
     return false;
-  if (kv[tri_count(n)] != 0.0) return false;  // R17 / R18 paths
-  const double cost_new = 0.5 * kv[tri_slot(n, n, n)];
+  if (kv_flag != 0.0) return false;  // R17 / R18 paths
+  const double cost_new = 0.5 * kv_rr;
   double ratio = 0.0, Delta_new = 0.0, alpha_new = 0.0;
   int nfev = 1;
   if (!init) {  // ---- st_after_trial (read-only)
-    const double cost = st->cost;
     const double actual = cost - cost_new;
-    const double pred_old = st->pred;
     if (pred_old > 0.0) ratio = actual / pred_old;
     else if (pred_old == 0.0 && actual == 0.0) ratio = 1.0;
     else ratio = 0.0;
-    const double Delta = st->Delta, hn_old = st->hn;
     Delta_new = Delta;
     if (ratio < 0.25) Delta_new = 0.25 * hn_old;
     else if (ratio > 0.75 && hn_old > 0.95 * Delta) Delta_new = 2.0 * Delta;
     const double xnorm = vnorm<n>(st->x);
-    const bool ft = actual < st->ftol * cost && ratio > 0.25;
-    const bool xt = st->step_norm < st->xtol * (st->xtol + xnorm);
+    const bool ft = actual < ftol * cost && ratio > 0.25;
+    const bool xt = step_norm < xtol * (xtol + xnorm);
     if (ft || xt || !(actual > 0.0)) return false;
-    nfev = st->nfev + 1;
-    if (st->auto_mode && !(st->kappa2_gn <= 1.0e6)) return false;  // AUTO re-check: general path
-    alpha_new = st->alpha * (Delta / Delta_new);
+    nfev = nfev0 + 1;
+    if (auto_mode && !(kappa2_gn <= 1.0e6)) return false;  // AUTO re-check: general path
+    alpha_new = alpha0 * (Delta / Delta_new);
   }
-  if (nfev == st->max_nfev) return false;
+  if (nfev == max_nfev) return false;
   // ---- the new iterate's g, G (from the K-vector) and scale (lane j: entry j)
   double gj = 0.0, gjj = 0.0, si = 1.0;
   if (lane < n) {
